@@ -1,0 +1,221 @@
+"""Seeded synthetic inputs shared by the oracle and the CUDA path.
+
+This module holds NONE of the method's arithmetic: it only describes the five
+synthetic scenes of BASELINE.json ``configs`` (SURVEY.md section 8(d), table
+d.1) as plain dicts, rounds them to the float32 values the device path sees,
+and draws seeded random debug records.  Both ``oracle/`` and
+``paper_2402_03106_b200/`` consume it; neither imports the other.
+
+Every scene stands in for the paper's mesh scenes (GLOSSY DRAGON, STAIRCASE,
+CORNELL BOX), which are not available; see DESIGN.md
+section 4 for the recipe.
+"""
+from __future__ import annotations
+
+import copy
+
+import numpy as np
+
+# R22 caps, R21 spp semantics, R29 direction modes, R8 table axes.
+CONFIGS = {
+    1: dict(
+        name="cfg1_infinite_detector",
+        sigma_s=0.9, sigma_a=0.1, g=0.0,
+        medium="infinite",
+        emitters=[((0.0, 0.0, 0.0), 0.0, 1.0)],
+        camera="detector", cam_pos=(2.0, 0.0, 0.0), det_radius=0.05,
+        width=1, height=1,
+        t0=2.0, t1=12.0, n_bins=128, warped=1,
+        spp=2048, spp_mode="cell", max_bounces=64, seed=0,
+        direction_mode="reuse",
+    ),
+    2: dict(
+        name="cfg2_sphere_unwarped",
+        sigma_s=4.75, sigma_a=0.25, g=0.5,
+        medium="sphere", center=(0.0, 0.0, 0.0), radius=1.0,
+        emitters=[((0.0, 0.0, -3.0), 0.0, 1.0)],
+        camera="pinhole", cam_pos=(0.0, 0.0, 4.0), fov_y_deg=40.0,
+        width=64, height=64,
+        t0=0.0, t1=20.0, n_bins=256, warped=0,
+        spp=16, spp_mode="cell", max_bounces=512, seed=1,
+        direction_mode="reuse",
+    ),
+    3: dict(
+        name="cfg3_slab_warped",
+        sigma_s=9.9, sigma_a=0.1, g=0.8,
+        medium="box", bmin=(-2.0, -2.0, 0.0), bmax=(2.0, 2.0, 1.0),
+        emitters=[((0.0, 0.0, -2.0), 0.0, 1.0)],
+        camera="pinhole", cam_pos=(0.0, 0.0, -2.0), fov_y_deg=60.0,
+        width=256, height=256,
+        t0=4.0, t1=40.0, n_bins=512, warped=1,
+        spp=64, spp_mode="cell", max_bounces=1024, seed=2,
+        direction_mode="split",
+    ),
+    4: dict(
+        name="cfg4_cube_walls_gate",
+        sigma_s=1.8, sigma_a=0.2, g=0.3,
+        medium="box", bmin=(-1.0, -1.0, -1.0), bmax=(1.0, 1.0, 1.0),
+        # faces: 0 -x, 1 +x, 2 -y, 3 +y, 4 -z (open front), 5 +z
+        wall_mask=0b101111, wall_albedo=(0.7, 0.7, 0.7, 0.7, 0.0, 0.7),
+        emitters=[((-0.5, 0.8, 0.0), 0.0, 1.0), ((0.5, 0.8, 0.0), 1.5, 1.0)],
+        camera="pinhole", cam_pos=(0.0, 0.0, -4.0), fov_y_deg=45.0,
+        width=512, height=512,
+        t0=6.0, t1=6.1, n_bins=1, warped=1,
+        spp=256, spp_mode="cell", max_bounces=128, seed=3,
+        direction_mode="reuse",
+    ),
+    5: dict(
+        name="cfg5_fogbox_warped",
+        sigma_s=19.98, sigma_a=0.02, g=0.9,
+        medium="box", bmin=(-5.0, -5.0, -5.0), bmax=(5.0, 5.0, 5.0),
+        emitters=[((0.0, 0.0, -6.0), 0.0, 1.0)],
+        camera="pinhole", cam_pos=(0.0, 0.0, -8.0), fov_y_deg=50.0,
+        width=1024, height=1024,
+        t0=0.0, t1=100.0, n_bins=1000, warped=1,
+        spp=1024, spp_mode="pixel", max_bounces=4096, seed=4,
+        direction_mode="split",
+    ),
+}
+
+_DEFAULTS = dict(
+    center=(0.0, 0.0, 0.0), radius=1.0, bmin=(0.0, 0.0, 0.0), bmax=(0.0, 0.0, 0.0),
+    wall_mask=0, wall_albedo=(0.0,) * 6, look_at=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0),
+    fov_y_deg=45.0, det_radius=0.0, strategy="darts", n_ris=8, alpha=0.5,
+    parity_r_excl=0.0, parity_s_excess=0.0, table_nr=16, table_ns=16,
+    crop=None, table_smin=None, table_smax=None,
+)
+
+
+def config(idx: int, **overrides) -> dict:
+    """Full scene dict for config ``idx`` (1..5) with defaults and overrides."""
+    c = copy.deepcopy(_DEFAULTS)
+    c.update(copy.deepcopy(CONFIGS[idx]))
+    c.update(overrides)
+    sigma_t = c["sigma_s"] + c["sigma_a"]
+    if c["table_smin"] is None:
+        c["table_smin"] = 1e-2 / sigma_t                     # R8
+    if c["table_smax"] is None:
+        c["table_smax"] = c["t1"] - min(e[1] for e in c["emitters"])
+    if c["crop"] is None:
+        c["crop"] = (0, 0, c["width"], c["height"])
+    return c
+
+
+def _f32(x):
+    return float(np.float32(x))
+
+
+def as_f32(c: dict) -> dict:
+    """Round every real scene parameter to float32 (what the device sees), so
+    the fp64 oracle integrates the identical scene."""
+    out = copy.deepcopy(c)
+    for k, v in c.items():
+        if isinstance(v, float):
+            out[k] = _f32(v)
+        elif isinstance(v, tuple) and v and all(isinstance(t, float) for t in v):
+            out[k] = tuple(_f32(t) for t in v)
+    out["emitters"] = [(tuple(_f32(t) for t in p), _f32(te), _f32(en)) for p, te, en in c["emitters"]]
+    return out
+
+
+def crop_center(c: dict, w: int, h: int) -> dict:
+    """Centre crop of w x h pixels (oracle sub-workloads)."""
+    out = dict(c)
+    x0 = (c["width"] - w) // 2
+    y0 = (c["height"] - h) // 2
+    out["crop"] = (x0, y0, x0 + w, y0 + h)
+    return out
+
+
+def small(c: dict, width: int, height: int, n_bins: int | None = None, t1: float | None = None) -> dict:
+    """A reduced-size variant of a config (same medium and geometry) for parity
+    runs the oracle finishes in seconds."""
+    out = dict(c)
+    out["width"], out["height"] = width, height
+    out["crop"] = (0, 0, width, height)
+    if n_bins is not None:
+        out["n_bins"] = n_bins
+    if t1 is not None:
+        out["t1"] = t1
+    return out
+
+
+# ----------------------------------------------------------------------------
+# seeded debug records: positions in the medium, E in [0, R_M),
+# random directions and raw 32-bit uniforms.
+def _unit(rng, n):
+    v = rng.normal(size=(n, 3))
+    return v / np.linalg.norm(v, axis=1, keepdims=True)
+
+
+def debug_records(c: dict, n: int, seed: int, kinds=("camera", "medium", "wall")) -> dict:
+    """Random vertex states for ``dts_sample_debug`` parity.  Returns a dict of
+    numpy arrays (kind, face, bin, emitter, x[n,3], w[n,3], E, beta, r[n,12])."""
+    rng = np.random.default_rng(seed)
+    kind = np.zeros(n, np.int32)
+    face = np.full(n, -1, np.int32)
+    x = np.zeros((n, 3))
+    w = _unit(rng, n)
+    names = {"camera": 0, "medium": 1, "wall": 2}
+    allowed = [names[k] for k in kinds]
+    if c["medium"] == "box" and c["wall_mask"] == 0 and 2 in allowed:
+        allowed.remove(2)
+    if c["medium"] != "box" and 2 in allowed:
+        allowed.remove(2)
+    kind[:] = rng.choice(allowed, size=n)
+    ne = len(c["emitters"])
+    emitter = rng.integers(0, ne, size=n).astype(np.int32)
+    b = rng.integers(0, c["n_bins"], size=n).astype(np.int32)
+    for i in range(n):
+        if kind[i] == 0:
+            if c["camera"] == "pinhole":
+                x[i] = c["cam_pos"]
+                tgt = rng.uniform(-0.5, 0.5, 3) * np.asarray(_extent(c))
+                d = tgt - np.asarray(c["cam_pos"])
+                w[i] = d / np.linalg.norm(d)
+            else:
+                x[i] = np.asarray(c["cam_pos"]) + _unit(rng, 1)[0] * c["det_radius"] * rng.uniform() ** (1 / 3)
+        elif kind[i] == 1:
+            x[i] = _inside(c, rng)
+        else:
+            faces = [f for f in range(6) if (c["wall_mask"] >> f) & 1]
+            f = int(rng.choice(faces))
+            face[i] = f
+            p = _inside(c, rng)
+            a = f // 2
+            p[a] = c["bmax"][a] if (f & 1) else c["bmin"][a]
+            x[i] = p
+    dt = (c["t1"] - c["t0"]) / c["n_bins"]
+    E = np.zeros(n)
+    for i in range(n):
+        te = c["emitters"][emitter[i]][1]
+        RM = c["t0"] + (b[i] + 1) * dt - te
+        C = np.linalg.norm(x[i] - np.asarray(c["emitters"][emitter[i]][0]))
+        if kind[i] != 0 and RM - C > 0:
+            E[i] = rng.uniform(0.0, RM - C)
+    r = rng.integers(0, 2**32, size=(n, 12), dtype=np.uint64).astype(np.uint32)
+    beta = np.ones(n)
+    return dict(kind=kind, face=face, bin=b, emitter=emitter, x=x, w=w, E=E, beta=beta, r=r)
+
+
+def _extent(c):
+    if c["medium"] == "sphere":
+        return (2 * c["radius"],) * 3
+    if c["medium"] == "box":
+        return tuple(c["bmax"][i] - c["bmin"][i] for i in range(3))
+    return (4.0, 4.0, 4.0)
+
+
+def _inside(c, rng):
+    if c["medium"] == "sphere":
+        u = _unit(rng, 1)[0] * c["radius"] * rng.uniform() ** (1 / 3)
+        return np.asarray(c["center"]) + u
+    if c["medium"] == "box":
+        return rng.uniform(np.asarray(c["bmin"]), np.asarray(c["bmax"]))
+    # infinite: around the emitter / detector region
+    return rng.uniform(-3.0, 3.0, 3)
+
+
+def n_cells(c: dict) -> int:
+    x0, y0, x1, y1 = c["crop"]
+    return (x1 - x0) * (y1 - y0) * c["n_bins"]

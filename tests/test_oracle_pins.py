@@ -1,0 +1,599 @@
+"""Pins of the fp64 oracle against things other than itself (no GPU needed).
+
+Every test names the passage it pins.  PAPER.md line numbers; readings R#
+are DESIGN.md section 3.  Closed forms, library routines (cuRAND's host
+Philox, numpy Gauss-Legendre, scipy adaptive quadrature), invariants and
+special cases -- never a retyping of the oracle's own formula.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import integrate, special, stats
+
+import dts_inputs as I
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- RNG (R24)
+def _kat():
+    rows = []
+    with open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                v = [int(x, 16) for x in line.split()]
+                rows.append((v[:4], v[4:6], v[6:10]))
+    return rows
+
+
+def test_philox_known_answer_vectors(oracle):
+    for ctr, key, out in _kat():
+        assert oracle.philox(ctr, key) == out
+
+
+def test_philox_matches_curand_host_generator(oracle):
+    """cuRAND's host PHILOX4_32_10 generator (an independent implementation)
+    emits block i = philox(ctr=(0, 0, i, 0), key=seed) for its first 4096
+    blocks (one subsequence per block)."""
+    path = "/usr/local/cuda/lib64/libcurand.so"
+    if not os.path.exists(path):
+        pytest.skip("libcurand not present")
+    cur = ctypes.CDLL(path)
+    for seed in (0, 1, 4, 0xDEADBEEF12345678):
+        gen = ctypes.c_void_p()
+        assert cur.curandCreateGeneratorHost(ctypes.byref(gen), 161) == 0
+        assert cur.curandSetPseudoRandomGeneratorSeed(gen, ctypes.c_ulonglong(seed)) == 0
+        out = np.zeros(64, np.uint32)
+        assert cur.curandGenerate(gen, out.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(64)) == 0
+        cur.curandDestroyGenerator(gen)
+        mine = []
+        for i in range(16):
+            mine += oracle.philox([0, 0, i, 0], [seed & 0xFFFFFFFF, seed >> 32])
+        assert mine == [int(x) for x in out]
+
+
+def test_uniform_mapping_never_one(oracle):
+    assert oracle.uniform(0) == 0.0
+    assert oracle.uniform(0xFFFFFFFF) == (2**24 - 1) / 2**24 < 1.0
+    assert oracle.uniform(0x80000000) == 0.5
+
+
+# ---------------------------------------------------------------- Sobol (R6)
+def test_sobol_table_is_van_der_corput(oracle):
+    # first points of Sobol dimension 0: 0, 1/2, 1/4, 3/4, 1/8, 5/8, 3/8, 7/8
+    assert [oracle.sobol(0, i) for i in range(8)] == [0, .5, .25, .75, .125, .625, .375, .875]
+    # each 8-point row holds exactly one point per 1/8 stratum (what makes the
+    # "pre-computed table prevents clustering" claim of PAPER.md:240 true)
+    for r in range(32):
+        row = [oracle.sobol(r, i) for i in range(8)]
+        assert sorted(int(8 * v) for v in row) == list(range(8))
+        assert all(0.0 <= v < 1.0 for v in row)
+
+
+# ---------------------------------------------------------------- DA fluence (E9)
+@pytest.mark.parametrize("cfg", [1, 2, 5])
+@pytest.mark.parametrize("dt", [0.05, 1.0, 7.5])
+def test_da_flux_spatial_integral(oracle, cfg, dt):
+    """int Phi dV = exp(-sigma_a dt): the Green's function of the transient
+    diffusion equation conserves energy up to absorption."""
+    c = I.config(cfg)
+    D = 1.0 / (3 * (c["sigma_a"] + c["sigma_s"] * (1 - c["g"])))
+    rmax = 12 * math.sqrt(4 * D * dt)
+    val, _ = integrate.quad(lambda r: 4 * math.pi * r * r * oracle.da_flux(c, r * r, dt), 0, rmax,
+                            epsabs=0, epsrel=1e-12, limit=200)
+    assert val == pytest.approx(math.exp(-c["sigma_a"] * dt), rel=1e-6)
+
+
+def test_da_flux_heaviside_and_peak(oracle):
+    c = I.config(1, sigma_a=0.0)
+    assert oracle.da_flux(c, 0.0, 0.0) == 0.0
+    assert oracle.da_flux(c, 1.0, -1.0) == 0.0
+    D = 1.0 / (3 * c["sigma_s"])
+    assert oracle.da_flux(c, 0.0, 2.0) == pytest.approx((4 * math.pi * D * 2.0) ** -1.5, rel=1e-14)
+
+
+# ---------------------------------------------------------------- HG
+@pytest.mark.parametrize("g", [-0.7, 0.0, 0.3, 0.5, 0.8, 0.9])
+def test_hg_normalisation(oracle, g):
+    val, _ = integrate.quad(lambda mu: 2 * math.pi * oracle.hg_eval(g, mu), -1, 1, epsrel=1e-12, limit=400)
+    assert val == pytest.approx(1.0, abs=1e-9)
+    assert oracle.hg_eval(0.0, 0.3) == pytest.approx(1 / (4 * math.pi), rel=1e-15)
+
+
+@pytest.mark.parametrize("g", [0.0, 0.5, 0.9])
+def test_hg_sampling_chi_square(oracle, g):
+    rng = np.random.default_rng(7)
+    u = rng.random(100_000)
+    mu = np.array([oracle.hg_sample_cos(g, x) for x in u])
+    edges = np.linspace(-1, 1, 41)
+    obs, _ = np.histogram(mu, edges)
+    exp = np.array([integrate.quad(lambda m: 2 * math.pi * oracle.hg_eval(g, m), a, b)[0]
+                    for a, b in zip(edges[:-1], edges[1:])]) * len(u)
+    keep = exp > 5
+    chi2 = ((obs[keep] - exp[keep]) ** 2 / exp[keep]).sum()
+    assert stats.chi2.sf(chi2, keep.sum() - 1) > 0.01
+
+
+# ---------------------------------------------------------------- ellipse (E18)
+def test_polar_distance_special_cases(oracle):
+    for S, C in [(3.0, 1.0), (2.0, 1.9), (5.0, 0.0)]:
+        assert oracle.polar_distance(C, S, 1.0) == pytest.approx((S + C) / 2, rel=1e-14)
+        assert oracle.polar_distance(C, S, -1.0) == pytest.approx((S - C) / 2, rel=1e-14)
+    assert oracle.polar_distance(0.0, 4.0, 0.123) == pytest.approx(2.0, rel=1e-15)
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        C = rng.uniform(0, 3)
+        S = C + rng.uniform(1e-3, 3)
+        mu = rng.uniform(-1, 1)
+        t = oracle.polar_distance(C, S, mu)
+        # |x_ell - x_k| + |x_ell - x_e| = S with x_e on the axis at distance C
+        r2 = math.sqrt(t * t - 2 * t * C * mu + C * C)
+        assert t + r2 == pytest.approx(S, rel=1e-12)
+
+
+# ---------------------------------------------------------------- geometry (R15)
+def test_intersections(oracle):
+    sph = I.config(2)
+    hit, lo, hi, _ = oracle.intersect(sph, (0, 0, 0), (0.6, 0.8, 0))
+    assert hit == 1 and lo == 0.0 and hi == pytest.approx(1.0)
+    hit, lo, hi, _ = oracle.intersect(sph, (0, 0, 4), (0, 0, -1))
+    assert (lo, hi) == (pytest.approx(3.0), pytest.approx(5.0))
+    assert oracle.intersect(sph, (0, 0, 4), (0, 0, 1))[0] == 3
+    box = I.config(4)
+    hit, lo, hi, face = oracle.intersect(box, (0, 0, -4), (0, 0, 1))
+    assert (lo, hi, face, hit) == (3.0, 5.0, 5, 2)          # enters the open -z face, exits the +z wall
+    hit, lo, hi, face = oracle.intersect(box, (0, 0, 0), (0, 0, -1))
+    assert (hit, face, hi) == (1, 4, 1.0)                    # open front face
+    assert oracle.intersect(I.config(1), (1, 2, 3), (0, 0, 1))[2] == math.inf
+
+
+# ---------------------------------------------------------------- Gauss-Legendre (R9)
+@pytest.mark.parametrize("n", [4, 8])
+def test_gauss_legendre_nodes(oracle, n):
+    x, w = oracle.gauss_legendre(n)
+    xr, wr = np.polynomial.legendre.leggauss(n)
+    np.testing.assert_allclose(x, xr, atol=1e-14)
+    np.testing.assert_allclose(w, wr, atol=1e-14)
+
+
+# ---------------------------------------------------------------- EDA table (E16-E18)
+def _e17_adaptive(c, C, S, mu):
+    """E17 by scipy adaptive quadrature over the FULL chord [0, t_M] (no
+    truncation, no panel split), using E9 through the oracle's Phi (pinned above)."""
+    st = c["sigma_s"] + c["sigma_a"]
+    tM = (S * S - C * C) / (2 * S - 2 * C * mu)
+    f = lambda t: c["sigma_s"] * math.exp(-st * t) * _phi(c, t * t - 2 * t * C * mu + C * C, S - t)
+    pts = [C * mu] if 0 < C * mu < tM else None
+    v, _ = integrate.quad(f, 0, tM, points=pts, epsabs=0, epsrel=1e-11, limit=500)
+    return v
+
+
+def _phi(c, r2, dt):
+    from oracle import oracle as O
+    return O.da_flux(c, r2, dt)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 5])
+def test_table_integrand_vs_adaptive_quadrature(oracle, cfg):
+    """R9's fixed rule (cut at 40/sigma_t, split at closest approach, 8 GL
+    panels) reproduces E17 to 1e-6 relative."""
+    c = I.config(cfg)
+    rng = np.random.default_rng(cfg)
+    for _ in range(12):
+        S = math.exp(rng.uniform(math.log(c["table_smin"] * 10), math.log(c["table_smax"])))
+        C = rng.uniform(0.02, 0.98) * S
+        mu = rng.uniform(-1, 1)
+        a = oracle.table_integrand(c, C, S, mu)
+        b = _e17_adaptive(c, C, S, mu)
+        assert a == pytest.approx(b, rel=1e-6, abs=1e-300)
+
+
+def test_table_integrand_isotropic_at_zero_focal_distance(oracle):
+    """C/S = 0: the ellipse is a sphere about the emitter, E17 cannot depend on
+    theta."""
+    c = I.config(2)
+    vals = [oracle.table_integrand(c, 0.0, 3.0, mu) for mu in np.linspace(-1, 1, 9)]
+    np.testing.assert_allclose(vals, vals[0], rtol=1e-12)
+
+
+@pytest.fixture(scope="module")
+def table_cfg2(oracle):
+    c = I.as_f32(I.config(2))
+    q, mass = oracle.build_table(c)
+    return c, q, mass
+
+
+def test_table_cdf_invariants(table_cfg2):
+    c, q, mass = table_cfg2
+    q = q.reshape(-1, 256).astype(np.int64)
+    mass = mass.reshape(-1, 256)
+    assert (q[:, 0] == 0).all()
+    assert (np.diff(q, axis=1) >= 0).all()                                # monotone CDF
+    np.testing.assert_allclose(mass.sum(1), 1.0, rtol=1e-12)             # terminal CDF = 1
+    # quantisation: q_j = round(65536 * CDF_j) (R10) within half a quantum
+    cdf = np.concatenate([np.zeros((len(mass), 1)), np.cumsum(mass, 1)[:, :-1]], 1)
+    assert np.abs(q - np.minimum(65536 * cdf, 65535)).max() <= 0.5 + 1e-6
+
+
+def test_table_cell_vs_adaptive_quadrature(oracle, table_cfg2):
+    """One cell's bin masses vs adaptive quadrature of E17 over each cos bin
+    (1e-3)."""
+    c, q, mass = table_cfg2
+    nr, ns = c["table_nr"], c["table_ns"]
+    for ir, is_ in [(3, 10), (13, 12), (15, 6)]:
+        ratio = (ir + 0.5) / nr
+        S = c["table_smin"] * (c["table_smax"] / c["table_smin"]) ** ((is_ + 0.5) / ns)
+        C = ratio * S
+        edges = np.linspace(-1, 1, 257)
+        sel = [0, 60, 128, 200, 250, 255]
+        ref = np.array([integrate.quad(lambda mu: _e17_adaptive(c, C, S, mu), edges[j], edges[j + 1],
+                                       epsrel=1e-9)[0] for j in sel])
+        got = mass.reshape(nr, ns, 256)[ir, is_, sel]
+        # normalise both by bin 128 (the full normalisation needs all 256 bins)
+        np.testing.assert_allclose(got / got[2], ref / ref[2], rtol=1e-3)
+
+
+# ---------------------------------------------------------------- debug-record helpers
+def _records(n, **fields):
+    rec = dict(kind=np.zeros(n, np.int32), face=np.full(n, -1, np.int32), bin=np.zeros(n, np.int32),
+               emitter=np.zeros(n, np.int32), x=np.zeros((n, 3)), w=np.zeros((n, 3)), E=np.zeros(n),
+               beta=np.ones(n), r=np.zeros((n, 12), np.uint32))
+    for k, v in fields.items():
+        rec[k][...] = v
+    return rec
+
+
+def _rand_words(rng, n):
+    return rng.integers(0, 2**32, size=(n, 12), dtype=np.uint64).astype(np.uint32)
+
+
+# ---------------------------------------------------------------- RIS (E12-E15)
+@pytest.mark.parametrize("case", ["infinite", "slab"])
+def test_ris_distance_estimator_unbiased(oracle, case):
+    """E[beta_ris * h(d*) * 1{medium event}] = int_{t_lo}^{t_hi} sigma_s e^{-sigma_t (d - t_lo)} h(d) dd
+    for any h supported where the DA target is positive (the causal ellipse,
+    R4).  Pins E13-E15 (candidate pdf, RIS weight, p_m of E12, sign of R1)."""
+    if case == "infinite":
+        c = I.config(1)
+        x = np.array([0.7, -0.4, 0.2])
+        w = np.array([0.3, 0.8, -0.52]); w /= np.linalg.norm(w)
+        b = 40
+    else:
+        c = I.config(3)
+        x = np.array([0.3, -0.2, 0.6])
+        w = np.array([0.1, 0.2, -0.97]); w /= np.linalg.norm(w)
+        b = 10
+    n = 400_000
+    rng = np.random.default_rng(3)
+    rec = _records(n, kind=0, bin=b, x=x, w=w, E=0.0)
+    rec["r"] = _rand_words(rng, n)
+    out = oracle.debug(c, None, rec)
+    st = c["sigma_s"] + c["sigma_a"]
+    dt = (c["t1"] - c["t0"]) / c["n_bins"]
+    RM = c["t0"] + (b + 1) * dt
+    xe = np.asarray(c["emitters"][0][0])
+    C = np.linalg.norm(xe - x)
+    mu = np.dot(w, xe - x) / C
+    dmax = (RM * RM - C * C) / (2 * RM - 2 * C * mu)      # causal iff d <= ellipse chord
+    hit, lo, hi, _ = oracle.intersect(c, x, w)
+    top = min(dmax, hi)
+    med = out["event"] == 1
+    d = out["d"]
+    for h in (lambda z: np.ones_like(z), lambda z: z, lambda z: np.exp(-2 * z) * (z < 0.5 * top)):
+        est = np.where(med, out["beta_ris"] * h(d), 0.0)
+        ref, _ = integrate.quad(lambda z: c["sigma_s"] * math.exp(-st * (z - lo)) * float(h(np.array(z))), lo, top,
+                                epsrel=1e-10, limit=200)
+        se = est.std() / math.sqrt(n)
+        assert abs(est.mean() - ref) < 3.5 * se, (est.mean(), ref, se)
+    # every resampled distance is causal (Fig. 4: invalid candidates get weight 0)
+    assert (d[med] <= dmax * (1 + 1e-12)).all()
+    # u = 0 -> d = t_lo, u -> 1 -> d -> t_hi (E14 endpoints, R1)
+    one = _records(2, kind=0, bin=b, x=x, w=w)
+    one["r"][:, 0] = 0
+    one["r"][0, 1] = one["r"][0, 2] = 0                   # row 0, shift 0 -> candidate 0 has u = 0
+    o1 = oracle.debug(c, None, one)
+    assert o1["cand_d"][0, 0] == pytest.approx(lo, abs=1e-15)
+
+
+def test_ris_selection_follows_weights(oracle):
+    """The resampled index is distributed as w_i / sum w (CDF inversion in
+    candidate order): chi-square over identical candidate sets."""
+    c = I.config(1)
+    n = 200_000
+    rng = np.random.default_rng(5)
+    rec = _records(n, kind=0, bin=60, x=(1.2, 0.3, 0.0), w=(0.0, 0.6, 0.8))
+    words = np.tile(rng.integers(0, 2**32, size=12, dtype=np.uint64).astype(np.uint32), (n, 1))
+    words[:, 3] = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)   # only u3 varies
+    rec["r"] = words
+    out = oracle.debug(c, None, rec)
+    wn = out["cand_wn"][0]
+    obs = np.bincount(out["istar"], minlength=8)
+    keep = wn * n > 5
+    chi2 = ((obs[keep] - n * wn[keep]) ** 2 / (n * wn[keep])).sum()
+    assert stats.chi2.sf(chi2, keep.sum() - 1) > 0.01
+
+
+# ---------------------------------------------------------------- direction MIS (E19)
+@pytest.mark.parametrize("cfg,ratio", [(2, 0.9), (2, 0.5), (5, 0.95), (4, 0.7)])
+def test_mixture_direction_estimator(oracle, cfg, ratio):
+    """E[p_HG(w)/p_mix(w) * h(w)] = E_HG[h] for the one-sample MIS; with the
+    Legendre addition theorem E_HG[P_l(w.a)] = g^l P_l(w_prev.a) in closed form.
+    Pins the EDA pdf normalisation, the mixture and gamma of E19."""
+    c = I.as_f32(I.config(cfg, direction_mode="reuse"))
+    q, _ = oracle.build_table(c)
+    g = c["g"]
+    b = c["n_bins"] - 1
+    dt = (c["t1"] - c["t0"]) / c["n_bins"]
+    xe = np.asarray(c["emitters"][0][0])
+    RM = c["t0"] + (b + 1) * dt - c["emitters"][0][1]
+    x = xe + np.array([0.3, -0.5, 0.8]) / np.linalg.norm([0.3, -0.5, 0.8]) * (0.5 * ratio * RM)
+    C = np.linalg.norm(x - xe)
+    S = C / ratio
+    E = RM - S
+    wprev = np.array([0.2, 0.9, -0.1]); wprev /= np.linalg.norm(wprev)
+    n = 400_000
+    rng = np.random.default_rng(11)
+    rec = _records(n, kind=1, bin=b, x=x, w=wprev, E=E)
+    rec["r"] = _rand_words(rng, n)
+    out = oracle.debug(c, q, rec)
+    assert out["gamma"][0] == pytest.approx(ratio / (ratio + 0.5), rel=1e-6)
+    assert 0.2 < (out["tech"] == 1).mean() < 0.8           # both techniques exercised
+    wt = out["beta_dir"]
+    om = out["ww"]
+    for a in [(xe - x) / C, np.array([1.0, 0, 0])]:
+        mu_a = om @ a
+        m0 = wprev @ a
+        for l, h in [(0, np.ones(n)), (1, mu_a), (2, 0.5 * (3 * mu_a ** 2 - 1))]:
+            est = wt * h
+            ref = g ** l * special.eval_legendre(l, m0)
+            se = est.std() / math.sqrt(n)
+            assert abs(est.mean() - ref) < 4 * se + 1e-12, (l, est.mean(), ref, se)
+
+
+def test_eda_sampling_follows_cell_cdf(oracle):
+    """With the EDA technique forced (u4 = 0), cos(theta) to the emitter axis is
+    distributed by the cell's tabulated masses; the returned pdf is the cell's
+    piecewise-constant density (PAPER.md:269 inverse-transform sampling)."""
+    c = I.as_f32(I.config(2, direction_mode="reuse"))
+    q, mass = oracle.build_table(c)
+    b = 200
+    dt = (c["t1"] - c["t0"]) / c["n_bins"]
+    xe = np.asarray(c["emitters"][0][0])
+    RM = c["t0"] + (b + 1) * dt
+    x = np.array([0.2, 0.1, -0.3])
+    C = np.linalg.norm(x - xe)
+    S = 1.25 * C
+    n = 300_000
+    rng = np.random.default_rng(2)
+    rec = _records(n, kind=1, bin=b, x=x, w=(0, 0, 1), E=RM - S)
+    rec["r"] = _rand_words(rng, n)
+    rec["r"][:, 4] = 0
+    out = oracle.debug(c, q, rec)
+    assert (out["tech"] == 1).all()
+    mu = out["ww"] @ ((xe - x) / C)
+    # the cell R10 picks for (C/S, S)
+    ir = int(math.floor(C / S * c["table_nr"]))
+    is_ = int(math.floor((math.log(S) - math.log(c["table_smin"])) /
+                         (math.log(c["table_smax"]) - math.log(c["table_smin"])) * c["table_ns"]))
+    qc = q.reshape(c["table_nr"], c["table_ns"], 256)[ir, is_].astype(np.float64)
+    pm = np.diff(np.append(qc, 65536.0)) / 65536.0
+    j = np.clip(np.floor((mu + 1) * 128).astype(int), 0, 255)
+    np.testing.assert_allclose(out["p_eda"], pm[j] * 128 / (2 * math.pi), rtol=1e-9)
+    obs = np.bincount(j, minlength=256)
+    keep = pm * n > 5
+    chi2 = ((obs[keep] - n * pm[keep]) ** 2 / (n * pm[keep])).sum()
+    assert stats.chi2.sf(chi2, keep.sum() - 1) > 0.01
+    # and the same cell is what the tabulated masses say (R8 bin centre values)
+    np.testing.assert_allclose(pm.sum(), 1.0, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- elliptical connection (E20-E22)
+def _conn_family(oracle, c, q, kind, x, w, E, b, m7):
+    n = len(m7)
+    rec = _records(n, kind=kind, bin=b, x=x, w=w, E=E)
+    rec["r"][:, 7] = (m7.astype(np.uint64) << 8).astype(np.uint32)
+    rec["r"][:, 4] = 0xFFFFFFFF      # u4 ~ 1: HG technique
+    rec["r"][:, 5] = 0xFFFFFFFF      # u5 ~ 1: HG cos ~ 1, the connection ray ~ w_prev
+    return oracle.debug(c, q, rec)
+
+
+@pytest.mark.parametrize("case", ["medium_vertex_cfg3", "camera_outside_cfg3", "medium_vertex_cfg4", "unwarped_camera_cfg2"])
+def test_connection_pdf_is_inverse_cdf_derivative(oracle, case):
+    """p_t returned with each sample equals d u / d t of the sampler's inverse
+    CDF: the density integrates to one over its support.  With
+    the printed Jacobian of E22 this fails (R2); with the derived one it holds."""
+    if case.endswith("cfg3"):
+        c = I.as_f32(I.config(3))
+    elif case.endswith("cfg4"):
+        c = I.as_f32(I.config(4))
+    else:
+        c = I.as_f32(I.config(2))
+    q, _ = oracle.build_table(c)
+    if case == "medium_vertex_cfg3":
+        kind, x, w, b, E = 1, np.array([0.2, -0.3, 0.1]), np.array([0.36, 0.48, 0.8]), 0, 0.1
+    elif case == "medium_vertex_cfg4":
+        kind, x, w, b, E = 1, np.array([0.2, -0.3, 0.4]), np.array([0.36, 0.48, 0.8]), 0, 4.5
+    else:
+        kind, x = 0, np.asarray(c["cam_pos"])
+        w = -x / np.linalg.norm(x) + np.array([0.05, 0.02, 0.0])
+        w /= np.linalg.norm(w)
+        E = 0.0
+        b = 10 if case.endswith("cfg3") else 40
+    m = np.arange(1 << 10, (1 << 24) - (1 << 10), 1 << 14, dtype=np.int64)
+    h = 1 << 9
+    o = _conn_family(oracle, c, q, kind, x, w, E, b, m)
+    assert o["conn_valid"].all(), "pick a state with a non-empty connection range"
+    op = _conn_family(oracle, c, q, kind, x, w, E, b, m + h)
+    om = _conn_family(oracle, c, q, kind, x, w, E, b, m - h)
+    dtdu = (op["t"] - om["t"]) / (2 * h / 2**24)
+    ratio = o["p_t"] * dtdu
+    smooth = np.abs(np.diff(o["t"], prepend=o["t"][0])) < 0.5   # skip the R17 interval switch
+    np.testing.assert_allclose(ratio[smooth], 1.0, rtol=2e-5)
+    # u7 = 0 -> S = S_lo (truncated exponential endpoint)
+    z = _conn_family(oracle, c, q, kind, x, w, E, b, np.array([0]))
+    if not case.startswith("unwarped"):
+        assert z["S"][0] == pytest.approx(z["S_lo"][0], rel=1e-15)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_connections_land_in_their_bin(oracle, cfg):
+    """Exact length control: every connection the oracle makes has
+    recorded time in [T_m, T_M), and |x_ell - x_k| + |x_ell - x_e| = S."""
+    c = I.as_f32(I.config(cfg))
+    q, _ = oracle.build_table(c)
+    rec = I.debug_records(c, 20_000, seed=cfg)
+    out = oracle.debug(c, q, rec)
+    v = out["conn_valid"] == 1
+    assert v.mean() > 0.05
+    dt = (c["t1"] - c["t0"]) / c["n_bins"]
+    te = np.array([c["emitters"][e][1] for e in rec["emitter"]])
+    xe = np.array([c["emitters"][e][0] for e in rec["emitter"]])
+    Tm = c["t0"] + rec["bin"] * dt
+    TM = Tm + dt
+    r2 = np.linalg.norm(xe - out["x_ell"], axis=1)
+    unw = (rec["kind"] == 0) & (c["warped"] == 0)
+    tcam = np.linalg.norm(out["x_ell"] - rec["x"], axis=1)
+    T = np.where(unw, te + rec["E"] + r2, te + rec["E"] + tcam + r2)
+    assert (T[v] >= Tm[v] - 1e-9).all() and (T[v] < TM[v] + 1e-9).all()
+    w = ~unw & v
+    np.testing.assert_allclose(tcam[w] + r2[w], out["S"][w], rtol=1e-10)
+    np.testing.assert_allclose(tcam[v], out["t"][v], rtol=1e-10)
+
+
+# ---------------------------------------------------------------- end-to-end closed forms (config 1)
+def _ball_single_scatter(c, edges):
+    """Bin-integrated, ball-averaged order-1 fluence: phi_1(R,t) =
+    sigma_s e^{-sigma_t t} ln((t+R)/(t-R)) / (4 pi R t) for a unit isotropic
+    pulse (prolate-spheroidal integral), averaged over the
+    detector ball (spherical-cap area pi R (a^2-(R-L)^2)/L)."""
+    ss, st = c["sigma_s"], c["sigma_s"] + c["sigma_a"]
+    L, a = 2.0, c["det_radius"]
+    xr, wr = np.polynomial.legendre.leggauss(48)
+    Rs = L + a * xr
+    ws = a * wr * np.pi * Rs * (a * a - (Rs - L) ** 2) / L / (4 / 3 * np.pi * a ** 3)
+    out = np.zeros(len(edges) - 1)
+    for R, wR in zip(Rs, ws):
+        f = lambda t: ss * math.exp(-st * t) * math.log((t + R) / (t - R)) / (4 * math.pi * R * t)
+        for j, (lo, hi) in enumerate(zip(edges[:-1], edges[1:])):
+            lo2 = max(lo, R)
+            if hi > lo2:
+                out[j] += wR * integrate.quad(f, lo2, hi, limit=100)[0]
+    return out
+
+
+@pytest.fixture(scope="module")
+def cfg1_runs(oracle):
+    c = I.as_f32(I.config(1))
+    q, _ = oracle.build_table(c)
+    runs = [oracle.render(c, q, 2048, seed, n_orders=1, sq=False) for seed in range(100, 108)]
+    return c, q, runs
+
+
+def test_single_scatter_closed_form(cfg1_runs):
+    c, q, runs = cfg1_runs
+    edges = np.linspace(c["t0"], c["t1"], c["n_bins"] + 1)
+    ref = _ball_single_scatter(c, edges)
+    o1 = np.array([r["order_hist"][0, 0, 0] for r in runs])
+    m, se = o1.mean(0), o1.std(0, ddof=1) / math.sqrt(len(o1))
+    z = (m - ref) / se
+    assert np.mean(np.abs(z[1:]) < 3) >= 0.97, z
+    # aggregate over bins 1..127 to 0.5 %
+    assert m[1:].sum() == pytest.approx(ref[1:].sum(), rel=5e-3)
+
+
+def test_multiple_scattering_tail_vs_diffusion(oracle, cfg1_runs):
+    """Total response at t in [6, 12) vs the E9 Green's function at R = 2:
+    the diffusion approximation is accurate there to ~7 %."""
+    c, q, runs = cfg1_runs
+    h = np.mean([r["hist"][0, 0] for r in runs], axis=0)
+    edges = np.linspace(c["t0"], c["t1"], c["n_bins"] + 1)
+    sel = edges[:-1] >= 6.0
+    da = np.array([integrate.quad(lambda t: oracle.da_flux(c, 4.0, t), a, b)[0]
+                   for a, b in zip(edges[:-1][sel], edges[1:][sel])])
+    ratio = h[sel].sum() / da.sum()
+    assert 0.88 < ratio < 1.08, ratio
+
+
+def test_absorption_factorisation(oracle):
+    """Infinite medium: every path of duration t carries e^{-sigma_a t}, so
+    H_{sa}[b] = e^{-(sa - sa') t_b} H_{sa'}[b] (exact up to the bin width)."""
+    base = I.config(1)
+    res = {}
+    for sa in (0.1, 0.05):
+        c = I.as_f32(dict(base, sigma_a=sa))
+        q, _ = oracle.build_table(c)
+        res[sa] = np.array([oracle.render(c, q, 2048, s, sq=False)["hist"][0, 0] for s in range(200, 206)])
+    edges = np.linspace(base["t0"], base["t1"], base["n_bins"] + 1)
+    mid = 0.5 * (edges[1:] + edges[:-1])
+    pred = np.exp(-0.05 * mid) * res[0.05].mean(0)
+    a = res[0.1].mean(0)
+    se = np.sqrt(res[0.1].var(0, ddof=1) / 6 + np.exp(-0.1 * mid) * res[0.05].var(0, ddof=1) / 6)
+    z = (a - pred) / se
+    assert np.mean(np.abs(z) < 3) >= 0.95
+    assert a.sum() == pytest.approx(pred.sum(), rel=1e-2)
+
+
+# ---------------------------------------------------------------- whole estimator: DARTS == vanilla
+XCHECK = [
+    ("cfg1", lambda: I.config(1, parity_r_excl=0.3, parity_s_excess=0.05), 8000, 160000),
+    ("cfg2_unwarped", lambda: dict(I.small(I.config(2, parity_s_excess=0.05), 1, 1, n_bins=16, t1=8.0),
+                                   fov_y_deg=10.0), 100000, 1000000),
+    ("cfg3_split", lambda: I.small(I.config(3, parity_s_excess=0.05), 3, 3, n_bins=8, t1=6.0), 4000, 40000),
+    ("cfg4_walls", lambda: I.small(I.config(4, parity_r_excl=0.3, parity_s_excess=0.05), 3, 3), 30000, 600000),
+    ("cfg5_split", lambda: I.small(I.config(5, parity_s_excess=0.05, spp_mode="cell"), 2, 2, n_bins=4, t1=12.0),
+     2000, 20000),
+]
+
+
+@pytest.mark.parametrize("name,mk,nd,nv", XCHECK, ids=[x[0] for x in XCHECK])
+def test_darts_equals_vanilla(oracle, name, mk, nd, nv):
+    """PAPER.md:340 "verified to converge to the same results": DARTS (RIS
+    distance, EDA+HG direction, elliptical connection from every vertex incl.
+    the camera, R13) and the vanilla estimator (exponential flight, phase
+    sampling, direct shadow connection) estimate the same restricted
+    transient integral; >= 99 % of cells within 3 SE (one allowed outlier)."""
+    c = I.as_f32(mk())
+    q, _ = oracle.build_table(c)
+    d = oracle.render(c, q, nd, 11)
+    v = oracle.render(dict(c, strategy="vanilla"), None, nv, 12)
+    hd, hv = d["hist"], v["hist"]
+    sed = np.sqrt(np.maximum(d["hist_sq"] - hd ** 2, 0) / (nd - 1))
+    sev = np.sqrt(np.maximum(v["hist_sq"] - hv ** 2, 0) / (nv - 1))
+    m = (hd > 0) | (hv > 0)
+    z = ((hd - hv) / np.sqrt(sed ** 2 + sev ** 2 + 1e-300))[m]
+    assert m.sum() >= 4
+    assert (np.abs(z) >= 3).sum() <= max(1, int(0.01 * m.sum())), z
+    assert hd[m].sum() == pytest.approx(hv[m].sum(), rel=0.05)
+
+
+# ---------------------------------------------------------------- causality and determinism
+def test_causality_zero_bins(oracle):
+    """Bins before the minimal arrival are exactly zero: config 2
+    unwarped r2 >= 2; config 5 warped t >= 3 + 1."""
+    c = I.as_f32(I.small(I.config(2), 4, 4, n_bins=16, t1=8.0))
+    q, _ = oracle.build_table(c)
+    h = oracle.render(c, q, 200, 1)["hist"]
+    assert (h[..., :4] == 0).all() and h[..., 4:].sum() > 0
+    c = I.as_f32(I.small(I.config(5, spp_mode="cell"), 2, 2, n_bins=8, t1=8.0))
+    q, _ = oracle.build_table(c)
+    h = oracle.render(c, q, 50, 1)["hist"]
+    assert (h[..., :4] == 0).all() and h[..., 4:].sum() > 0
+
+
+def test_sharding_and_determinism(oracle):
+    """Disjoint Philox key ranges: two half renders sum to the full render; the
+    same seed reproduces it."""
+    c = I.as_f32(I.small(I.config(4), 4, 4))
+    q, _ = oracle.build_table(c)
+    full = oracle.render(c, q, 64, 9)
+    a = oracle.render(c, q, 64, 9, 0, 23)
+    b = oracle.render(c, q, 64, 9, 23, 64)
+    np.testing.assert_allclose(a["hist"] + b["hist"], full["hist"], rtol=1e-12, atol=1e-300)
+    again = oracle.render(c, q, 64, 9, nthreads=3)
+    np.testing.assert_allclose(again["hist"], full["hist"], rtol=1e-12)
+    assert a["stats"]["paths"] + b["stats"]["paths"] == full["stats"]["paths"]
