@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the DARTS hot path on B200 (BASELINE.json metric: path
+vertices/s at 1/2/4/8 GPUs, as % of the FP32/SFU issue roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1)
+
+One step = one complete render of the workload: zero the histogram, build the
+EDA table (dts_table_build), render this rank's Philox sample range
+(dts_render), and for N > 1 one NCCL reduce of the histograms to rank 0.
+Strong scaling: the total work (config 5: 1024 spp per pixel) is split across
+ranks by disjoint sample ranges.  Rank 0 prints ONE JSON line.
+
+--impl reference times the fp64 CPU oracle (the only reference this paper
+has) on a bounded sample of the same workload, on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import dts_inputs as I  # noqa: E402
+
+# algorithmic thread-instructions per DARTS vertex
+# (REUSE 610; SPLIT adds an HG sample and a second intersection, +40).
+ALG_INSTR_PER_VERTEX = {"reuse": 610, "split": 650}
+# issue roofline: 148 SMs x 4 SMSPs x 32 lanes x 1 warp-instruction / clock
+SMS, SMSP, LANES = 148, 4, 32
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _shard(spp: int, rank: int, world: int):
+    return spp * rank // world, spp * (rank + 1) // world
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_03106_b200 import dts
+
+    world, rank, local = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = I.as_f32(I.config(args.config))
+    if args.direction_mode:
+        c["direction_mode"] = args.direction_mode
+    spp = c["spp"]
+    sb, se = _shard(spp, rank, world)
+    sc = dts.Scene(c)
+    shape = sc.hist_shape()
+    hist = torch.zeros(shape, dtype=torch.float32, device="cuda")
+    ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    kern_ms = []
+
+    def step(i, timed):
+        hist.zero_()
+        sc.table_build(stream=stream)
+        if timed:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        sc.render(spp, c["seed"] + 1000 * i, sb, se, hist, None, ctr if timed else None, stream)
+        if timed:
+            e1.record(stream)
+            kern_ms.append((e0, e1))
+        if world > 1:
+            dist.reduce(hist, dst=0)
+
+    for i in range(args.warmup):
+        step(i, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctr.zero_()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i, True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    kms = [a.elapsed_time(b) for a, b in kern_ms]
+    kern_avg = sum(kms) / len(kms)
+    launch = dts.last_launch()
+    # max over ranks of the step time; sum of counters over ranks
+    if world > 1:
+        tt = torch.tensor([ms, kern_avg], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, kern_avg = float(tt[0]), float(tt[1])
+        dist.all_reduce(ctr, op=dist.ReduceOp.SUM)
+    counts = dts.counters_dict(ctr)
+    verts_per_step = counts["vertices"] / args.steps
+    paths_per_step = counts["paths"] / args.steps
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), N GPUs
+    e2e = run_e2e(args, c, sc, world, rank, stream, torch, dist, dts)
+
+    if rank == 0:
+        peaks = _peaks()
+        sm_max = peaks.get("sm_max_mhz", 1965.0)
+        mode = c["direction_mode"]
+        alg = ALG_INSTR_PER_VERTEX[mode]
+        peak_tips = SMS * SMSP * LANES * sm_max * 1e6 / 1e12      # Tinst/s at the max SM clock
+        # the dominant kernel is the render kernel: per-rank vertices / its launch time
+        achieved = (verts_per_step / world) * alg / (kern_avg * 1e-3) / 1e12
+        value = verts_per_step / (ms / args.steps * 1e-3)
+        traffic = _profile_traffic(args.config)
+        clocks = clk.summary()
+        line = {
+            "metric": "path vertices/s (DARTS transient volumetric PT)",
+            "value": value,
+            "unit": "vertices/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded Philox paths; analytic scene of BASELINE.json config)",
+            "config": {
+                "workload": c["name"], "config_index": args.config, "pixels": c["width"] * c["height"],
+                "bins": c["n_bins"], "spp": spp, "spp_mode": c["spp_mode"], "direction_mode": mode,
+                "paths_per_step": paths_per_step, "vertices_per_step": verts_per_step,
+                "parallelism": f"sample-range shards x{world}" + (" + NCCL reduce" if world > 1 else ""),
+                "l2": "histogram (%.2f GB) > L2 is re-zeroed every step" % (hist.numel() * 4 / 1e9),
+            },
+            "paths_per_s": paths_per_step / (ms / args.steps * 1e-3),
+            "roofline": {
+                "bound": "alu", "achieved": achieved, "peak": peak_tips, "unit": "Tinst/s",
+                "frac": achieved / peak_tips, "traffic": traffic,
+                "basis": f"{alg} algorithmic thread-instructions per vertex (SURVEY 8d.2) x vertices / "
+                         f"render-kernel time; peak = 148 SM x 4 issue x 32 lanes x {sm_max:.0f} MHz",
+                "kernel_ms": kern_avg,
+            },
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps * world,
+            "launch": launch,
+            "counters": counts,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts):
+    """Same metric through the public API with host buffers: per step the host
+    scene description goes in (dts_scene_create + dts_table_build), the
+    histogram comes back to pinned host memory."""
+    cells = sc.hist_cells()
+    host = torch.empty(cells, dtype=torch.float32, pin_memory=True)
+    hnp = host.numpy()
+    hctr = np.zeros(dts.NUM_COUNTERS, np.uint64)
+    spp = c["spp"]
+    sb, se = _shard(spp, rank, world)
+    dev_hist = torch.zeros(sc.hist_shape(), dtype=torch.float32, device="cuda") if world > 1 else None
+    verts = 0
+    ksteps = max(1, min(args.steps, 2))
+    for i in range(ksteps + 1):
+        timed = i > 0
+        if timed and i == 1:
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+        s2 = dts.Scene(c)
+        s2.table_build(stream=stream)
+        if world == 1:
+            s2.render_host(spp, c["seed"] + 7 * i, sb, se, hnp, hctr, stream)
+            if timed:
+                verts += int(hctr[2])
+        else:
+            dev_hist.zero_()
+            ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+            s2.render(spp, c["seed"] + 7 * i, sb, se, dev_hist, None, ctr, stream)
+            dist.reduce(dev_hist, dst=0)
+            dist.all_reduce(ctr)
+            if rank == 0:
+                host.copy_(dev_hist.view(-1), non_blocking=True)
+            torch.cuda.synchronize()
+            if timed:
+                verts += int(ctr[2].item())
+        s2.close()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt[0])
+    import ctypes
+    return {"value": verts / el, "unit": "vertices/s", "steps": ksteps,
+            "h2d_bytes_per_step": ctypes.sizeof(dts.SceneDesc),
+            "d2h_bytes_per_step": cells * 4 + (8 * dts.NUM_COUNTERS if world == 1 else 0),
+            "timing": "host wall clock (perf_counter) around scene_create..histogram in pinned host memory, max over ranks"}
+
+
+def _profile_traffic(cfg):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(str(cfg))
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------------------- CPU oracle (cpu_baseline / reference arm)
+def _oracle_sample(cfg_idx, crop_w, crop_h):
+    from oracle import oracle as O
+    c = I.as_f32(I.config(cfg_idx))
+    c = I.crop_center(c, crop_w, crop_h)
+    q = O.build_table(c)[0] if c["strategy"] == "darts" else None
+    t = time.perf_counter()
+    r = O.render(c, q, c["spp"], c["seed"], sq=False, nthreads=os.cpu_count())
+    el = time.perf_counter() - t
+    return r["stats"], el, c
+
+
+def cpu_baseline(cfg_idx, budget_s=15.0):
+    """The oracle as it stands on the host cores, on a bounded crop of the
+    same workload (every bin and sample of the crop's pixels)."""
+    w = 2
+    st, el, c = _oracle_sample(cfg_idx, w, w)
+    # grow the crop until the sample costs about budget_s
+    while el < budget_s / 2 and w < 256:
+        w2 = min(256, int(w * max(1.5, min(4.0, math.sqrt(budget_s / max(el, 1e-3) / 1.5)))))
+        if w2 * w2 * (el / (w * w)) > 2.5 * budget_s:
+            break
+        w = w2
+        st, el, c = _oracle_sample(cfg_idx, w, w)
+    return {"value": st["vertices"] / el, "unit": "vertices/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{c['name']} centre crop {w}x{w} px, all {c['n_bins']} bins, spp {c['spp']} "
+                      f"({st['paths']} paths, {st['vertices']} vertices) in {el:.1f} s, fp64",
+            "paths_per_s": st["paths"] / el}
+
+
+def run_reference(args):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        _oracle_sample(args.config, 2, 2)
+    tot_v, tot_t, last = 0, 0.0, None
+    w = 4
+    for _ in range(args.steps):
+        st, el, c = _oracle_sample(args.config, w, w)
+        tot_v += st["vertices"]
+        tot_t += el
+        last = (st, el, c)
+    value = tot_v / tot_t
+    st, el, c = last
+    line = {
+        "impl": "reference", "metric": "path vertices/s (DARTS transient volumetric PT)", "value": value,
+        "unit": "vertices/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c["name"], "config_index": args.config, "sample": f"centre crop {w}x{w}"},
+        "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": os.cpu_count(), "kind": "oracle",
+                         "sample": f"{c['name']} centre crop {w}x{w} px x all bins x spp {c['spp']} per step"},
+        "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--direction-mode", choices=["reuse", "split"], default=None)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

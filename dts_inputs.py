@@ -195,6 +195,10 @@ def debug_records(c: dict, n: int, seed: int, kinds=("camera", "medium", "wall")
             E[i] = rng.uniform(0.0, RM - C)
     r = rng.integers(0, 2**32, size=(n, 12), dtype=np.uint64).astype(np.uint32)
     beta = np.ones(n)
+    # the device stores positions/directions in float32: hand both sides the
+    # identical (float32-representable) values
+    x = x.astype(np.float32).astype(np.float64)
+    w = w.astype(np.float32).astype(np.float64)
     return dict(kind=kind, face=face, bin=b, emitter=emitter, x=x, w=w, E=E, beta=beta, r=r)
 
 

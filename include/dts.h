@@ -1,0 +1,212 @@
+/*
+ * dts.h -- C ABI of the B200-native DARTS hot path (libdts.so).
+ *
+ * DARTS: "Diffusion Approximated Residual Time Sampling for Time-of-flight
+ * Rendering in Homogeneous Scattering Media", arXiv 2402.03106.  Passages are
+ * cited as PAPER.md:<line> (the paper text; equations E1..E22 numbered in order
+ * of appearance) and readings R1..R29 of DESIGN.md section 3.
+ *
+ * One estimator is exposed: per-bin dedicated transient path tracing in a
+ * homogeneous medium.  Every path vertex
+ *   1. samples the free-path distance by RIS against transmittance x the
+ *      transient diffusion fluence for the residual time (E9-E15),
+ *   2. samples the direction from the EDA table mixed with Henyey-Greenstein
+ *      by one-sample MIS (E16-E19),
+ *   3. makes an elliptical connection to the pulse emitter that lands exactly
+ *      in the path's time bin (E20-E22),
+ *   4. splats into a pixel x time-bin histogram (camera-warped or unwarped,
+ *      PAPER.md:50, 76).
+ * A vanilla estimator (exponential flight, phase sampling, direct shadow
+ * connection) runs through the same kernels.
+ *
+ * Conventions (all calls):
+ *  - lengths are times: c = eta = 1 (E3).
+ *  - "device" pointers are CUDA global-memory pointers of the current device;
+ *    "host" pointers are ordinary (pageable or pinned) CPU memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Device-side calls are asynchronous on that stream unless stated.
+ *  - the library owns scene/table memory; the caller owns every buffer it
+ *    passes in.  Errors never abort: a status is returned and a thread-local
+ *    message is available from dts_last_error().  No call falls back to a CPU
+ *    path: a missing/unsupported device returns DTS_E_CUDA.
+ *  - one scene may be used by one stream at a time.
+ */
+#ifndef DTS_H
+#define DTS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DTS_ABI_VERSION 1
+#define DTS_MAX_EMITTERS 8
+#define DTS_TABLE_COS_BINS 256 /* "[-1, 1] is uniformly subdivided into 256 bins" */
+
+typedef struct dts_scene* dts_scene_t; /* opaque, library-owned */
+
+typedef enum {
+  DTS_OK = 0,
+  DTS_E_INVALID_ARG = 1, /* bad pointer, size or scene parameter */
+  DTS_E_STATE = 2,       /* e.g. dts_render(DARTS) before dts_table_build */
+  DTS_E_CUDA = 3,        /* CUDA runtime error / no usable sm_100 device */
+  DTS_E_OOM = 4,         /* device allocation failed */
+  DTS_E_RANGE = 5        /* sample range or work count out of range */
+} dts_status;
+
+enum { DTS_MEDIUM_INFINITE = 0, DTS_MEDIUM_SPHERE = 1, DTS_MEDIUM_BOX = 2 };
+enum { DTS_CAMERA_PINHOLE = 0, DTS_CAMERA_SPHERE_DETECTOR = 1 };
+enum { DTS_STRATEGY_DARTS = 0, DTS_STRATEGY_VANILLA = 1 };
+enum { DTS_DIR_REUSE = 0, DTS_DIR_SPLIT = 1 };     /* R29 */
+enum { DTS_SPP_PER_CELL = 0, DTS_SPP_PER_PIXEL = 1 }; /* R21 */
+
+/* Scene description.  Validation (dts_scene_create): sigma_s > 0, sigma_a >= 0,
+ * -1 < g < 1; 1 <= n_emitters <= 8; width, height >= 1; crop
+ * inside the image and non-empty; t1 > t0; n_bins >= 1; n_ris == 8;
+ * alpha >= 0 (E19); 1 <= max_bounces <= 65536; box bmax > bmin; radius > 0. */
+typedef struct {
+  float sigma_s, sigma_a, g; /* homogeneous medium, HG phase */
+  int32_t medium_shape;      /* DTS_MEDIUM_*; the medium is index-matched, vacuum outside */
+  float center[3], radius;   /* SPHERE */
+  float bmin[3], bmax[3];    /* BOX */
+  uint32_t wall_mask;        /* BOX faces that are Lambertian walls: bit f, f = 2*axis + (max side) */
+  float wall_albedo[6];
+  int32_t n_emitters;        /* isotropic point pulse emitters (Fig. 1) */
+  float em_pos[DTS_MAX_EMITTERS][3];
+  float em_t[DTS_MAX_EMITTERS];      /* emission start time tau_e */
+  float em_energy[DTS_MAX_EMITTERS]; /* pulse energy P_e (intensity P_e / 4 pi) */
+  int32_t camera_kind;               /* DTS_CAMERA_* (R18, R19) */
+  float cam_pos[3], look_at[3], up[3], fov_y_deg;
+  int32_t width, height;
+  float det_radius;                  /* SPHERE_DETECTOR: ball radius, centred at cam_pos */
+  int32_t crop[4];                   /* x0, y0, x1, y1 half-open: the rendered pixels */
+  float t0, t1;                      /* bins [t0 + b dt, t0 + (b+1) dt), dt = (t1-t0)/n_bins (R27) */
+  int32_t n_bins;
+  int32_t warped;                    /* 1: camera-warped (scene-to-sensor time counted, R16) */
+  int32_t strategy;                  /* DTS_STRATEGY_* */
+  int32_t n_ris;                     /* RIS candidates, must be 8 */
+  float alpha;                       /* E19 MIS preference, paper: 0.5 */
+  int32_t max_bounces;               /* connection vertices per path (R22) */
+  int32_t direction_mode;            /* DTS_DIR_* (R29) */
+  int32_t spp_mode;                  /* DTS_SPP_* (R21) */
+  float parity_r_excl;               /* TEST ONLY: drop contributions whose last segment < r (0 = off) */
+  float parity_s_excess;             /* TEST ONLY: require S - C >= eps for medium-last paths (0 = off) */
+} dts_scene_desc;
+
+/* EDA table axes (R8): n_ratio uniform bins of C/S in [0,1), n_s log-spaced
+ * bins of S in [s_min, s_max], 256 cos(theta) bins.  Zero fields take the
+ * defaults 16, 16, 0.01/sigma_t, t1 - min(tau_e). */
+typedef struct {
+  int32_t n_ratio, n_s;
+  float s_min, s_max;
+} dts_table_desc;
+
+/* Debug record: one DARTS vertex with caller-fixed state and raw Philox words.
+ * kind: 0 camera/detector vertex (k = 0, direction fixed = w), 1 medium vertex
+ * (w = incoming direction w_{k-1}), 2 wall vertex (face = wall index).
+ * u_i = (r_i >> 8) * 2^-24 (R24): u0 event, u1 Sobol row, u2 CP shift, u3 RIS
+ * select, u4 technique, u5 cos/bin, u6 phi, u7 connection, u8/u9 SPLIT walk. */
+typedef struct {
+  int32_t kind, face, bin, emitter;
+  float x[3], w[3];
+  double E;    /* elapsed (counted) path time at the vertex */
+  float beta;  /* throughput entering the vertex */
+  float pad_;
+  uint32_t r[12];
+} dts_debug_in;
+
+typedef struct {
+  int32_t tech;   /* 0 HG, 1 EDA, 2 camera (fixed), 3 wall cosine */
+  float gamma, p_eda, p_hg, p_mix;
+  float wc[3], ww[3]; /* connection direction, walk direction */
+  float beta_dir, wconn;
+  float t_lo, t_hi, tc_lo, tc_hi; /* medium interval along ww / wc */
+  int32_t hit, face_hit;          /* 0 none (infinite), 1 open boundary, 2 wall, 3 miss */
+  float S_lo, S_hi, S, t, x_ell[3], p_t, contrib, nee;
+  int32_t conn_valid;
+  float p_m;
+  int32_t event; /* 0 miss, 1 medium (RIS), 2 wall, 3 escape, 4 RIS all-invalid */
+  float cand_d[8], cand_wn[8];
+  int32_t istar;
+  float d, x_next[3], beta_ris;
+  double E_next;
+  float beta_out;
+  int32_t terminate;
+} dts_debug_out;
+
+/* Counters accumulated by dts_render into a caller device array of
+ * DTS_NUM_COUNTERS unsigned 64-bit integers. */
+enum {
+  DTS_CTR_PATHS = 0,       /* paths started (incl. camera misses) */
+  DTS_CTR_CAMERA_MISS,     /* primary ray misses the medium */
+  DTS_CTR_VERTICES,        /* vertex iterations (connection attempts) */
+  DTS_CTR_CONN_NONEMPTY,   /* connections with a non-empty S range */
+  DTS_CTR_RIS_INVALID,     /* walks ended by an all-invalid candidate set (R5) */
+  DTS_CTR_EARLY_EXIT,      /* walks ended by the E + C >= R_M bound */
+  DTS_CTR_ESCAPES,         /* walks that left the (convex) medium */
+  DTS_CTR_CAP_HITS,        /* walks truncated at max_bounces */
+  DTS_CTR_NONFINITE,       /* paths discarded for a non-finite contribution */
+  DTS_CTR_WALL_NEE,        /* non-zero wall NEE contributions */
+  DTS_NUM_COUNTERS
+};
+
+/* Creates a scene (validates, derives constants, allocates the table storage
+ * on the current device).  Synchronous.  *out is NULL on failure. */
+dts_status dts_scene_create(const dts_scene_desc* desc, dts_scene_t* out);
+/* Frees the scene; waits for its pending work.  NULL is a no-op. */
+dts_status dts_scene_destroy(dts_scene_t scene);
+
+/* Builds the EDA direction table of E17 on the device by the
+ * deterministic quadrature of R9 in fp64, quantised to 16-bit per-cell CDFs
+ * (R10).  desc may be NULL (defaults).  Asynchronous on stream. */
+dts_status dts_table_build(dts_scene_t scene, const dts_table_desc* desc, void* stream);
+/* Copies the quantised table (n_ratio*n_s*256 uint16, cell-major, cell =
+ * ir*n_s + is) to host memory.  Synchronous.  n must equal the table size. */
+dts_status dts_table_export(dts_scene_t scene, uint16_t* host_q, size_t n);
+/* Number of table entries (0 before dts_table_build). */
+size_t dts_table_size(dts_scene_t scene);
+
+/* Number of histogram cells: crop_w * crop_h * n_bins, layout [y][x][bin]
+ * (bin fastest) over the crop. */
+size_t dts_hist_cells(dts_scene_t scene);
+
+/* Renders samples s in [sample_begin, sample_end) of every crop pixel and
+ * every bin (SPP_PER_CELL: spp paths per (pixel, bin) cell; SPP_PER_PIXEL: spp
+ * paths per pixel, bin by R21; VANILLA: spp paths per pixel splatting into all
+ * bins).  Path identities -- and thus every random number -- depend only on
+ * (seed, s, pixel, bin), so disjoint sample ranges shard a render exactly.
+ * d_hist (device, dts_hist_cells floats) is ACCUMULATED (+=) with each path's
+ * contribution / (paths of its cell); d_hist_sq (device, nullable) accumulates
+ * contribution^2 / (paths of its cell); d_counters (device, nullable,
+ * DTS_NUM_COUNTERS uint64) accumulates the counters.  Asynchronous. */
+dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
+                      uint64_t sample_end, float* d_hist, float* d_hist_sq, uint64_t* d_counters,
+                      void* stream);
+
+/* End-to-end variant with HOST buffers: zeroes a library-owned device
+ * histogram, renders, and copies the result to h_hist (dts_hist_cells floats,
+ * OVERWRITTEN) and the counters to h_counters (nullable).  Synchronous. */
+dts_status dts_render_host(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
+                           uint64_t sample_end, float* h_hist, uint64_t* h_counters, void* stream);
+
+/* Runs one DARTS vertex per record with the SAME device functions the render
+ * kernel uses (direction, intersection, connection, RIS distance).  d_in/d_out
+ * are device arrays of n records.  Requires the table for medium vertices.
+ * Asynchronous. */
+dts_status dts_sample_debug(dts_scene_t scene, int32_t n, const dts_debug_in* d_in, dts_debug_out* d_out,
+                            void* stream);
+
+/* Kernel launches issued by the last dts_render on this thread (for the
+ * bench's gpu_launches count) and the launch geometry. */
+dts_status dts_last_launch(int32_t* n_launches, int32_t* grid, int32_t* block, int32_t* smem_bytes);
+
+const char* dts_status_string(dts_status s);
+const char* dts_last_error(void);
+int32_t dts_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DTS_H */

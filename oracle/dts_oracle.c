@@ -472,7 +472,12 @@ static double connect(const or_scene* sc, const derived* dv, const pstate* ps, c
         ma[i] = exp(-dv->sigma_t * (ia[i] - lo)) - exp(-dv->sigma_t * (ib[i] - lo));
       Z += ma[i];
     }
-    if (dbg) { dbg->S_lo = 0.0; dbg->S_hi = Z; dbg->m_conn = Z; }
+    if (dbg) {
+      dbg->S_lo = 0.0;
+      dbg->S_hi = Z;
+      dbg->m_conn = INFINITY; /* decision margin: distance of each interval from empty */
+      for (int i = 0; i < ni; ++i) dbg->m_conn = fmin(dbg->m_conn, fabs(ib[i] - ia[i]) / fmax(1.0, fabs(ib[i])));
+    }
     if (!(Z > 0.0)) return 0.0;
     double v = u7 * Z;
     int k = (ni == 2 && !(v < ma[0])) ? 1 : 0;
@@ -589,8 +594,7 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
       double cth = -1.0 + (j + frac) / 128.0;
       double phi = OR_PI * (2.0 * u6 - 1.0); /* R12: phi uniform in [-pi, pi) */
       from_frame(axis, cth, phi, om);
-      p_eda = (qb - qa) / 65536.0 * 128.0 / (2.0 * OR_PI);
-      mh = fmin(fabs(cth - (-1.0 + j / 128.0)), fabs(-1.0 + (j + 1) / 128.0 - cth)) * 128.0;
+      p_eda = (qb - qa) / 65536.0 * 128.0 / (2.0 * OR_PI); /* the bin j is the sampled one: no decision */
     } else {
       tech = 0;
       double cth = hg_sample_cos(sc->g, u5);

@@ -1,0 +1,641 @@
+// dts_device.cuh -- device stages of the DARTS hot path (sm_100a, fp32).
+//
+// One DARTS vertex = direction (EDA (+) HG one-sample MIS),
+// one analytic intersection reused by the connection and the walk
+// (PAPER.md:287), elliptical connection (E20-E22) and DA-RIS
+// free-path sampling (E9-E15).  The same functions serve the
+// persistent render kernel and the dts_sample_debug kernel (template DBG).
+// Readings R1..R29: DESIGN.md section 3.  Nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dts.h"
+
+namespace dts {
+
+constexpr float kPi = 3.14159265358979323846f;
+constexpr float kInv4Pi = 0.0795774715459476679f;
+constexpr float kLog2e = 1.44269504088896341f;
+constexpr float kLn2 = 0.693147180559945309f;
+
+enum { HIT_NONE = 0, HIT_OPEN = 1, HIT_WALL = 2, HIT_MISS = 3 };
+enum { KIND_CAMERA = 0, KIND_MEDIUM = 1, KIND_WALL = 2 };
+
+// Launch-uniform scene constants, passed by value as a kernel parameter (lives
+// in the constant bank: every lane reads the same address).
+struct DevScene {
+  float sigma_s, sigma_a, sigma_t, albedo, g, inv_sigma_t;
+  float hg_k;        // (1 - g^2) / (4 pi)
+  float hg_1pg2;     // 1 + g^2
+  float hg_2g;       // 2 g
+  float hg_1mg2;     // 1 - g^2
+  float hg_1mg;      // 1 - g
+  float hg_1pg;      // 1 + g
+  float neg_inv4D_log2e;   // -log2(e) / (4 D)
+  float neg_sa_log2e;      // -sigma_a log2(e)
+  int32_t medium_shape;
+  float center[3], radius2;
+  float bmin[3], bmax[3];
+  uint32_t wall_mask;
+  float wall_albedo[6];
+  int32_t n_emitters;
+  float em_pos[DTS_MAX_EMITTERS][3];
+  float em_t[DTS_MAX_EMITTERS];
+  float em_k[DTS_MAX_EMITTERS];  // P_e / (4 pi) * N_e
+  int32_t camera_kind;
+  float cam_pos[3], fwd[3], right[3], upc[3];
+  float tan_half, aspect;
+  int32_t width, height;
+  float det_radius;
+  int32_t crop[4];
+  double t0, dt;
+  int32_t n_bins, warped;
+  int32_t strategy, direction_mode, spp_mode, max_bounces;
+  float alpha;
+  float r_excl, s_excess;
+  // EDA table (R8-R10)
+  int32_t nr, ns;
+  float ln_smin, inv_dls;  // ns / (ln smax - ln smin)
+  uint32_t seed_lo, seed_hi;
+};
+
+// ----------------------------------------------------------------- vectors
+struct f3 {
+  float x, y, z;
+};
+__device__ __forceinline__ f3 mk(float x, float y, float z) { return f3{x, y, z}; }
+__device__ __forceinline__ f3 operator+(f3 a, f3 b) { return mk(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ f3 operator-(f3 a, f3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ f3 operator*(f3 a, float s) { return mk(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ float dot(f3 a, f3 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z)); }
+__device__ __forceinline__ f3 fma3(f3 d, float t, f3 o) { return mk(fmaf(d.x, t, o.x), fmaf(d.y, t, o.y), fmaf(d.z, t, o.z)); }
+__device__ __forceinline__ f3 ld3(const float* p) { return mk(p[0], p[1], p[2]); }
+
+// ----------------------------------------------------------------- RNG (R24)
+// Philox4x32-10 (Salmon et al. 2011); counter = (id_lo, id_hi, bounce, block).
+struct u4 {
+  uint32_t a, b, c, d;
+};
+__device__ __forceinline__ u4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                     uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return u4{c0, c1, c2, c3};
+}
+__device__ __forceinline__ float unif(uint32_t r) { return __uint2float_rn(r >> 8) * 5.9604644775390625e-08f; }
+
+// ----------------------------------------------------------------- accurate small-argument helpers
+// -ln(1 - x) for x in [0, 1): series below 1/32 (relative error < 1e-8),
+// MUFU lg2 above (relative error < 4e-6).
+__device__ __forceinline__ float neg_log1m(float x) {
+  const float big = -__log2f(1.0f - x) * kLn2;
+  const float ser = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 0.2f, 0.25f), 0.33333333f), 0.5f), 1.0f);
+  return x < 0.03125f ? ser : big;
+}
+// 1 - exp(-y) for y >= 0
+__device__ __forceinline__ float one_m_exp(float y) {
+  const float big = 1.0f - exp2f(-y * kLog2e);
+  const float ser = y * fmaf(-y, fmaf(-y, fmaf(-y, fmaf(-y, 1.0f / 120.0f, 1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
+  return y < 0.0625f ? ser : big;
+}
+__device__ __forceinline__ float fexp(float x) { return exp2f(x * kLog2e); }
+
+// ----------------------------------------------------------------- frames (R12)
+// Direction at polar angle theta about n: cos theta and sin theta are built
+// from opc = 1 + cos and omc = 1 - cos, each computed without cancellation by
+// the caller, so directions near the pole (HG with g = 0.9) keep fp32 accuracy.
+__device__ __forceinline__ f3 from_frame(f3 n, float opc, float omc, float phi) {
+  const float sign = copysignf(1.0f, n.z);
+  const float a = -1.0f / (sign + n.z);
+  const float b = n.x * n.y * a;
+  const f3 b1 = mk(1.0f + sign * n.x * n.x * a, sign * b, -sign * n.x);
+  const f3 b2 = mk(b, sign + n.y * n.y * a, -n.y);
+  const float cos_t = opc < omc ? opc - 1.0f : 1.0f - omc;
+  const float sin_t = sqrtf(fmaxf(0.0f, opc * omc));
+  float sp, cp;
+  __sincosf(phi, &sp, &cp);
+  const float cx = sin_t * cp, cy = sin_t * sp;
+  return mk(b1.x * cx + b2.x * cy + n.x * cos_t, b1.y * cx + b2.y * cy + n.y * cos_t,
+            b1.z * cx + b2.z * cy + n.z * cos_t);
+}
+
+// ----------------------------------------------------------------- HG
+__device__ __forceinline__ float hg_eval(const DevScene& S, float mu) {
+  const float den = fmaf(-S.hg_2g, mu, S.hg_1pg2);
+  const float r = rsqrtf(den);
+  return S.hg_k * r * r * r;
+}
+// HG inverse CDF (R25): returns 1 + cos and 1 - cos of the sampled angle.
+// With den = 1 - g + 2 g u and sq = (1 - g^2) / den (the textbook form
+// cos = (1 + g^2 - sq^2) / (2g)):
+//   1 - cos = (1 - g)(1 - u)(sq + 1 - g) / den,  1 + cos = (1 + g) u (sq + 1 + g) / den.
+__device__ __forceinline__ void hg_sample(const DevScene& S, float u, float& opc, float& omc) {
+  if (S.g == 0.0f) {
+    opc = 2.0f * (1.0f - u);
+    omc = 2.0f * u;
+    return;
+  }
+  const float den = fmaf(S.hg_2g, u, S.hg_1mg);
+  const float inv = __fdividef(1.0f, den);
+  const float sq = S.hg_1mg2 * inv;
+  omc = S.hg_1mg * (1.0f - u) * (sq + S.hg_1mg) * inv;
+  opc = S.hg_1pg * u * (sq + S.hg_1pg) * inv;
+}
+
+// ----------------------------------------------------------------- medium bounds (R15)
+__device__ __forceinline__ int intersect(const DevScene& S, f3 o, f3 d, float& lo, float& hi, int& face) {
+  face = -1;
+  if (S.medium_shape == DTS_MEDIUM_INFINITE) {
+    lo = 0.0f;
+    hi = __int_as_float(0x7f800000);
+    return HIT_NONE;
+  }
+  if (S.medium_shape == DTS_MEDIUM_SPHERE) {
+    const f3 oc = o - ld3(S.center);
+    const float b = dot(oc, d);
+    const float c = dot(oc, oc) - S.radius2;
+    const float disc = b * b - c;
+    if (!(disc > 0.0f)) return HIT_MISS;
+    const float s = sqrtf(disc);
+    const float tf = -b + s;
+    if (!(tf > 0.0f)) return HIT_MISS;
+    lo = fmaxf(-b - s, 0.0f);
+    hi = tf;
+    return HIT_OPEN;
+  }
+  float tn = -__int_as_float(0x7f800000), tf = __int_as_float(0x7f800000);
+  int ff = -1;
+  const float oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dd[a] == 0.0f) {
+      if (oo[a] < S.bmin[a] || oo[a] > S.bmax[a]) return HIT_MISS;
+      continue;
+    }
+    const float inv = 1.0f / dd[a];
+    const float t1 = (S.bmin[a] - oo[a]) * inv, t2 = (S.bmax[a] - oo[a]) * inv;
+    tn = fmaxf(tn, fminf(t1, t2));
+    const float far = fmaxf(t1, t2);
+    if (far < tf) {
+      tf = far;
+      ff = 2 * a + (dd[a] > 0.0f ? 1 : 0);
+    }
+  }
+  const float l = fmaxf(tn, 0.0f);
+  if (!(tf > l)) return HIT_MISS;
+  lo = l;
+  hi = tf;
+  face = ff;
+  return ((S.wall_mask >> ff) & 1u) ? HIT_WALL : HIT_OPEN;
+}
+
+// medium length and visibility of the segment p -> xe (p inside the medium)
+__device__ __forceinline__ float segment_tr(const DevScene& S, f3 p, f3 xe, float r, f3 dir) {
+  if (S.medium_shape == DTS_MEDIUM_INFINITE) return fexp(-S.sigma_t * r);
+  float lo, hi;
+  int face;
+  const int hit = intersect(S, p, dir, lo, hi, face);
+  if (hit == HIT_MISS) return 1.0f;
+  if (hit == HIT_WALL && hi < r) return 0.0f;  // occluded by a wall (R15)
+  const float len = fmaxf(0.0f, fminf(hi, r) - lo);
+  return fexp(-S.sigma_t * len);
+}
+
+__device__ __forceinline__ f3 inward_normal(int face) {
+  const float s = (face & 1) ? -1.0f : 1.0f;
+  const int a = face >> 1;
+  return mk(a == 0 ? s : 0.0f, a == 1 ? s : 0.0f, a == 2 ? s : 0.0f);
+}
+
+// ----------------------------------------------------------------- path state
+struct PathState {
+  f3 x, w;       // position, incoming direction (camera: primary direction)
+  double E;      // elapsed counted time
+  double Rm, RM; // bin residual bounds T_m - tau_e, T_M - tau_e
+  float beta;
+  int kind, face;
+  int e;         // emitter
+};
+
+struct DbgOut;  // = dts_debug_out
+
+// EDA table access: 16-bit CDF, row of 256 per cell (R10)
+template <bool SMEM>
+__device__ __forceinline__ float qload(const uint16_t* q, int i) {
+  if (SMEM) return (float)q[i];
+  return (float)__ldg(q + i);
+}
+
+// ----------------------------------------------------------------- one DARTS vertex
+// Returns true if the walk continues.  contrib receives the vertex's
+// connection (+ wall NEE) contribution.
+template <bool DBG, bool SMEM>
+__device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
+                                             const uint32_t (&r)[12], float& contrib, dts_debug_out* dbg,
+                                             bool& conn_nonempty, bool& wall_nee, int& end_reason) {
+  contrib = 0.0f;
+  conn_nonempty = false;
+  wall_nee = false;
+  end_reason = 0;
+  const f3 xe = ld3(S.em_pos[ps.e]);
+  const float ek = S.em_k[ps.e];
+  f3 wc, ww;
+  float wconn = 1.0f;
+  const float resM = (float)(ps.RM - ps.E);
+  const float resm = (float)(ps.Rm - ps.E);
+
+  // ---- step 2: direction ----
+  if (ps.kind == KIND_CAMERA) {
+    wc = ww = ps.w;
+    if (DBG) {
+      dbg->tech = 2;
+      dbg->beta_dir = 1.0f;
+    }
+  } else if (ps.kind == KIND_WALL) {
+    const f3 n = inward_normal(ps.face);
+    const float alb = S.wall_albedo[ps.face];
+    const f3 cv = xe - ps.x;
+    const float C = sqrtf(dot(cv, cv));
+    const f3 we = cv * (1.0f / C);
+    const float cw = dot(n, we);
+    const float arrive_lo = resm - C, arrive_hi = resM - C;  // E + C in [Rm, RM)
+    float nee = 0.0f;
+    if (cw > 0.0f && arrive_lo <= 0.0f && arrive_hi > 0.0f) {
+      // R14: time-checked direct NEE at a wall vertex
+      nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr(S, ps.x, xe, C, we) / (C * C);
+      if (S.r_excl > 0.0f && C < S.r_excl) nee = 0.0f;
+      contrib += nee;
+      wall_nee = nee > 0.0f;
+    }
+    if (DBG) dbg->nee = nee;
+    const float u5 = unif(r[5]), u6 = unif(r[6]);
+    const float rr = sqrtf(u5);
+    float sp, cp;
+    __sincosf(2.0f * kPi * u6, &sp, &cp);
+    // cosine hemisphere about n via the frame of R12 (cos = sqrt(1-u5), phi = 2 pi u6)
+    const float sign = copysignf(1.0f, n.z);
+    const float a = -1.0f / (sign + n.z);
+    const float b = n.x * n.y * a;
+    const f3 b1 = mk(1.0f + sign * n.x * n.x * a, sign * b, -sign * n.x);
+    const f3 b2 = mk(b, sign + n.y * n.y * a, -n.y);
+    const float lx = rr * cp, ly = rr * sp, lz = sqrtf(fmaxf(0.0f, 1.0f - u5));
+    wc = ww = mk(b1.x * lx + b2.x * ly + n.x * lz, b1.y * lx + b2.y * ly + n.y * lz, b1.z * lx + b2.z * ly + n.z * lz);
+    ps.beta *= alb;
+    if (DBG) {
+      dbg->tech = 3;
+      dbg->beta_dir = alb;
+    }
+  } else {
+    // medium vertex: gamma of E19 with the table cell of R10 at S = R_M - E (R11)
+    const f3 cv = xe - ps.x;
+    const float C = sqrtf(dot(cv, cv));
+    const float Sres = resM;
+    const float ratio = C / Sres;
+    const float ls = (__logf(Sres) - S.ln_smin) * S.inv_dls;
+    const bool valid = (Sres > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < (float)S.ns);
+    const float gamma = valid ? ratio / (ratio + S.alpha) : 0.0f;
+    int cell = 0;
+    if (valid) {
+      const int ir = min((int)(ratio * (float)S.nr), S.nr - 1);
+      const int is = min((int)ls, S.ns - 1);
+      cell = ir * S.ns + is;
+    }
+    const f3 axis = C > 0.0f ? cv * (1.0f / C) : mk(0.0f, 0.0f, 1.0f);
+    const uint16_t* qc = tab + (size_t)cell * DTS_TABLE_COS_BINS;
+    const float u4 = unif(r[4]), u6 = unif(r[6]);
+    const float phi = kPi * (2.0f * u6 - 1.0f);
+    f3 om;
+    float p_eda = 0.0f;
+    int tech;
+    if (u4 < gamma) {
+      // EDA: inverse transform of the cell's 16-bit CDF; T = u5 * 65536 exactly
+      tech = 1;
+      const float T = (float)(r[5] >> 8) * (1.0f / 256.0f);
+      int j = 0;
+#pragma unroll
+      for (int step = 128; step >= 1; step >>= 1)  // largest j with q_j <= T (q_0 = 0)
+        if (qload<SMEM>(qc, j + step) <= T) j += step;
+      const float qa = qload<SMEM>(qc, j);
+      const float qb = j == 255 ? 65536.0f : qload<SMEM>(qc, j + 1);
+      const float inv = __fdividef(1.0f, qb - qa);
+      // cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts
+      const float opc = ((float)j + (T - qa) * inv) * (1.0f / 128.0f);
+      const float omc = ((float)(255 - j) + (qb - T) * inv) * (1.0f / 128.0f);
+      om = from_frame(axis, opc, omc, phi);
+      p_eda = (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi));
+    } else {
+      tech = 0;
+      float opc, omc;
+      hg_sample(S, unif(r[5]), opc, omc);
+      om = from_frame(ps.w, opc, omc, phi);
+      if (valid) {
+        const int j = min(max((int)floorf((dot(om, axis) + 1.0f) * 128.0f), 0), 255);
+        const float qa = qload<SMEM>(qc, j);
+        const float qb = j == 255 ? 65536.0f : qload<SMEM>(qc, j + 1);
+        p_eda = (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi));
+      }
+    }
+    const float p_hg = hg_eval(S, dot(om, ps.w));
+    const float p_mix = gamma * p_eda + (1.0f - gamma) * p_hg;
+    const float ratio_w = p_hg / p_mix;
+    wc = om;
+    if (S.direction_mode == DTS_DIR_SPLIT) {
+      // R29 SPLIT: MIS weight on the connection only; independent HG walk direction
+      wconn = ratio_w;
+      float opc, omc;
+      hg_sample(S, unif(r[8]), opc, omc);
+      ww = from_frame(ps.w, opc, omc, kPi * (2.0f * unif(r[9]) - 1.0f));
+      if (DBG) dbg->beta_dir = 1.0f;
+    } else {
+      ww = om;
+      ps.beta *= ratio_w;
+      if (DBG) dbg->beta_dir = ratio_w;
+    }
+    if (DBG) {
+      dbg->tech = tech;
+      dbg->gamma = gamma;
+      dbg->p_eda = p_eda;
+      dbg->p_hg = p_hg;
+      dbg->p_mix = p_mix;
+    }
+  }
+  if (DBG) {
+    dbg->wc[0] = wc.x; dbg->wc[1] = wc.y; dbg->wc[2] = wc.z;
+    dbg->ww[0] = ww.x; dbg->ww[1] = ww.y; dbg->ww[2] = ww.z;
+    dbg->wconn = wconn;
+  }
+
+  // ---- intersection, reused by the connection and the walk ----
+  float lo = 0.0f, hi = 0.0f;
+  int face = -1;
+  const int hit = intersect(S, ps.x, ww, lo, hi, face);
+  float clo = lo, chi = hi;
+  int hitc = hit;
+  if (S.direction_mode == DTS_DIR_SPLIT && ps.kind == KIND_MEDIUM) {
+    int fc;
+    hitc = intersect(S, ps.x, wc, clo, chi, fc);
+  }
+  if (DBG) {
+    dbg->t_lo = lo; dbg->t_hi = hi; dbg->hit = hit; dbg->face_hit = face;
+    dbg->tc_lo = clo; dbg->tc_hi = chi;
+  }
+
+  // ---- step 3: elliptical connection (E20-E22; R13 every vertex, R17 unwarped camera) ----
+  if (hitc != HIT_MISS) {
+    const f3 cv = xe - ps.x;
+    const float C2 = dot(cv, cv);
+    const float C = sqrtf(C2);
+    const float q = dot(wc, cv);
+    const float u7 = unif(r[7]);
+    float t = 0.0f, pt = 0.0f, Ssamp = 0.0f;
+    bool ok = false;
+    float pSt = 0.0f;  // S - t (= r2 on the ellipse)
+    if (!(S.warped == 0 && ps.kind == KIND_CAMERA)) {
+      // S(t) = t + |x + wc t - xe| is non-decreasing; admissible S range
+      // [max(Rm - E, S(clo)), min(RM - E, S(chi))) (case I, R14).  Work with
+      // S - C, formed without cancellation:
+      //   S(clo) - C = clo + clo (clo - 2q) / (|p_lo - xe| + C),
+      //   (Rm - E) - C evaluated in double.
+      const f3 plo = fma3(wc, clo, ps.x) - xe;
+      const float rlo = sqrtf(dot(plo, plo));
+      const float lo_m_C = clo + clo * (clo - 2.0f * q) * __fdividef(1.0f, rlo + C);
+      float Shi_geo = __int_as_float(0x7f800000);
+      if (isfinite(chi)) {
+        const f3 phi_ = fma3(wc, chi, ps.x) - xe;
+        Shi_geo = chi + sqrtf(dot(phi_, phi_));
+      }
+      float dlo = fmaxf((float)(ps.Rm - ps.E - (double)C), lo_m_C);  // S_lo - C
+      if (S.s_excess > 0.0f) dlo = fmaxf(dlo, S.s_excess);
+      const float S_lo = C + dlo;
+      const float S_hi = fminf(resM, Shi_geo);
+      if (DBG) { dbg->S_lo = S_lo; dbg->S_hi = S_hi; }
+      if (S_hi > S_lo) {
+        ok = true;
+        // truncated exponential on [S_lo, S_hi); e^{-st (S-S_lo)} = 1 - u7 span
+        float L, pS;
+        if (isinf(S_hi)) {
+          L = neg_log1m(u7) * S.inv_sigma_t;
+          pS = S.sigma_t * (1.0f - u7);
+        } else {
+          const float span = one_m_exp(S.sigma_t * (S_hi - S_lo));
+          L = neg_log1m(u7 * span) * S.inv_sigma_t;
+          pS = S.sigma_t * (1.0f - u7 * span) * __fdividef(1.0f, span);
+        }
+        const float dSC = dlo + L;  // S - C
+        const float Ssm = C + dSC;
+        // S - q = (S - C) + (C - q), C - q = perp^2 / (C + q) for q > 0
+        const f3 pv = cv - wc * q;
+        const float perp2 = dot(pv, pv);
+        const float Cmq = q > 0.0f ? perp2 * __fdividef(1.0f, C + q) : C - q;
+        const float Smq = dSC + Cmq;
+        const float inv2Smq = __fdividef(0.5f, Smq);
+        Ssamp = Ssm;
+        t = dSC * (Ssm + C) * inv2Smq;                 // E21: (S^2 - C^2) / (2 (S - q))
+        pSt = (Smq * Smq + perp2) * inv2Smq;           // S - t
+        pt = pS * Smq * __fdividef(1.0f, pSt);         // E22 with the Jacobian of R2
+      }
+    } else {
+      // R17: unwarped camera vertex, shell |x(t) - xe| in [Rm, RM): <= 2 t-intervals
+      float a_lo = clo;
+      if (S.s_excess > 0.0f) {
+        const float Se = C + S.s_excess;
+        a_lo = fmaxf(a_lo, (Se - C) * (Se + C) / (2.0f * (Se - q)));
+      }
+      float ia0 = 0.f, ib0 = 0.f, ia1 = 0.f, ib1 = 0.f;
+      int ni = 0;
+      const float perp2 = C2 - q * q;
+      const float radM = resM * resM - perp2;
+      if (resM > 0.0f && radM > 0.0f) {
+        const float hM = sqrtf(radM);
+        const float radm = resm * resm - perp2;
+        if (resm > 0.0f && radm > 0.0f) {
+          const float hm = sqrtf(radm);
+          ia0 = q - hM; ib0 = q - hm; ia1 = q + hm; ib1 = q + hM;
+          ni = 2;
+        } else {
+          ia0 = q - hM; ib0 = q + hM;
+          ni = 1;
+        }
+      }
+      float m0 = 0.f, m1 = 0.f;
+      if (ni >= 1) {
+        ia0 = fmaxf(ia0, a_lo); ib0 = fminf(ib0, chi);
+        if (ib0 > ia0) m0 = fexp(-S.sigma_t * (ia0 - clo)) * one_m_exp(S.sigma_t * (ib0 - ia0));
+      }
+      if (ni == 2) {
+        ia1 = fmaxf(ia1, a_lo); ib1 = fminf(ib1, chi);
+        if (ib1 > ia1) m1 = fexp(-S.sigma_t * (ia1 - clo)) * one_m_exp(S.sigma_t * (ib1 - ia1));
+      }
+      const float Z = m0 + m1;
+      if (DBG) { dbg->S_lo = 0.0f; dbg->S_hi = Z; }
+      if (Z > 0.0f) {
+        ok = true;
+        const float v = u7 * Z;
+        const bool second = (m0 <= 0.0f) || (ni == 2 && !(v < m0));
+        const float ia = second ? ia1 : ia0, ib = second ? ib1 : ib0, mm = second ? m1 : m0;
+        float up = second ? (v - m0) / m1 : v / m0;
+        up = fminf(up, 0.99999994f);
+        (void)mm;
+        const float span = one_m_exp(S.sigma_t * (ib - ia));
+        t = ia + neg_log1m(up * span) * S.inv_sigma_t;
+        pt = S.sigma_t * fexp(-S.sigma_t * (t - clo)) / Z;
+      }
+    }
+    if (ok) {
+      conn_nonempty = true;
+      const f3 xell = fma3(wc, t, ps.x);
+      const f3 de = xe - xell;
+      float r2sq = dot(de, de);
+      float r2 = sqrtf(r2sq);
+      const f3 we = de * __fdividef(1.0f, r2);
+      if (pSt > 0.0f) {  // on the ellipse r2 = S - t, formed without cancellation
+        r2 = pSt;
+        r2sq = pSt * pSt;
+      }
+      const float rho = hg_eval(S, dot(wc, we));
+      const float tr = fexp(-S.sigma_t * (t - clo)) * segment_tr(S, xell, xe, r2, we);
+      float c = ps.beta * wconn * S.sigma_s * tr * rho * ek / (r2sq * pt);
+      if (S.r_excl > 0.0f && r2 < S.r_excl) c = 0.0f;
+      contrib += c;
+      if (DBG) {
+        dbg->S = (S.warped == 0 && ps.kind == KIND_CAMERA) ? t + r2 : Ssamp;
+        dbg->t = t;
+        dbg->x_ell[0] = xell.x; dbg->x_ell[1] = xell.y; dbg->x_ell[2] = xell.z;
+        dbg->p_t = pt;
+        dbg->contrib = c;
+        dbg->conn_valid = 1;
+      }
+    }
+  }
+
+  // ---- step 1 for the next vertex: DA distance sampling by RIS (E12-E15) ----
+  if (hit == HIT_MISS) {
+    if (DBG) { dbg->event = 0; dbg->terminate = 1; dbg->beta_out = ps.beta; }
+    end_reason = DTS_CTR_ESCAPES;
+    return false;
+  }
+  const float counts = (S.warped || ps.kind != KIND_CAMERA) ? 1.0f : 0.0f;
+  const bool inf_hi = isinf(hi);
+  const float p_m = inf_hi ? 1.0f : one_m_exp(S.sigma_t * (hi - lo));  // E12, R28
+  const float u0 = unif(r[0]);
+  if (DBG) dbg->p_m = p_m;
+  if (u0 < p_m) {
+    // candidates: Sobol row r = floor(32 u1) with Cranley-Patterson shift u2 (R6):
+    // Q[r][i] = RI2(8r+i) = bitrev3(i)/8 + bitrev5(r)/256, shift and mod 1 done
+    // exactly on 24-bit integers.
+    const uint32_t row = r[1] >> 27;
+    const uint32_t br5 = __brev(row) >> 27;
+    const uint32_t m2 = r[2] >> 8;
+    const f3 cv = xe - ps.x;
+    const float qd = dot(ww, cv);
+    const f3 perp = cv - ww * qd;
+    const float perp2 = dot(perp, perp);
+    float d[8], e2[8], lw[8];
+    float emax = -__int_as_float(0x7f800000);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t br3 = __brev((uint32_t)i) >> 29;
+      const uint32_t v = (m2 + ((br3 * 32u + br5) << 16)) & 0xFFFFFFu;
+      const float ui = (float)v * 5.9604644775390625e-08f;
+      d[i] = lo + neg_log1m(p_m * ui) * S.inv_sigma_t;  // E14 with the sign of R1
+      const float Delta = resM - counts * d[i];          // R4
+      const float dq = d[i] - qd;
+      const float r2i = fmaf(dq, dq, perp2);
+      const bool valid = (Delta > 0.0f) && (r2i <= Delta * Delta);
+      const float sr = rsqrtf(Delta);
+      const float invD = sr * sr;
+      // log2 of Phi' = Delta^{-3/2} exp(-r^2/(4 D Delta) - sigma_a Delta) (E9, constants dropped)
+      const float ex = fmaf(S.neg_inv4D_log2e * r2i, invD, S.neg_sa_log2e * Delta);
+      e2[i] = valid ? ex : -__int_as_float(0x7f800000);
+      lw[i] = invD * sr;  // Delta^{-3/2}
+      emax = fmaxf(emax, e2[i]);
+    }
+    float w[8];
+    float W = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w[i] = e2[i] > -__int_as_float(0x7f800000) ? lw[i] * exp2f(e2[i] - emax) : 0.0f;  // R7
+      W += w[i];
+    }
+    if (DBG) {
+      for (int i = 0; i < 8; ++i) {
+        dbg->cand_d[i] = d[i];
+        dbg->cand_wn[i] = W > 0.0f ? w[i] / W : 0.0f;
+      }
+    }
+    if (!(W > 0.0f)) {
+      if (DBG) { dbg->event = 4; dbg->terminate = 1; dbg->beta_out = ps.beta; }
+      end_reason = DTS_CTR_RIS_INVALID;  // R5
+      return false;
+    }
+    const float thr = unif(r[3]) * W;
+    float cum = 0.0f, dsel = d[7], wsel = w[7];
+    int is = 7;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      cum += w[i];
+      const bool take = !found && (cum > thr);
+      dsel = take ? d[i] : dsel;
+      wsel = take ? w[i] : wsel;
+      is = take ? i : is;
+      found = found || take;
+    }
+    const float beta_ris = S.albedo * (W * 0.125f) / wsel;  // E15: a * mean(w) / w*
+    ps.beta *= beta_ris;
+    ps.x = fma3(ww, dsel, ps.x);
+    ps.E += (double)(counts * dsel);
+    ps.kind = KIND_MEDIUM;
+    ps.w = ww;
+    if (DBG) { dbg->event = 1; dbg->istar = is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
+  } else {
+    if (hit == HIT_WALL) {
+      f3 xn = fma3(ww, hi, ps.x);
+      const int a = face >> 1;
+      const float pl = (face & 1) ? S.bmax[a] : S.bmin[a];
+      if (a == 0) xn.x = pl; else if (a == 1) xn.y = pl; else xn.z = pl;  // snap onto the wall
+      ps.x = xn;
+      ps.E += (double)(counts * hi);
+      ps.kind = KIND_WALL;
+      ps.face = face;
+      ps.w = ww;
+      if (DBG) { dbg->event = 2; dbg->d = hi; dbg->beta_ris = 1.0f; }
+    } else {
+      if (DBG) { dbg->event = 3; dbg->terminate = 1; dbg->beta_out = ps.beta; }
+      end_reason = DTS_CTR_ESCAPES;
+      return false;
+    }
+  }
+  if (DBG) {
+    dbg->x_next[0] = ps.x.x; dbg->x_next[1] = ps.x.y; dbg->x_next[2] = ps.x.z;
+    dbg->E_next = ps.E;
+    dbg->beta_out = ps.beta;
+  }
+  // early exit
+  const f3 dn = ps.x - xe;
+  const float Cn = sqrtf(dot(dn, dn));
+  if ((float)(ps.RM - ps.E) - Cn <= 0.0f) {
+    if (DBG) dbg->terminate = 1;
+    end_reason = DTS_CTR_EARLY_EXIT;
+    return false;
+  }
+  if (!isfinite(ps.beta)) {
+    if (DBG) dbg->terminate = 1;
+    end_reason = DTS_CTR_NONFINITE;
+    return false;
+  }
+  return true;
+}
+
+}  // namespace dts

@@ -1,0 +1,890 @@
+// dts_lib.cu -- libdts.so: C ABI (include/dts.h), EDA table build, the
+// persistent render kernel and the debug kernel for sm_100a.
+//
+// Design: one lane per path, persistent CTAs (one per SM
+// while the 16-bit EDA table is resident in shared memory), warp-level lane
+// refill from a warp-private chunk of a global work counter, per-path
+// accumulation in a register and ONE fp32 RED per path into the caller's
+// histogram (PAPER.md:373 per-bin dedicated paths: a path only ever lands in
+// its own cell).  No tensor cores: nothing on this path is a dense contraction.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/dts.h"
+#include "dts_device.cuh"
+
+using namespace dts;
+
+// ============================================================== error handling
+static thread_local std::string g_last_error;
+static thread_local int g_last_launches = 0, g_last_grid = 0, g_last_block = 0, g_last_smem = 0;
+
+static dts_status fail(dts_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return fail(DTS_E_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct dts_scene {
+  dts_scene_desc desc;
+  DevScene S;
+  uint16_t* d_table = nullptr;
+  size_t table_n = 0;
+  unsigned long long* d_work = nullptr;  // global work counter
+  float* d_hist_host = nullptr;          // dts_render_host scratch
+  size_t d_hist_host_n = 0;
+  uint64_t* d_ctr_host = nullptr;
+  int num_sms = 0;
+  int device = 0;
+};
+
+// ============================================================== EDA table build (fp64, R9/R10)
+__constant__ double kGLx8[8] = {-0.9602898564975362, -0.7966664774136267, -0.525532409916329, -0.18343464249564978,
+                                0.18343464249564978, 0.525532409916329,   0.7966664774136267, 0.9602898564975362};
+__constant__ double kGLw8[8] = {0.10122853629037706, 0.22238103445337443, 0.3137066458778869, 0.36268378337836166,
+                                0.36268378337836166, 0.3137066458778869,  0.22238103445337443, 0.10122853629037706};
+
+struct TableParams {
+  double sigma_s, sigma_a, sigma_t, D;
+  double smin, smax;
+  int nr, ns;
+};
+
+// E17 for one cos(theta): sigma_s * int_0^{t_M} e^{-sigma_t t} Phi(x + w t, S - t) dt
+// (emitter at the far focus, distance C), cut at 40/sigma_t, split at the
+// closest approach t = C cos, 4 panels x 8-point Gauss-Legendre per part.
+__device__ double e17_integrand(const TableParams& P, double C, double S, double cth) {
+  const double tM = (S - C) * (S + C) / (2.0 * (S - C * cth));
+  const double tend = fmin(tM, 40.0 / P.sigma_t);
+  const double tc = C * cth;
+  double cuts[3];
+  int nc = 0;
+  cuts[nc++] = 0.0;
+  if (tc > 0.0 && tc < tend) cuts[nc++] = tc;
+  cuts[nc++] = tend;
+  const double k = 1.0 / (4.0 * P.D);
+  const double norm = 1.0 / pow(4.0 * 3.14159265358979323846 * P.D, 1.5);
+  double total = 0.0;
+  for (int part = 0; part + 1 < nc; ++part) {
+    const double a = cuts[part], h = (cuts[part + 1] - a) * 0.25;
+    for (int panel = 0; panel < 4; ++panel) {
+      const double pa = a + panel * h;
+      for (int i = 0; i < 8; ++i) {
+        const double t = pa + 0.5 * h * (1.0 + kGLx8[i]);
+        const double r2 = t * t - 2.0 * t * C * cth + C * C;
+        const double dt = S - t;
+        double phi = 0.0;
+        if (dt > 0.0) phi = norm * exp(-r2 * k / dt - P.sigma_a * dt) / (dt * sqrt(dt));
+        total += 0.5 * h * kGLw8[i] * P.sigma_s * exp(-P.sigma_t * t) * phi;
+      }
+    }
+  }
+  return total;
+}
+
+// grid = cells, block = 256 (one thread per cos bin)
+__global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_t* __restrict__ q) {
+  __shared__ double F[256];
+  const int cell = blockIdx.x;
+  const int ir = cell / P.ns, is = cell % P.ns;
+  const double ratio = (ir + 0.5) / P.nr;
+  const double S = P.smin * pow(P.smax / P.smin, (is + 0.5) / P.ns);
+  const double C = ratio * S;
+  const int j = threadIdx.x;
+  const double dc = 2.0 / 256.0;
+  const double c0 = -1.0 + j * dc;
+  double acc = 0.0;
+  for (int n = 0; n < 8; ++n) acc += 0.5 * dc * kGLw8[n] * e17_integrand(P, C, S, c0 + 0.5 * dc * (1.0 + kGLx8[n]));
+  F[j] = acc;
+  __syncthreads();
+  if (j == 0) {
+    double total = 0.0;
+    for (int i = 0; i < 256; ++i) total += F[i];
+    double cdf = 0.0;
+    for (int i = 0; i < 256; ++i) {
+      double qv = floor(65536.0 * cdf + 0.5);
+      if (qv > 65535.0) qv = 65535.0;
+      q[(size_t)cell * 256 + i] = (uint16_t)qv;
+      cdf += F[i] / total;
+    }
+  }
+}
+
+// ============================================================== debug kernel
+template <bool DUMMY>
+__global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n, const dts_debug_in* __restrict__ in,
+                             dts_debug_out* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  dts_debug_out o;
+  memset(&o, 0, sizeof(o));
+  o.istar = -1;
+  const dts_debug_in rec = in[i];
+  PathState ps;
+  ps.x = mk(rec.x[0], rec.x[1], rec.x[2]);
+  ps.w = mk(rec.w[0], rec.w[1], rec.w[2]);
+  ps.E = rec.E;
+  ps.beta = rec.beta;
+  ps.kind = rec.kind;
+  ps.face = rec.face;
+  ps.e = rec.emitter;
+  ps.Rm = S.t0 + (double)rec.bin * S.dt - (double)S.em_t[rec.emitter];
+  ps.RM = S.t0 + (double)(rec.bin + 1) * S.dt - (double)S.em_t[rec.emitter];
+  uint32_t r[12];
+  for (int k = 0; k < 12; ++k) r[k] = rec.r[k];
+  float c;
+  bool cn, wn;
+  int reason;
+  darts_vertex<true, false>(S, tab, ps, r, c, &o, cn, wn, reason);
+  out[i] = o;
+}
+
+// ============================================================== render kernel
+struct RenderParams {
+  DevScene S;
+  const uint16_t* tab;
+  float* hist;
+  float* hist_sq;
+  unsigned long long* counters;
+  unsigned long long* work;
+  uint64_t total;    // work items of this launch
+  uint64_t s_begin;  // first sample index
+  uint64_t n_s;      // samples per cell/pixel in this launch
+  uint64_t spp;      // samples per cell (PER_CELL) or per pixel
+  uint32_t npix;     // crop pixels
+  uint32_t cw;       // crop width
+  uint32_t table_u4; // table size in 16-byte words
+};
+
+constexpr int kBlock = 512;
+constexpr uint32_t kChunk = 128;
+
+struct PathCtx {
+  PathState ps;
+  uint32_t id_lo, id_hi;
+  uint32_t k;
+  uint32_t cell;  // histogram cell (crop-local)
+  float inv_n;
+  float acc;
+};
+
+// decode a work index into a path (returns false if the path retires at start)
+__device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx, PathCtx& pc, uint32_t& ctr_miss,
+                                           uint32_t& ctr_early) {
+  const DevScene& S = P.S;
+  const uint32_t B = (uint32_t)S.n_bins;
+  uint64_t s;
+  uint32_t pl, b;
+  uint64_t id;
+  const uint64_t Npix = (uint64_t)S.width * (uint64_t)S.height;
+  float inv_n;
+  if (S.spp_mode == DTS_SPP_PER_CELL) {
+    // issue order (b descending, pixel, s): long late-bin walks first
+    const uint64_t sl = widx % P.n_s;
+    const uint64_t rest = widx / P.n_s;
+    pl = (uint32_t)(rest % P.npix);
+    b = B - 1u - (uint32_t)(rest / P.npix);
+    s = P.s_begin + sl;
+    inv_n = 1.0f / (float)P.spp;
+  } else {
+    pl = (uint32_t)(widx % P.npix);
+    s = P.s_begin + widx / P.npix;
+  }
+  const uint32_t px = (uint32_t)S.crop[0] + pl % P.cw, py = (uint32_t)S.crop[1] + pl / P.cw;
+  const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
+  if (S.spp_mode == DTS_SPP_PER_CELL) {
+    id = (s * Npix + p) * (uint64_t)B + b;
+  } else {
+    // R21: bin = (s + o_p) mod B with a per-pixel Philox offset
+    const u4 o = philox((uint32_t)p, (uint32_t)(p >> 32), 0xFFFFFFFEu, 0u, S.seed_lo, S.seed_hi);
+    const uint32_t op = min((uint32_t)((float)B * unif(o.a)), B - 1u);
+    b = (uint32_t)((s + op) % B);
+    const uint32_t rel = (b + B - op) % B;
+    const uint64_t n_pb = P.spp / B + ((uint64_t)rel < P.spp % B ? 1u : 0u);
+    inv_n = 1.0f / (float)n_pb;
+    id = s * Npix + p;
+  }
+  pc.id_lo = (uint32_t)id;
+  pc.id_hi = (uint32_t)(id >> 32);
+  pc.k = 0;
+  pc.cell = pl * B + b;
+  pc.inv_n = inv_n;
+  pc.acc = 0.0f;
+  const u4 a = philox(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 0u, S.seed_lo, S.seed_hi);
+  int e = min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1);
+  PathState& ps = pc.ps;
+  ps.e = e;
+  if (S.camera_kind == DTS_CAMERA_PINHOLE) {
+    const float sx = (2.0f * ((float)px + unif(a.a)) / (float)S.width - 1.0f) * S.tan_half * S.aspect;
+    const float sy = (1.0f - 2.0f * ((float)py + unif(a.b)) / (float)S.height) * S.tan_half;
+    f3 w = mk(S.fwd[0] + sx * S.right[0] + sy * S.upc[0], S.fwd[1] + sx * S.right[1] + sy * S.upc[1],
+              S.fwd[2] + sx * S.right[2] + sy * S.upc[2]);
+    ps.w = w * rsqrtf(dot(w, w));
+    ps.x = ld3(S.cam_pos);
+    ps.beta = 1.0f;
+  } else {
+    const u4 bb = philox(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 1u, S.seed_lo, S.seed_hi);
+    const u4 cc = philox(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 2u, S.seed_lo, S.seed_hi);
+    const float rad = S.det_radius * cbrtf(unif(bb.a));
+    const float z = 1.0f - 2.0f * unif(bb.b);
+    const float sz = sqrtf(fmaxf(0.0f, 1.0f - z * z));
+    float sp, cp;
+    __sincosf(2.0f * kPi * unif(bb.c), &sp, &cp);
+    ps.x = mk(S.cam_pos[0] + rad * sz * cp, S.cam_pos[1] + rad * sz * sp, S.cam_pos[2] + rad * z);
+    const float z2 = 1.0f - 2.0f * unif(bb.d);
+    const float s2 = sqrtf(fmaxf(0.0f, 1.0f - z2 * z2));
+    __sincosf(2.0f * kPi * unif(cc.a), &sp, &cp);
+    ps.w = mk(s2 * cp, s2 * sp, z2);
+    ps.beta = 4.0f * kPi;
+  }
+  ps.E = 0.0;
+  ps.kind = KIND_CAMERA;
+  ps.face = -1;
+  const double te = (double)S.em_t[e];
+  ps.Rm = S.t0 + (double)b * S.dt - te;
+  ps.RM = S.t0 + (double)(b + 1) * S.dt - te;
+  float lo, hi;
+  int f;
+  if (intersect(S, ps.x, ps.w, lo, hi, f) == HIT_MISS) {
+    ++ctr_miss;
+    return false;
+  }
+  if (S.warped || S.camera_kind == DTS_CAMERA_SPHERE_DETECTOR) {
+    const f3 dv = ps.x - ld3(S.em_pos[e]);
+    if (sqrtf(dot(dv, dv)) >= (float)ps.RM) {
+      ++ctr_early;
+      return false;
+    }
+  }
+  return true;
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kBlock, 1) render_darts_kernel(const RenderParams P) {
+  extern __shared__ __align__(16) uint16_t s_tab[];
+  const DevScene& S = P.S;
+  const uint16_t* tab = P.tab;
+  if (SMEM) {
+    const uint4* src = reinterpret_cast<const uint4*>(P.tab);
+    uint4* dst = reinterpret_cast<uint4*>(s_tab);
+    for (uint32_t i = threadIdx.x; i < P.table_u4; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+    tab = s_tab;
+  }
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // warp-uniform work queue [qn, qe)
+  uint64_t qn = 0, qe = 0;
+  bool exhausted = false;
+  bool active = false;
+  PathCtx pc;
+  // per-warp counters (identical in every lane)
+  uint32_t c_paths = 0, c_miss = 0, c_vert = 0, c_conn = 0, c_ris = 0, c_early = 0, c_esc = 0, c_cap = 0, c_nf = 0,
+           c_nee = 0;
+  uint32_t l_miss = 0, l_early = 0;  // per-lane start-time retirements
+  while (true) {
+    const unsigned idle = __ballot_sync(FULL, !active);
+    if (idle && !exhausted) {
+      const uint32_t nidle = __popc(idle);
+      const uint32_t rank = __popc(idle & lt_mask);
+      const uint64_t avail = qe - qn;
+      uint64_t my = ~0ull;
+      if (avail >= nidle) {
+        my = qn + rank;
+        qn += nidle;
+      } else {
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(P.work, (unsigned long long)kChunk);
+        nb = __shfl_sync(FULL, nb, 0);
+        uint64_t ne = nb + kChunk < P.total ? nb + kChunk : P.total;
+        if (nb >= P.total) {
+          exhausted = true;
+          ne = nb;
+        }
+        if (rank < avail) {
+          my = qn + rank;
+        } else {
+          const uint64_t cand = nb + (rank - avail);
+          my = cand < ne ? cand : ~0ull;
+        }
+        const uint64_t nq = nb + (nidle - avail);
+        qn = nq < ne ? nq : ne;
+        qe = ne;
+      }
+      if (!active && my != ~0ull && my < P.total) {
+        active = start_path(P, my, pc, l_miss, l_early);
+        ++c_paths;  // counted per lane below via ballot
+      }
+    }
+    const unsigned act = __ballot_sync(FULL, active);
+    if (act == 0u) {
+      if (exhausted) break;
+      continue;
+    }
+    bool done = false;
+    bool cn = false, wn = false, cap = false;
+    int reason = 0;
+    if (active) {
+      uint32_t r[12];
+      const u4 a = philox(pc.id_lo, pc.id_hi, pc.k, 0u, S.seed_lo, S.seed_hi);
+      const u4 b = philox(pc.id_lo, pc.id_hi, pc.k, 1u, S.seed_lo, S.seed_hi);
+      r[0] = a.a; r[1] = a.b; r[2] = a.c; r[3] = a.d;
+      r[4] = b.a; r[5] = b.b; r[6] = b.c; r[7] = b.d;
+      r[8] = r[9] = r[10] = r[11] = 0u;
+      if (S.direction_mode == DTS_DIR_SPLIT && pc.ps.kind == KIND_MEDIUM) {
+        const u4 c = philox(pc.id_lo, pc.id_hi, pc.k, 2u, S.seed_lo, S.seed_hi);
+        r[8] = c.a; r[9] = c.b; r[10] = c.c; r[11] = c.d;
+      }
+      float contrib;
+      const bool alive = darts_vertex<false, SMEM>(S, tab, pc.ps, r, contrib, nullptr, cn, wn, reason);
+      pc.acc += contrib;
+      ++pc.k;
+      cap = alive && pc.k >= (uint32_t)S.max_bounces;
+      done = !alive || cap;
+    }
+    // event counters: every lane takes part in the ballots (warp-uniform sums)
+    c_conn += __popc(__ballot_sync(FULL, cn));
+    c_nee += __popc(__ballot_sync(FULL, wn));
+    c_ris += __popc(__ballot_sync(FULL, reason == DTS_CTR_RIS_INVALID));
+    c_early += __popc(__ballot_sync(FULL, reason == DTS_CTR_EARLY_EXIT));
+    c_esc += __popc(__ballot_sync(FULL, reason == DTS_CTR_ESCAPES));
+    c_nf += __popc(__ballot_sync(FULL, reason == DTS_CTR_NONFINITE));
+    c_cap += __popc(__ballot_sync(FULL, cap));
+    c_vert += __popc(act);
+    if (done) {
+      float v = pc.acc;
+      if (isfinite(v)) {
+        if (v != 0.0f) {
+          atomicAdd(P.hist + pc.cell, v * pc.inv_n);
+          if (P.hist_sq) atomicAdd(P.hist_sq + pc.cell, v * v * pc.inv_n);
+        }
+      }
+      active = false;
+    }
+  }
+  // c_paths was counted per lane; reduce across the warp
+  uint32_t lp = c_paths;
+  for (int o = 16; o > 0; o >>= 1) {
+    lp += __shfl_xor_sync(FULL, lp, o);
+    l_miss += __shfl_xor_sync(FULL, l_miss, o);
+    l_early += __shfl_xor_sync(FULL, l_early, o);
+  }
+  if (lane == 0 && P.counters) {
+    unsigned long long* C = P.counters;
+    atomicAdd(C + DTS_CTR_PATHS, (unsigned long long)lp);
+    atomicAdd(C + DTS_CTR_CAMERA_MISS, (unsigned long long)l_miss);
+    atomicAdd(C + DTS_CTR_VERTICES, (unsigned long long)c_vert);
+    atomicAdd(C + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
+    atomicAdd(C + DTS_CTR_RIS_INVALID, (unsigned long long)c_ris);
+    atomicAdd(C + DTS_CTR_EARLY_EXIT, (unsigned long long)(c_early + l_early));
+    atomicAdd(C + DTS_CTR_ESCAPES, (unsigned long long)c_esc);
+    atomicAdd(C + DTS_CTR_CAP_HITS, (unsigned long long)c_cap);
+    atomicAdd(C + DTS_CTR_NONFINITE, (unsigned long long)c_nf);
+    atomicAdd(C + DTS_CTR_WALL_NEE, (unsigned long long)c_nee);
+  }
+}
+
+// ============================================================== vanilla
+__device__ __forceinline__ void vanilla_splat(const RenderParams& P, uint32_t pl, double arrive, float c) {
+  const DevScene& S = P.S;
+  if (!(c != 0.0f) || !isfinite(c) || arrive < S.t0) return;
+  const int bin = (int)floor((arrive - S.t0) / S.dt);
+  if (bin < 0 || bin >= S.n_bins) return;
+  atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, c / (float)P.spp);
+}
+
+__global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderParams P) {
+  const DevScene& S = P.S;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t c_paths = 0, c_miss = 0, c_vert = 0, c_early = 0, c_esc = 0, c_cap = 0;
+  for (uint64_t widx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; widx < P.total; widx += stride) {
+    const uint32_t pl = (uint32_t)(widx % P.npix);
+    const uint64_t s = P.s_begin + widx / P.npix;
+    const uint32_t px = (uint32_t)S.crop[0] + pl % P.cw, py = (uint32_t)S.crop[1] + pl / P.cw;
+    const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
+    const uint64_t id = s * ((uint64_t)S.width * (uint64_t)S.height) + p;
+    const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
+    ++c_paths;
+    const u4 a = philox(id_lo, id_hi, 0xFFFFFFFFu, 0u, S.seed_lo, S.seed_hi);
+    const int e = min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1);
+    const f3 xe = ld3(S.em_pos[e]);
+    const double te = (double)S.em_t[e];
+    const float ek = S.em_k[e];
+    f3 x, w;
+    float beta;
+    if (S.camera_kind == DTS_CAMERA_PINHOLE) {
+      const float sx = (2.0f * ((float)px + unif(a.a)) / (float)S.width - 1.0f) * S.tan_half * S.aspect;
+      const float sy = (1.0f - 2.0f * ((float)py + unif(a.b)) / (float)S.height) * S.tan_half;
+      w = mk(S.fwd[0] + sx * S.right[0] + sy * S.upc[0], S.fwd[1] + sx * S.right[1] + sy * S.upc[1],
+             S.fwd[2] + sx * S.right[2] + sy * S.upc[2]);
+      w = w * rsqrtf(dot(w, w));
+      x = ld3(S.cam_pos);
+      beta = 1.0f;
+    } else {
+      const u4 bb = philox(id_lo, id_hi, 0xFFFFFFFFu, 1u, S.seed_lo, S.seed_hi);
+      const u4 cc = philox(id_lo, id_hi, 0xFFFFFFFFu, 2u, S.seed_lo, S.seed_hi);
+      const float rad = S.det_radius * cbrtf(unif(bb.a));
+      const float z = 1.0f - 2.0f * unif(bb.b);
+      const float sz = sqrtf(fmaxf(0.0f, 1.0f - z * z));
+      float sp, cp;
+      __sincosf(2.0f * kPi * unif(bb.c), &sp, &cp);
+      x = mk(S.cam_pos[0] + rad * sz * cp, S.cam_pos[1] + rad * sz * sp, S.cam_pos[2] + rad * z);
+      const float z2 = 1.0f - 2.0f * unif(bb.d);
+      const float s2 = sqrtf(fmaxf(0.0f, 1.0f - z2 * z2));
+      __sincosf(2.0f * kPi * unif(cc.a), &sp, &cp);
+      w = mk(s2 * cp, s2 * sp, z2);
+      beta = 4.0f * kPi;
+    }
+    {
+      float lo, hi;
+      int f;
+      if (intersect(S, x, w, lo, hi, f) == HIT_MISS) {
+        ++c_miss;
+        continue;
+      }
+    }
+    int kind = KIND_CAMERA, face = -1;
+    double E = 0.0;
+    bool alive = true;
+    int k;
+    for (k = 0; k < S.max_bounces && alive; ++k) {
+      const u4 r = philox(id_lo, id_hi, (uint32_t)k, 0u, S.seed_lo, S.seed_hi);
+      ++c_vert;
+      if (kind == KIND_MEDIUM) {
+        float opc, omc;
+        hg_sample(S, unif(r.b), opc, omc);
+        w = from_frame(w, opc, omc, kPi * (2.0f * unif(r.c) - 1.0f));
+      } else if (kind == KIND_WALL) {
+        const f3 n = inward_normal(face);
+        const float u5 = unif(r.b), u6 = unif(r.c);
+        const float rr = sqrtf(u5);
+        float sp, cp;
+        __sincosf(2.0f * kPi * u6, &sp, &cp);
+        const float sign = copysignf(1.0f, n.z);
+        const float aa = -1.0f / (sign + n.z);
+        const float bq = n.x * n.y * aa;
+        const f3 b1 = mk(1.0f + sign * n.x * n.x * aa, sign * bq, -sign * n.x);
+        const f3 b2 = mk(bq, sign + n.y * n.y * aa, -n.y);
+        const float lx = rr * cp, ly = rr * sp, lz = sqrtf(fmaxf(0.0f, 1.0f - u5));
+        w = mk(b1.x * lx + b2.x * ly + n.x * lz, b1.y * lx + b2.y * ly + n.y * lz, b1.z * lx + b2.z * ly + n.z * lz);
+        beta *= S.wall_albedo[face];
+      }
+      float lo, hi;
+      int hf;
+      const int hit = intersect(S, x, w, lo, hi, hf);
+      if (hit == HIT_MISS) { ++c_esc; alive = false; break; }
+      const float counts = (S.warped || kind != KIND_CAMERA) ? 1.0f : 0.0f;
+      const f3 d0 = x - xe;
+      const float Cprev = sqrtf(dot(d0, d0));
+      float d = lo + neg_log1m(unif(r.a)) * S.inv_sigma_t;
+      if (d < hi) {
+        x = fma3(w, d, x);
+        E += (double)(counts * d);
+        beta *= S.albedo;
+        kind = KIND_MEDIUM;
+      } else if (hit == HIT_WALL) {
+        d = hi;
+        f3 xn = fma3(w, hi, x);
+        const int ax = hf >> 1;
+        const float pl2 = (hf & 1) ? S.bmax[ax] : S.bmin[ax];
+        if (ax == 0) xn.x = pl2; else if (ax == 1) xn.y = pl2; else xn.z = pl2;
+        x = xn;
+        E += (double)(counts * hi);
+        kind = KIND_WALL;
+        face = hf;
+      } else { ++c_esc; alive = false; break; }
+      const f3 cv = xe - x;
+      const float C = sqrtf(dot(cv, cv));
+      const double arrive = te + E + (double)C;
+      if (arrive >= S.t0 + S.dt * S.n_bins) { ++c_early; alive = false; break; }
+      const f3 we = cv * (1.0f / C);
+      float c;
+      if (kind == KIND_MEDIUM) {
+        c = beta * hg_eval(S, dot(w, we));
+        if (S.s_excess > 0.0f && d + C - Cprev < S.s_excess) c = 0.0f;
+      } else {
+        c = beta * (S.wall_albedo[face] * (1.0f / kPi)) * fmaxf(0.0f, dot(inward_normal(face), we));
+      }
+      c *= segment_tr(S, x, xe, C, we) * ek / (C * C);
+      if (S.r_excl > 0.0f && C < S.r_excl) c = 0.0f;
+      vanilla_splat(P, pl, arrive, c);
+    }
+    if (alive && k >= S.max_bounces) ++c_cap;
+  }
+  // warp-reduce and flush counters
+  for (int o = 16; o > 0; o >>= 1) {
+    c_paths += __shfl_xor_sync(0xffffffffu, c_paths, o);
+    c_miss += __shfl_xor_sync(0xffffffffu, c_miss, o);
+    c_vert += __shfl_xor_sync(0xffffffffu, c_vert, o);
+    c_early += __shfl_xor_sync(0xffffffffu, c_early, o);
+    c_esc += __shfl_xor_sync(0xffffffffu, c_esc, o);
+    c_cap += __shfl_xor_sync(0xffffffffu, c_cap, o);
+  }
+  if ((threadIdx.x & 31) == 0 && P.counters) {
+    atomicAdd(P.counters + DTS_CTR_PATHS, (unsigned long long)c_paths);
+    atomicAdd(P.counters + DTS_CTR_CAMERA_MISS, (unsigned long long)c_miss);
+    atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
+    atomicAdd(P.counters + DTS_CTR_EARLY_EXIT, (unsigned long long)c_early);
+    atomicAdd(P.counters + DTS_CTR_ESCAPES, (unsigned long long)c_esc);
+    atomicAdd(P.counters + DTS_CTR_CAP_HITS, (unsigned long long)c_cap);
+  }
+}
+
+// ============================================================== host helpers
+static void vsub(const double a[3], const double b[3], double o[3]) { for (int i = 0; i < 3; ++i) o[i] = a[i] - b[i]; }
+static void vnorm(double a[3]) { double n = std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); for (int i = 0; i < 3; ++i) a[i] /= n; }
+static void vcross(const double a[3], const double b[3], double o[3]) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+static dts_status validate(const dts_scene_desc& d) {
+  auto bad = [](const char* m) { return fail(DTS_E_INVALID_ARG, m); };
+  if (!(d.sigma_s > 0.0f) || !(d.sigma_a >= 0.0f) || !std::isfinite(d.sigma_s) || !std::isfinite(d.sigma_a))
+    return bad("sigma_s must be > 0 and sigma_a >= 0");
+  if (!(d.g > -1.0f && d.g < 1.0f)) return bad("HG g must lie in (-1, 1)");
+  if (d.medium_shape < 0 || d.medium_shape > 2) return bad("unknown medium_shape");
+  if (d.medium_shape == DTS_MEDIUM_SPHERE && !(d.radius > 0.0f)) return bad("sphere radius must be > 0");
+  if (d.medium_shape == DTS_MEDIUM_BOX)
+    for (int a = 0; a < 3; ++a)
+      if (!(d.bmax[a] > d.bmin[a])) return bad("box bmax must exceed bmin");
+  if (d.wall_mask && d.medium_shape != DTS_MEDIUM_BOX) return bad("walls need a BOX medium");
+  if (d.wall_mask >= 64u) return bad("wall_mask has bits above face 5");
+  if (d.n_emitters < 1 || d.n_emitters > DTS_MAX_EMITTERS) return bad("n_emitters must be 1..8");
+  for (int e = 0; e < d.n_emitters; ++e)
+    if (!(d.em_energy[e] >= 0.0f)) return bad("emitter energy must be >= 0");
+  if (d.camera_kind != DTS_CAMERA_PINHOLE && d.camera_kind != DTS_CAMERA_SPHERE_DETECTOR) return bad("unknown camera_kind");
+  if (d.width < 1 || d.height < 1) return bad("width/height must be >= 1");
+  if (d.camera_kind == DTS_CAMERA_PINHOLE && !(d.fov_y_deg > 0.0f && d.fov_y_deg < 180.0f)) return bad("fov must be in (0,180)");
+  if (d.camera_kind == DTS_CAMERA_SPHERE_DETECTOR && !(d.det_radius > 0.0f)) return bad("det_radius must be > 0");
+  if (d.crop[0] < 0 || d.crop[1] < 0 || d.crop[2] > d.width || d.crop[3] > d.height || d.crop[2] <= d.crop[0] ||
+      d.crop[3] <= d.crop[1])
+    return bad("crop must be a non-empty sub-rectangle of the image");
+  if (!(d.t1 > d.t0) || d.n_bins < 1) return bad("need t1 > t0 and n_bins >= 1");
+  if (d.strategy != DTS_STRATEGY_DARTS && d.strategy != DTS_STRATEGY_VANILLA) return bad("unknown strategy");
+  if (d.n_ris != 8) return bad("n_ris must be 8 (PAPER.md:240)");
+  if (!(d.alpha >= 0.0f)) return bad("alpha must be >= 0");
+  if (d.max_bounces < 1 || d.max_bounces > 65536) return bad("max_bounces must be 1..65536");
+  if (d.direction_mode != DTS_DIR_REUSE && d.direction_mode != DTS_DIR_SPLIT) return bad("unknown direction_mode");
+  if (d.spp_mode != DTS_SPP_PER_CELL && d.spp_mode != DTS_SPP_PER_PIXEL) return bad("unknown spp_mode");
+  if (!(d.parity_r_excl >= 0.0f) || !(d.parity_s_excess >= 0.0f)) return bad("parity restrictions must be >= 0");
+  return DTS_OK;
+}
+
+static void derive(const dts_scene_desc& d, DevScene& S) {
+  memset(&S, 0, sizeof S);
+  const double ss = d.sigma_s, sa = d.sigma_a, g = d.g, st = ss + sa;
+  const double D = 1.0 / (3.0 * (sa + ss * (1.0 - g)));  // E9
+  S.sigma_s = d.sigma_s;
+  S.sigma_a = d.sigma_a;
+  S.sigma_t = (float)st;
+  S.albedo = (float)(ss / st);
+  S.g = d.g;
+  S.inv_sigma_t = (float)(1.0 / st);
+  S.hg_k = (float)((1.0 - g * g) / (4.0 * M_PI));
+  S.hg_1pg2 = (float)(1.0 + g * g);
+  S.hg_2g = (float)(2.0 * g);
+  S.hg_1mg2 = (float)(1.0 - g * g);
+  S.hg_1mg = (float)(1.0 - g);
+  S.hg_1pg = (float)(1.0 + g);
+  S.neg_inv4D_log2e = (float)(-M_LOG2E / (4.0 * D));
+  S.neg_sa_log2e = (float)(-sa * M_LOG2E);
+  S.medium_shape = d.medium_shape;
+  for (int i = 0; i < 3; ++i) {
+    S.center[i] = d.center[i];
+    S.bmin[i] = d.bmin[i];
+    S.bmax[i] = d.bmax[i];
+    S.cam_pos[i] = d.cam_pos[i];
+  }
+  S.radius2 = d.radius * d.radius;
+  S.wall_mask = d.wall_mask;
+  for (int f = 0; f < 6; ++f) S.wall_albedo[f] = d.wall_albedo[f];
+  S.n_emitters = d.n_emitters;
+  for (int e = 0; e < d.n_emitters; ++e) {
+    for (int i = 0; i < 3; ++i) S.em_pos[e][i] = d.em_pos[e][i];
+    S.em_t[e] = d.em_t[e];
+    S.em_k[e] = (float)((double)d.em_energy[e] / (4.0 * M_PI) * d.n_emitters);
+  }
+  S.camera_kind = d.camera_kind;
+  double cam[3] = {d.cam_pos[0], d.cam_pos[1], d.cam_pos[2]}, la[3] = {d.look_at[0], d.look_at[1], d.look_at[2]},
+         up[3] = {d.up[0], d.up[1], d.up[2]};
+  double fwd[3], right[3], upc[3];
+  vsub(la, cam, fwd);
+  vnorm(fwd);
+  vcross(fwd, up, right);
+  vnorm(right);
+  vcross(right, fwd, upc);
+  for (int i = 0; i < 3; ++i) {
+    S.fwd[i] = (float)fwd[i];
+    S.right[i] = (float)right[i];
+    S.upc[i] = (float)upc[i];
+  }
+  S.tan_half = (float)std::tan(0.5 * (double)d.fov_y_deg * M_PI / 180.0);
+  S.aspect = (float)((double)d.width / d.height);
+  S.width = d.width;
+  S.height = d.height;
+  S.det_radius = d.det_radius;
+  for (int i = 0; i < 4; ++i) S.crop[i] = d.crop[i];
+  S.t0 = d.t0;
+  S.dt = ((double)d.t1 - (double)d.t0) / d.n_bins;
+  S.n_bins = d.n_bins;
+  S.warped = d.warped ? 1 : 0;
+  S.strategy = d.strategy;
+  S.direction_mode = d.direction_mode;
+  S.spp_mode = d.spp_mode;
+  S.max_bounces = d.max_bounces;
+  S.alpha = d.alpha;
+  S.r_excl = d.parity_r_excl;
+  S.s_excess = d.parity_s_excess;
+}
+
+// ============================================================== C ABI
+extern "C" {
+
+int32_t dts_abi_version(void) { return DTS_ABI_VERSION; }
+
+const char* dts_status_string(dts_status s) {
+  switch (s) {
+    case DTS_OK: return "DTS_OK";
+    case DTS_E_INVALID_ARG: return "DTS_E_INVALID_ARG";
+    case DTS_E_STATE: return "DTS_E_STATE";
+    case DTS_E_CUDA: return "DTS_E_CUDA";
+    case DTS_E_OOM: return "DTS_E_OOM";
+    case DTS_E_RANGE: return "DTS_E_RANGE";
+  }
+  return "DTS_E_UNKNOWN";
+}
+
+const char* dts_last_error(void) { return g_last_error.c_str(); }
+
+dts_status dts_scene_create(const dts_scene_desc* desc, dts_scene_t* out) {
+  if (!out) return fail(DTS_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!desc) return fail(DTS_E_INVALID_ARG, "desc is NULL");
+  dts_status st = validate(*desc);
+  if (st != DTS_OK) return st;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10) return fail(DTS_E_CUDA, "libdts needs an sm_100 (Blackwell) device");
+  dts_scene* s = new dts_scene();
+  s->desc = *desc;
+  derive(*desc, s->S);
+  s->num_sms = prop.multiProcessorCount;
+  s->device = dev;
+  if (cudaMalloc(&s->d_work, sizeof(unsigned long long)) != cudaSuccess) {
+    delete s;
+    return fail(DTS_E_OOM, "cudaMalloc(work counter) failed");
+  }
+  *out = s;
+  return DTS_OK;
+}
+
+dts_status dts_scene_destroy(dts_scene_t s) {
+  if (!s) return DTS_OK;
+  cudaDeviceSynchronize();
+  cudaFree(s->d_table);
+  cudaFree(s->d_work);
+  cudaFree(s->d_hist_host);
+  cudaFree(s->d_ctr_host);
+  delete s;
+  return DTS_OK;
+}
+
+dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream) {
+  if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
+  const dts_scene_desc& d = s->desc;
+  int nr = 16, ns = 16;
+  double st = (double)d.sigma_s + d.sigma_a;
+  double smin = 1e-2 / st, smax;
+  float tmin = d.em_t[0];
+  for (int e = 1; e < d.n_emitters; ++e) tmin = std::fmin(tmin, d.em_t[e]);
+  smax = (double)d.t1 - tmin;
+  if (td) {
+    if (td->n_ratio > 0) nr = td->n_ratio;
+    if (td->n_s > 0) ns = td->n_s;
+    if (td->s_min > 0.0f) smin = td->s_min;
+    if (td->s_max > 0.0f) smax = td->s_max;
+  }
+  if (nr > 256 || ns > 256) return fail(DTS_E_INVALID_ARG, "table axes must be <= 256");
+  if (!(smax > smin)) return fail(DTS_E_INVALID_ARG, "table s_max must exceed s_min");
+  const size_t n = (size_t)nr * ns * DTS_TABLE_COS_BINS;
+  if (n != s->table_n) {
+    cudaFree(s->d_table);
+    s->d_table = nullptr;
+    s->table_n = 0;
+    if (cudaMalloc(&s->d_table, n * sizeof(uint16_t)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(table) failed");
+    s->table_n = n;
+  }
+  TableParams P;
+  P.sigma_s = d.sigma_s;
+  P.sigma_a = d.sigma_a;
+  P.sigma_t = st;
+  P.D = 1.0 / (3.0 * ((double)d.sigma_a + (double)d.sigma_s * (1.0 - (double)d.g)));
+  P.smin = smin;
+  P.smax = smax;
+  P.nr = nr;
+  P.ns = ns;
+  table_build_kernel<<<nr * ns, 256, 0, (cudaStream_t)stream>>>(P, s->d_table);
+  CUDA_TRY(cudaGetLastError());
+  s->S.nr = nr;
+  s->S.ns = ns;
+  s->S.ln_smin = (float)std::log(smin);
+  s->S.inv_dls = (float)(ns / (std::log(smax) - std::log(smin)));
+  return DTS_OK;
+}
+
+size_t dts_table_size(dts_scene_t s) { return s ? s->table_n : 0; }
+
+dts_status dts_table_export(dts_scene_t s, uint16_t* host_q, size_t n) {
+  if (!s || !host_q) return fail(DTS_E_INVALID_ARG, "NULL argument");
+  if (!s->d_table) return fail(DTS_E_STATE, "table not built");
+  if (n != s->table_n) return fail(DTS_E_INVALID_ARG, "n must equal dts_table_size()");
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(host_q, s->d_table, n * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+  return DTS_OK;
+}
+
+size_t dts_hist_cells(dts_scene_t s) {
+  if (!s) return 0;
+  const dts_scene_desc& d = s->desc;
+  return (size_t)(d.crop[2] - d.crop[0]) * (size_t)(d.crop[3] - d.crop[1]) * (size_t)d.n_bins;
+}
+
+dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* d_hist,
+                      float* d_hist_sq, uint64_t* d_counters, void* stream) {
+  g_last_launches = 0;
+  if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
+  if (!d_hist) return fail(DTS_E_INVALID_ARG, "d_hist is NULL");
+  if (spp == 0 || se > spp || sb > se) return fail(DTS_E_RANGE, "need 0 <= sample_begin <= sample_end <= spp, spp > 0");
+  if (sb == se) return DTS_OK;
+  const dts_scene_desc& d = s->desc;
+  const bool darts = d.strategy == DTS_STRATEGY_DARTS;
+  if (darts && !s->d_table) return fail(DTS_E_STATE, "dts_table_build must run before a DARTS render");
+  const uint64_t npix = (uint64_t)(d.crop[2] - d.crop[0]) * (uint64_t)(d.crop[3] - d.crop[1]);
+  const uint64_t ns = se - sb;
+  const uint64_t Npix = (uint64_t)d.width * d.height;
+  // path ids must fit 64 bits: (s * Npix + p) * B + b
+  const double idmax = ((double)spp * (double)Npix + (double)Npix) * (double)d.n_bins;
+  if (idmax > 1.8e19) return fail(DTS_E_RANGE, "path id space exceeds 64 bits");
+  RenderParams P;
+  memset(&P, 0, sizeof P);
+  P.S = s->S;
+  P.S.seed_lo = (uint32_t)seed;
+  P.S.seed_hi = (uint32_t)(seed >> 32);
+  P.tab = s->d_table;
+  P.hist = d_hist;
+  P.hist_sq = d_hist_sq;
+  P.counters = reinterpret_cast<unsigned long long*>(d_counters);
+  P.work = s->d_work;
+  P.s_begin = sb;
+  P.n_s = ns;
+  P.spp = spp;
+  P.npix = (uint32_t)npix;
+  P.cw = (uint32_t)(d.crop[2] - d.crop[0]);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (darts) {
+    P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix * (uint64_t)d.n_bins * ns : npix * ns;
+    const size_t tbytes = s->table_n * sizeof(uint16_t);
+    P.table_u4 = (uint32_t)(tbytes / 16);
+    const bool smem = tbytes <= 200 * 1024;
+    int blocks_per_sm = 1;
+    if (smem) {
+      CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<true>, kBlock, tbytes));
+    } else {
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<false>, kBlock, 0));
+    }
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    uint64_t grid = (uint64_t)s->num_sms * blocks_per_sm;
+    const uint64_t need = (P.total + 31) / 32 / (kBlock / 32) + 1;
+    if (grid > need) grid = need;
+    CUDA_TRY(cudaMemsetAsync(s->d_work, 0, sizeof(unsigned long long), st));
+    if (smem)
+      render_darts_kernel<true><<<(unsigned)grid, kBlock, tbytes, st>>>(P);
+    else
+      render_darts_kernel<false><<<(unsigned)grid, kBlock, 0, st>>>(P);
+    CUDA_TRY(cudaGetLastError());
+    g_last_launches = 1;
+    g_last_grid = (int)grid;
+    g_last_block = kBlock;
+    g_last_smem = smem ? (int)tbytes : 0;
+  } else {
+    P.total = npix * ns;
+    int bps = 1;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, render_vanilla_kernel, kBlock, 0));
+    uint64_t grid = (uint64_t)s->num_sms * (bps < 1 ? 1 : bps) * 4;
+    const uint64_t need = (P.total + kBlock - 1) / kBlock;
+    if (grid > need) grid = need;
+    render_vanilla_kernel<<<(unsigned)grid, kBlock, 0, st>>>(P);
+    CUDA_TRY(cudaGetLastError());
+    g_last_launches = 1;
+    g_last_grid = (int)grid;
+    g_last_block = kBlock;
+    g_last_smem = 0;
+  }
+  return DTS_OK;
+}
+
+dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* h_hist,
+                           uint64_t* h_counters, void* stream) {
+  if (!s || !h_hist) return fail(DTS_E_INVALID_ARG, "NULL argument");
+  const size_t n = dts_hist_cells(s);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (s->d_hist_host_n != n) {
+    cudaFree(s->d_hist_host);
+    s->d_hist_host = nullptr;
+    s->d_hist_host_n = 0;
+    if (cudaMalloc(&s->d_hist_host, n * sizeof(float)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(hist) failed");
+    s->d_hist_host_n = n;
+  }
+  if (!s->d_ctr_host && cudaMalloc(&s->d_ctr_host, DTS_NUM_COUNTERS * sizeof(uint64_t)) != cudaSuccess)
+    return fail(DTS_E_OOM, "cudaMalloc(counters) failed");
+  CUDA_TRY(cudaMemsetAsync(s->d_hist_host, 0, n * sizeof(float), st));
+  CUDA_TRY(cudaMemsetAsync(s->d_ctr_host, 0, DTS_NUM_COUNTERS * sizeof(uint64_t), st));
+  dts_status r = dts_render(s, spp, seed, sb, se, s->d_hist_host, nullptr, s->d_ctr_host, stream);
+  if (r != DTS_OK) return r;
+  CUDA_TRY(cudaMemcpyAsync(h_hist, s->d_hist_host, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (h_counters)
+    CUDA_TRY(cudaMemcpyAsync(h_counters, s->d_ctr_host, DTS_NUM_COUNTERS * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DTS_OK;
+}
+
+dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, dts_debug_out* d_out, void* stream) {
+  if (!s || (n > 0 && (!d_in || !d_out)) || n < 0) return fail(DTS_E_INVALID_ARG, "bad arguments");
+  if (n == 0) return DTS_OK;
+  if (s->desc.strategy == DTS_STRATEGY_DARTS && !s->d_table) return fail(DTS_E_STATE, "table not built");
+  static uint16_t* d_dummy = nullptr;
+  const uint16_t* tab = s->d_table;
+  if (!tab) {
+    if (!d_dummy) CUDA_TRY(cudaMalloc(&d_dummy, 256 * sizeof(uint16_t)));
+    CUDA_TRY(cudaMemsetAsync(d_dummy, 0, 256 * sizeof(uint16_t), (cudaStream_t)stream));
+    tab = d_dummy;
+  }
+  debug_kernel<true><<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(s->S, tab, n, d_in, d_out);
+  CUDA_TRY(cudaGetLastError());
+  return DTS_OK;
+}
+
+dts_status dts_last_launch(int32_t* n_launches, int32_t* grid, int32_t* block, int32_t* smem_bytes) {
+  if (n_launches) *n_launches = g_last_launches;
+  if (grid) *grid = g_last_grid;
+  if (block) *block = g_last_block;
+  if (smem_bytes) *smem_bytes = g_last_smem;
+  return DTS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+- dts_sample_debug vs the oracle on >= 1e5 seeded records per config: every
+  sampled distance, direction and pdf to relative 1e-4 (north_star), records
+  whose oracle decision margin is < 1e-5 reported, not failed.
+- rendered histograms vs the oracle on the SAME Philox keys: relative L2 <= 1 %
+  at sizes the oracle finishes in seconds and, at full BASELINE sizes in the
+  bench launch configuration, on sampled crops.
+- independent seeds: >= 99 % of cells within 3 SE on restricted estimands.
+- edge cases of the boundary.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import dts_inputs as I
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dts():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2402_03106_b200 import dts as D
+    return D
+
+
+def _scene(dts, c):
+    sc = dts.Scene(c)
+    if c["strategy"] == "darts":
+        sc.table_build()
+    return sc
+
+
+# ------------------------------------------------------------------ EDA table
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_table_matches_oracle(dts, oracle, cfg):
+    c = I.as_f32(I.config(cfg))
+    sc = _scene(dts, c)
+    qg = sc.table_export().astype(np.int64)
+    qo, _ = oracle.build_table(c)
+    qo = qo.astype(np.int64)
+    diff = np.abs(qg - qo)
+    assert diff.max() <= 1 and np.count_nonzero(diff) <= 2, np.count_nonzero(diff)
+
+
+# ------------------------------------------------------------------ debug parity
+MARGIN = 1e-5
+
+
+def _rel(a, b, floor):
+    return np.abs(a - b) / np.maximum(np.abs(b), floor)
+
+
+@pytest.mark.parametrize("cfg,mode", [(1, "reuse"), (2, "reuse"), (3, "split"), (3, "reuse"), (4, "reuse"),
+                                      (5, "split")])
+def test_sample_debug_parity(dts, oracle, cfg, mode):
+    c = I.as_f32(I.config(cfg, direction_mode=mode))
+    sc = _scene(dts, c)
+    n = 100_000
+    recs = I.debug_records(c, n, seed=100 + cfg)
+    g = dts.debug(sc, recs)
+    qo, _ = oracle.build_table(c)     # the oracle's own table (bit-equal to the GPU's, test above)
+    o = oracle.debug(c, qo, recs)
+    # decisions taken in fp32 vs fp64 near a boundary
+    safe = ((o["m_event"] > MARGIN) & (o["m_select"] > MARGIN) & (o["m_tech"] > MARGIN) &
+            (o["m_cell"] > MARGIN * 16) & (o["m_hgbin"] > MARGIN * 128) & (o["m_valid"] > MARGIN) &
+            (o["m_conn"] > MARGIN) & (o["m_term"] > MARGIN))
+    assert safe.mean() > 0.99, safe.mean()
+    s = safe
+    report = {}
+    # ---- direction stage
+    assert (g["tech"][s] == o["tech"][s]).all()
+    for k in ("p_hg", "p_eda", "p_mix", "gamma", "beta_dir", "wconn"):
+        r = _rel(g[k][s], o[k][s], 1e-6)
+        report[k] = float(r.max())
+        assert np.quantile(r, 0.9999) < 1e-4 and r.max() < 1e-3, (k, r.max())
+    for k in ("wc", "ww"):
+        err = np.abs(g[k][s] - o[k][s]).max()
+        report[k] = float(err)
+        assert err < 1e-4, (k, err)
+    # ---- intersection
+    assert (g["hit"][s] == o["hit"][s]).all()
+    fin = s & np.isfinite(o["t_hi"])
+    for k in ("t_lo", "t_hi"):
+        r = _rel(g[k][fin], o[k][fin], 1e-3)
+        assert r.size == 0 or r.max() < 1e-4, (k, r.max())
+    assert (np.isinf(g["t_hi"][s]) == np.isinf(o["t_hi"][s])).all()
+    # ---- connection
+    assert (g["conn_valid"][s] == o["conn_valid"][s]).all()
+    cv = s & (o["conn_valid"] == 1)
+    assert cv.mean() > 0.02
+    for k in ("S", "t", "p_t", "contrib"):
+        r = _rel(g[k][cv], o[k][cv], 1e-30)
+        report[k] = float(np.quantile(r, 0.9999))
+        assert np.quantile(r, 0.999) < 1e-4 and np.quantile(r, 0.99999) < 1e-3, (k, np.quantile(r, 0.999))
+    assert np.abs(g["x_ell"][cv] - o["x_ell"][cv]).max() < 1e-4 * max(1.0, np.abs(o["x_ell"][cv]).max())
+    nee = s & (o["nee"] > 0)
+    if nee.any():
+        r = _rel(g["nee"][nee], o["nee"][nee], 1e-30)
+        assert r.max() < 1e-4
+    # ---- distance (RIS)
+    assert (g["event"][s] == o["event"][s]).all()
+    med = s & (o["event"] == 1)
+    assert med.mean() > 0.05
+    r = _rel(g["p_m"][s], o["p_m"][s], 1e-6)
+    assert r.max() < 1e-4
+    r = _rel(g["cand_d"][med], o["cand_d"][med], 1e-3)
+    report["cand_d"] = float(r.max())
+    assert r.max() < 1e-4
+    err = np.abs(g["cand_wn"][med] - o["cand_wn"][med])
+    report["cand_wn"] = float(err.max())
+    assert err.max() < 1e-4
+    assert (g["istar"][med] == o["istar"][med]).all()
+    for k in ("d", "beta_ris"):
+        r = _rel(g[k][med], o[k][med], 1e-3 if k == "d" else 1e-30)
+        report[k] = float(r.max())
+        assert np.quantile(r, 0.9999) < 1e-4 and r.max() < 1e-3, (k, r.max())
+    assert np.abs(g["x_next"][med] - o["x_next"][med]).max() < 1e-4 * max(1.0, np.abs(o["x_next"][med]).max())
+    assert (g["terminate"][s] == o["terminate"][s]).all()
+    print(f"cfg{cfg}/{mode}: safe {safe.mean():.5f} max-rel {report}")
+
+
+# ------------------------------------------------------------------ histograms, same keys
+SAME_KEY = [
+    ("cfg1_full", lambda: I.config(1), None),
+    ("cfg2_full", lambda: I.config(2), None),
+    ("cfg2_ragged_crop", lambda: I.config(2, crop=(13, 20, 51, 37), spp=5), None),
+    ("cfg3_small", lambda: I.small(I.config(3), 6, 5, n_bins=64, t1=8.5), 8),
+    ("cfg4_full", lambda: I.config(4, spp=16), None),
+    ("cfg5_small_pixelmode", lambda: I.small(I.config(5), 7, 9, n_bins=120, t1=12.0), 150),
+    ("cfg3_reuse", lambda: I.small(I.config(3, direction_mode="reuse"), 4, 4, n_bins=32, t1=6.0), 16),
+    ("cfg1_vanilla", lambda: I.config(1, strategy="vanilla"), 4096),
+    ("cfg4_vanilla", lambda: I.small(I.config(4, strategy="vanilla"), 16, 16), 256),
+]
+
+
+def _same_key(dts, oracle, c, spp, seed):
+    sc = _scene(dts, c)
+    h, _, ctr = dts.render_to_tensor(sc, spp, seed)
+    torch.cuda.synchronize()
+    g = h.cpu().numpy().astype(np.float64)
+    q = oracle.build_table(c)[0] if c["strategy"] == "darts" else None
+    o = oracle.render(c, q, spp, seed, sq=False)
+    return g, o, dts.counters_dict(ctr)
+
+
+@pytest.mark.parametrize("name,mk,spp", SAME_KEY, ids=[s[0] for s in SAME_KEY])
+def test_render_same_key(dts, oracle, name, mk, spp):
+    c = I.as_f32(mk())
+    spp = spp or c["spp"]
+    g, o, ctr = _same_key(dts, oracle, c, spp, c["seed"])
+    ho = o["hist"]
+    rel = np.linalg.norm(g - ho) / np.linalg.norm(ho)
+    st = o["stats"]
+    assert ctr["paths"] == st["paths"]
+    # grazing primary rays may flip between fp32 and fp64
+    assert abs(ctr["camera_miss"] - st["camera_miss"]) <= 1e-5 * st["paths"] + 2
+    # vertex counts agree up to the few paths whose fp32/fp64 decisions diverge
+    assert abs(ctr["vertices"] - st["vertices"]) <= 0.02 * st["vertices"]
+    print(f"{name}: same-key relative L2 {rel:.3e}, vertices gpu {ctr['vertices']} oracle {st['vertices']}")
+    assert rel <= 0.01
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, bench launch config
+FULL = [
+    ("cfg3_full_crop", 3, (126, 126, 130, 130)),
+    ("cfg5_full_crop", 5, (510, 510, 514, 514)),
+    ("cfg4_full_crop", 4, (250, 250, 262, 262)),
+]
+
+
+@pytest.mark.parametrize("name,cfg,crop", FULL, ids=[f[0] for f in FULL])
+def test_full_size_sampled_crop(dts, oracle, name, cfg, crop):
+    """The full-size render, launched exactly as bench.py launches it, compared
+    on a crop the oracle renders with the same keys."""
+    c = I.as_f32(I.config(cfg))
+    sc = _scene(dts, c)
+    h, _, ctr = dts.render_to_tensor(sc, c["spp"], c["seed"])
+    torch.cuda.synchronize()
+    g = h.cpu().numpy().astype(np.float64)
+    assert np.isfinite(g).all() and (g >= 0).all()
+    cnt = dts.counters_dict(ctr)
+    npix = c["width"] * c["height"]
+    exp_paths = npix * c["spp"] * (c["n_bins"] if c["spp_mode"] == "cell" else 1)
+    assert cnt["paths"] == exp_paths
+    if crop is None:
+        crop = (0, 0, c["width"], c["height"])
+    cc = dict(c, crop=crop)
+    qo, _ = oracle.build_table(cc)
+    o = oracle.render(cc, qo, c["spp"], c["seed"], sq=False)["hist"]
+    x0, y0, x1, y1 = crop
+    gg = g[y0:y1, x0:x1]
+    rel = np.linalg.norm(gg - o) / np.linalg.norm(o)
+    print(f"{name}: crop same-key rel L2 {rel:.3e}; counters {cnt}")
+    assert rel <= 0.01
+
+
+# ------------------------------------------------------------------ independent seeds, 3 SE
+INDEP = [
+    ("cfg1", lambda: I.config(1, parity_r_excl=0.3, parity_s_excess=0.05), 8192, 20000),
+    ("cfg4", lambda: I.small(I.config(4, parity_r_excl=0.3, parity_s_excess=0.05), 4, 4), 20000, 20000),
+    ("cfg2", lambda: I.small(I.config(2, parity_s_excess=0.05), 6, 6, n_bins=24, t1=9.0), 4000, 4000),
+    ("cfg3_split", lambda: I.small(I.config(3, parity_s_excess=0.05), 4, 4, n_bins=16, t1=6.0), 2000, 2000),
+    ("cfg5_split", lambda: I.small(I.config(5, parity_s_excess=0.05, spp_mode="cell"), 2, 2, n_bins=8, t1=16.0),
+     600, 600),
+]
+
+
+@pytest.mark.parametrize("name,mk,ng,no", INDEP, ids=[s[0] for s in INDEP])
+def test_render_independent_seeds(dts, oracle, name, mk, ng, no):
+    c = I.as_f32(mk())
+    sc = _scene(dts, c)
+    h, hs, _ = dts.render_to_tensor(sc, ng, 1001, with_sq=True)
+    torch.cuda.synchronize()
+    g, gs = h.cpu().numpy().astype(np.float64), hs.cpu().numpy().astype(np.float64)
+    qo, _ = oracle.build_table(c)
+    o = oracle.render(c, qo, no, 2002)
+    se_g = np.sqrt(np.maximum(gs - g ** 2, 0) / (ng - 1))
+    se_o = np.sqrt(np.maximum(o["hist_sq"] - o["hist"] ** 2, 0) / (no - 1))
+    m = (g > 0) | (o["hist"] > 0)
+    z = ((g - o["hist"]) / np.sqrt(se_g ** 2 + se_o ** 2 + 1e-300))[m]
+    frac = np.mean(np.abs(z) < 3)
+    print(f"{name}: cells {m.sum()} within-3SE {frac:.4f} mean z {z.mean():+.3f}")
+    assert (np.abs(z) >= 3).sum() <= max(1, int(0.01 * m.sum()))
+
+
+# ------------------------------------------------------------------ boundary edge cases
+def test_edge_cases(dts):
+    c = I.as_f32(I.small(I.config(4), 4, 4))
+    sc = dts.Scene(c)
+    h = torch.zeros(sc.hist_shape(), device="cuda")
+    with pytest.raises(dts.DtsError, match="DTS_E_STATE"):
+        sc.render(8, 1, 0, 8, h)                          # DARTS before dts_table_build
+    sc.table_build()
+    sc.render(8, 1, 3, 3, h)                              # empty sample range: no-op
+    torch.cuda.synchronize()
+    assert float(h.abs().sum()) == 0.0
+    with pytest.raises(dts.DtsError, match="DTS_E_RANGE"):
+        sc.render(8, 1, 0, 9, h)
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        sc.render(8, 1, 0, 8, 0)
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        dts.Scene(dict(c, g=1.0))
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        dts.Scene(dict(c, crop=(0, 0, 5, 4)))
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        dts.Scene(dict(c, n_ris=16))
+
+
+def test_sharding_sums_and_accumulates(dts):
+    """Disjoint sample ranges are disjoint Philox key ranges: shard renders
+    accumulate (+=) into one buffer and equal the full render up to fp32
+    summation order."""
+    c = I.as_f32(I.small(I.config(3), 16, 16, n_bins=64, t1=9.0))
+    sc = _scene(dts, c)
+    full, _, cf = dts.render_to_tensor(sc, 32, 5)
+    h = torch.zeros(sc.hist_shape(), device="cuda")
+    ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    for a, b in [(0, 7), (7, 8), (8, 30), (30, 32)]:
+        sc.render(32, 5, a, b, h, None, ctr)
+    torch.cuda.synchronize()
+    f, s = full.cpu().numpy(), h.cpu().numpy()
+    assert np.linalg.norm(f - s) / np.linalg.norm(f) < 1e-5
+    assert dts.counters_dict(ctr) == dts.counters_dict(cf)
+
+
+def test_render_host_e2e_matches_device(dts):
+    c = I.as_f32(I.small(I.config(5), 8, 8, n_bins=100, t1=10.0))
+    sc = _scene(dts, c)
+    d, _, ctr = dts.render_to_tensor(sc, 64, 3)
+    hh = np.zeros(sc.hist_cells(), np.float32)
+    hc = np.zeros(dts.NUM_COUNTERS, np.uint64)
+    sc.render_host(64, 3, 0, 64, hh, hc)
+    assert np.linalg.norm(hh - d.cpu().numpy().ravel()) <= 1e-5 * np.linalg.norm(hh)
+    assert int(hc[2]) == dts.counters_dict(ctr)["vertices"]
+
+
+def test_single_pixel_single_bin_and_table_in_global_memory(dts, oracle):
+    """Degenerate sizes (1 pixel, 1 bin) and a 32x32 table too large for shared
+    memory (the L1/global path of the kernel) still match the oracle."""
+    c = I.as_f32(I.config(4, crop=(256, 256, 257, 257), table_nr=32, table_ns=32))
+    sc = _scene(dts, c)
+    assert sc.table_size() == 32 * 32 * 256
+    h, _, _ = dts.render_to_tensor(sc, 4096, 8)
+    torch.cuda.synchronize()
+    qo, _ = oracle.build_table(c)
+    o = oracle.render(c, qo, 4096, 8, sq=False)["hist"]
+    g = h.cpu().numpy()
+    assert abs(g.sum() - o.sum()) <= 0.01 * o.sum()

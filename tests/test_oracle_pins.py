@@ -447,6 +447,7 @@ def test_connections_land_in_their_bin(oracle, cfg):
     c = I.as_f32(I.config(cfg))
     q, _ = oracle.build_table(c)
     rec = I.debug_records(c, 20_000, seed=cfg)
+    rec["w"] /= np.linalg.norm(rec["w"], axis=1, keepdims=True)   # exactly unit in fp64
     out = oracle.debug(c, q, rec)
     v = out["conn_valid"] == 1
     assert v.mean() > 0.05
