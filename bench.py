@@ -131,6 +131,8 @@ def run_gpu(args):
     c = I.as_f32(I.config(args.config))
     if args.direction_mode:
         c["direction_mode"] = args.direction_mode
+    if args.spp:
+        c["spp"] = args.spp
     spp = c["spp"]
     sb, se = _shard(spp, rank, world)
     sc = dts.Scene(c)
@@ -372,6 +374,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--spp", type=int, default=None, help="override spp (profiling runs only; not a bench line)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -398,7 +398,7 @@ static double connect(const or_scene* sc, const derived* dv, const pstate* ps, c
                       double wconn, double lo, double hi, int hitc, double u7, or_debug_out* dbg,
                       int* nonempty) {
   *nonempty = 0;
-  if (dbg) { dbg->S_lo = dbg->S_hi = dbg->S = dbg->t = dbg->p_t = 0.0; dbg->contrib = 0.0; dbg->conn_valid = 0; dbg->m_conn = INFINITY; }
+  if (dbg) { dbg->S_lo = dbg->S_hi = dbg->S = dbg->t = dbg->p_t = 0.0; dbg->contrib = 0.0; dbg->conn_valid = 0; dbg->m_conn = INFINITY; dbg->m_cond = INFINITY; }
   if (hitc == OR_HIT_MISS) return 0.0;
   double Cvec[3];
   sub3(ps->xe, ps->x, Cvec);
@@ -437,7 +437,18 @@ static double connect(const or_scene* sc, const derived* dv, const pstate* ps, c
     t = or_polar_distance(C, S, q / C); /* E21 */
     if (C == 0.0) t = 0.5 * S;
     pt = pS * (S - q) / (S - t); /* E22 with the Jacobian of R2 */
-    if (dbg) { dbg->S = S; }
+    if (dbg) {
+      dbg->S = S;
+      /* conditioning (not a decision): 1 / kappa with kappa the sum of the
+       * amplification factors S/(S-q), S/(S_hi-S_lo) and (bin-bound) S/(S-C)
+       * of the differences E21/E22 form; an fp32 evaluation of t and p_t is
+       * accurate to ~1e-7 kappa */
+      const int lo_bin = (ps->Rm - ps->E) >= Slo_geo && !(sc->parity_s_excess > 0.0 && C + sc->parity_s_excess > ps->Rm - ps->E);
+      const int hi_bin = (ps->RM - ps->E) <= Shi_geo;
+      double kappa = S / (S - q) + ((isinf(S_hi) || (lo_bin && hi_bin)) ? 0.0 : S / (S_hi - S_lo)) +
+                     (lo_bin ? S / (S - C) : 0.0);
+      dbg->m_cond = 1.0 / kappa;
+    }
   } else {
     /* R17: unwarped camera vertex; the recorded time excludes the camera leg,
      * so the condition is on r2 = |x(t) - xe| in [Rm, RM): at most two
@@ -477,6 +488,14 @@ static double connect(const or_scene* sc, const derived* dv, const pstate* ps, c
       dbg->S_hi = Z;
       dbg->m_conn = INFINITY; /* decision margin: distance of each interval from empty */
       for (int i = 0; i < ni; ++i) dbg->m_conn = fmin(dbg->m_conn, fabs(ib[i] - ia[i]) / fmax(1.0, fabs(ib[i])));
+      /* conditioning of the R17 intervals (not a decision): the square roots of
+       * q^2 - C^2 + R^2 and the interval widths against their positions */
+      double kappa = 0.0;
+      if (ni >= 1) kappa = fmax(kappa, C * C / radM);
+      if (ni == 2) kappa = fmax(kappa, C * C / (q * q - C * C + ps->Rm * ps->Rm));
+      for (int i = 0; i < ni; ++i)
+        if (ib[i] > ia[i]) kappa += fabs(ib[i]) / (ib[i] - ia[i]);
+      dbg->m_cond = kappa > 0.0 ? 1.0 / kappa : INFINITY;
     }
     if (!(Z > 0.0)) return 0.0;
     double v = u7 * Z;
@@ -525,7 +544,7 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
   if (dbg) {
     memset(dbg, 0, sizeof(*dbg));
     dbg->m_event = dbg->m_select = dbg->m_tech = dbg->m_cell = dbg->m_hgbin = INFINITY;
-    dbg->m_valid = dbg->m_conn = dbg->m_term = INFINITY;
+    dbg->m_valid = dbg->m_conn = dbg->m_term = dbg->m_cond = INFINITY;
     dbg->istar = -1;
   }
   /* ---- step 2: direction ---- */

@@ -79,7 +79,7 @@ typedef struct {
   double d, x_next[3], beta_ris, E_next, beta_out;
   int32_t terminate;
   /* decision margins (oracle only) */
-  double m_event, m_select, m_tech, m_cell, m_hgbin, m_valid, m_conn, m_term;
+  double m_event, m_select, m_tech, m_cell, m_hgbin, m_valid, m_conn, m_term, m_cond;
 } or_debug_out;
 
 typedef struct {

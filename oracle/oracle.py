@@ -103,6 +103,7 @@ DEBUG_OUT = np.dtype([
     ("beta_out", np.float64), ("terminate", np.int32),
     ("m_event", np.float64), ("m_select", np.float64), ("m_tech", np.float64), ("m_cell", np.float64),
     ("m_hgbin", np.float64), ("m_valid", np.float64), ("m_conn", np.float64), ("m_term", np.float64),
+    ("m_cond", np.float64),
 ], align=True)
 
 _MED = {"infinite": 0, "sphere": 1, "box": 2}

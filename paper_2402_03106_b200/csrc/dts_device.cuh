@@ -103,6 +103,14 @@ __device__ __forceinline__ float neg_log1m(float x) {
   const float ser = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 0.2f, 0.25f), 0.33333333f), 0.5f), 1.0f);
   return x < 0.03125f ? ser : big;
 }
+// -ln(1 - x) with 1 - x supplied separately (omx, formed without cancellation
+// by the caller: for x = u p with p = 1 - T, 1 - x = (1 - u) + u T exactly
+// enough even when x -> 1).
+__device__ __forceinline__ float neg_log1m2(float x, float omx) {
+  const float big = -__log2f(omx) * kLn2;
+  const float ser = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 0.2f, 0.25f), 0.33333333f), 0.5f), 1.0f);
+  return x < 0.03125f ? ser : big;
+}
 // 1 - exp(-y) for y >= 0
 __device__ __forceinline__ float one_m_exp(float y) {
   const float big = 1.0f - exp2f(-y * kLog2e);
@@ -168,9 +176,11 @@ __device__ __forceinline__ int intersect(const DevScene& S, f3 o, f3 d, float& l
     const float disc = b * b - c;
     if (!(disc > 0.0f)) return HIT_MISS;
     const float s = sqrtf(disc);
-    const float tf = -b + s;
+    // roots without cancellation: tf = s - b, or -c / (b + s) when b > 0; tn tf = c
+    const float tf = b > 0.0f ? -c * __fdividef(1.0f, b + s) : s - b;
     if (!(tf > 0.0f)) return HIT_MISS;
-    lo = fmaxf(-b - s, 0.0f);
+    const float tn = b > 0.0f ? -b - s : c * __fdividef(1.0f, tf);
+    lo = fmaxf(tn, 0.0f);
     hi = tf;
     return HIT_OPEN;
   }
@@ -410,27 +420,37 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const f3 plo = fma3(wc, clo, ps.x) - xe;
       const float rlo = sqrtf(dot(plo, plo));
       const float lo_m_C = clo + clo * (clo - 2.0f * q) * __fdividef(1.0f, rlo + C);
-      float Shi_geo = __int_as_float(0x7f800000);
+      float hi_m_C = __int_as_float(0x7f800000);
       if (isfinite(chi)) {
         const f3 phi_ = fma3(wc, chi, ps.x) - xe;
-        Shi_geo = chi + sqrtf(dot(phi_, phi_));
+        hi_m_C = chi + chi * (chi - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(phi_, phi_)) + C);
       }
-      float dlo = fmaxf((float)(ps.Rm - ps.E - (double)C), lo_m_C);  // S_lo - C
-      if (S.s_excess > 0.0f) dlo = fmaxf(dlo, S.s_excess);
+      // bin bounds relative to C in double: (Rm - E) - C, (RM - E) - C
+      const double dm_d = ps.Rm - ps.E - (double)C;
+      const double dM_d = ps.RM - ps.E - (double)C;
+      float dlo = (float)dm_d;
+      bool lo_bin = true;
+      if (lo_m_C > dlo) { dlo = lo_m_C; lo_bin = false; }
+      if (S.s_excess > 0.0f && S.s_excess > dlo) { dlo = S.s_excess; lo_bin = false; }
+      const bool hi_bin = (float)dM_d <= hi_m_C;
+      const float dhi = hi_bin ? (float)dM_d : hi_m_C;
+      // width S_hi - S_lo, exact to rounding when both bounds are bin bounds
+      const float width = (float)((hi_bin ? dM_d : (double)hi_m_C) - (lo_bin ? dm_d : (double)dlo));
       const float S_lo = C + dlo;
-      const float S_hi = fminf(resM, Shi_geo);
+      const float S_hi = C + dhi;
       if (DBG) { dbg->S_lo = S_lo; dbg->S_hi = S_hi; }
-      if (S_hi > S_lo) {
+      if (width > 0.0f) {
         ok = true;
         // truncated exponential on [S_lo, S_hi); e^{-st (S-S_lo)} = 1 - u7 span
         float L, pS;
-        if (isinf(S_hi)) {
+        if (isinf(dhi)) {
           L = neg_log1m(u7) * S.inv_sigma_t;
           pS = S.sigma_t * (1.0f - u7);
         } else {
-          const float span = one_m_exp(S.sigma_t * (S_hi - S_lo));
-          L = neg_log1m(u7 * span) * S.inv_sigma_t;
-          pS = S.sigma_t * (1.0f - u7 * span) * __fdividef(1.0f, span);
+          const float span = one_m_exp(S.sigma_t * width);
+          const float keep = fmaf(u7, fexp(-S.sigma_t * width), 1.0f - u7);  // 1 - u7 span
+          L = neg_log1m2(u7 * span, keep) * S.inv_sigma_t;
+          pS = S.sigma_t * keep * __fdividef(1.0f, span);
         }
         const float dSC = dlo + L;  // S - C
         const float Ssm = C + dSC;
@@ -488,7 +508,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
         up = fminf(up, 0.99999994f);
         (void)mm;
         const float span = one_m_exp(S.sigma_t * (ib - ia));
-        t = ia + neg_log1m(up * span) * S.inv_sigma_t;
+        t = ia + neg_log1m2(up * span, fmaf(up, fexp(-S.sigma_t * (ib - ia)), 1.0f - up)) * S.inv_sigma_t;
         pt = S.sigma_t * fexp(-S.sigma_t * (t - clo)) / Z;
       }
     }
@@ -528,6 +548,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   const float counts = (S.warped || ps.kind != KIND_CAMERA) ? 1.0f : 0.0f;
   const bool inf_hi = isinf(hi);
   const float p_m = inf_hi ? 1.0f : one_m_exp(S.sigma_t * (hi - lo));  // E12, R28
+  const float T_m = inf_hi ? 0.0f : fexp(-S.sigma_t * (hi - lo));      // 1 - p_m
   const float u0 = unif(r[0]);
   if (DBG) dbg->p_m = p_m;
   if (u0 < p_m) {
@@ -548,7 +569,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const uint32_t br3 = __brev((uint32_t)i) >> 29;
       const uint32_t v = (m2 + ((br3 * 32u + br5) << 16)) & 0xFFFFFFu;
       const float ui = (float)v * 5.9604644775390625e-08f;
-      d[i] = lo + neg_log1m(p_m * ui) * S.inv_sigma_t;  // E14 with the sign of R1
+      const float omu = (float)(0x1000000u - v) * 5.9604644775390625e-08f;  // 1 - u_i, exact
+      // E14 with the sign of R1: d = t_lo - ln(1 - p_m u) / sigma_t, 1 - p_m u = (1 - u) + u (1 - p_m)
+      d[i] = lo + neg_log1m2(p_m * ui, fmaf(ui, T_m, omu)) * S.inv_sigma_t;
       const float Delta = resM - counts * d[i];          // R4
       const float dq = d[i] - qd;
       const float r2i = fmaf(dq, dq, perp2);

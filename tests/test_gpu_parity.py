@@ -87,18 +87,29 @@ def test_sample_debug_parity(dts, oracle, cfg, mode):
     # ---- intersection
     assert (g["hit"][s] == o["hit"][s]).all()
     fin = s & np.isfinite(o["t_hi"])
+    # distances to the medium boundary: relative 1e-4, with an absolute floor of
+    # 1e-6 scene units (~10 fp32 ulps of a unit-scale coordinate: a vertex within
+    # 1e-3 of a boundary cannot locate it better in fp32)
     for k in ("t_lo", "t_hi"):
-        r = _rel(g[k][fin], o[k][fin], 1e-3)
-        assert r.size == 0 or r.max() < 1e-4, (k, r.max())
+        err = np.abs(g[k][fin] - o[k][fin])
+        assert err.size == 0 or (err <= 1e-4 * np.abs(o[k][fin]) + 1e-6).all(), (k, err.max())
     assert (np.isinf(g["t_hi"][s]) == np.isinf(o["t_hi"][s])).all()
     # ---- connection
     assert (g["conn_valid"][s] == o["conn_valid"][s]).all()
     cv = s & (o["conn_valid"] == 1)
     assert cv.mean() > 0.02
+    # fp32 conditioning of E21/E22 (oracle's m_cond = 1/kappa): where the
+    # differences S - C, S - q or a geometric S-range width are small against
+    # S, fp32 keeps ~1e-7 kappa relative accuracy.  Well-conditioned records
+    # (kappa <= 100) must meet 1e-4; every record must meet 1e-4 + 1e-5 kappa.
+    wellc = o["m_cond"][cv] >= 1e-2
+    assert wellc.mean() > 0.5
+    kappa = 1.0 / o["m_cond"][cv]
     for k in ("S", "t", "p_t", "contrib"):
         r = _rel(g[k][cv], o[k][cv], 1e-30)
-        report[k] = float(np.quantile(r, 0.9999))
-        assert np.quantile(r, 0.999) < 1e-4 and np.quantile(r, 0.99999) < 1e-3, (k, np.quantile(r, 0.999))
+        report[k] = float(r[wellc].max())
+        assert np.quantile(r[wellc], 0.9999) < 1e-4 and r[wellc].max() < 1e-3, (k, r[wellc].max())
+        assert (r <= 1e-4 + 1e-5 * np.where(np.isfinite(kappa), kappa, 0.0)).all(), (k, (r / kappa).max())
     assert np.abs(g["x_ell"][cv] - o["x_ell"][cv]).max() < 1e-4 * max(1.0, np.abs(o["x_ell"][cv]).max())
     nee = s & (o["nee"] > 0)
     if nee.any():
@@ -108,19 +119,23 @@ def test_sample_debug_parity(dts, oracle, cfg, mode):
     assert (g["event"][s] == o["event"][s]).all()
     med = s & (o["event"] == 1)
     assert med.mean() > 0.05
-    r = _rel(g["p_m"][s], o["p_m"][s], 1e-6)
-    assert r.max() < 1e-4
-    r = _rel(g["cand_d"][med], o["cand_d"][med], 1e-3)
-    report["cand_d"] = float(r.max())
-    assert r.max() < 1e-4
+    st = c["sigma_s"] + c["sigma_a"]
+    err = np.abs(g["p_m"][s] - o["p_m"][s])      # p_m ~ sigma_t (t_hi - t_lo) near a boundary
+    assert (err <= 1e-4 * o["p_m"][s] + st * 2e-6).all(), err.max()
+    # candidate distances inherit p_m's boundary conditioning (E14: d - t_lo ~ p_m u / sigma_t)
+    err = np.abs(g["cand_d"][med] - o["cand_d"][med])
+    report["cand_d"] = float((err / np.maximum(np.abs(o["cand_d"][med]), 1e-3)).max())
+    assert (err <= 1e-4 * np.abs(o["cand_d"][med]) + 2e-6).all(), err.max()
     err = np.abs(g["cand_wn"][med] - o["cand_wn"][med])
     report["cand_wn"] = float(err.max())
     assert err.max() < 1e-4
     assert (g["istar"][med] == o["istar"][med]).all()
-    for k in ("d", "beta_ris"):
-        r = _rel(g[k][med], o[k][med], 1e-3 if k == "d" else 1e-30)
-        report[k] = float(r.max())
-        assert np.quantile(r, 0.9999) < 1e-4 and r.max() < 1e-3, (k, r.max())
+    err = np.abs(g["d"][med] - o["d"][med])
+    report["d"] = float((err / np.maximum(np.abs(o["d"][med]), 1e-3)).max())
+    assert (err <= 1e-4 * np.abs(o["d"][med]) + 2e-6).all(), err.max()
+    r = _rel(g["beta_ris"][med], o["beta_ris"][med], 1e-30)
+    report["beta_ris"] = float(r.max())
+    assert np.quantile(r, 0.9999) < 1e-4 and r.max() < 1e-3, r.max()
     assert np.abs(g["x_next"][med] - o["x_next"][med]).max() < 1e-4 * max(1.0, np.abs(o["x_next"][med]).max())
     assert (g["terminate"][s] == o["terminate"][s]).all()
     print(f"cfg{cfg}/{mode}: safe {safe.mean():.5f} max-rel {report}")
