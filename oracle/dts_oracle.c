@@ -392,6 +392,14 @@ typedef struct {
 
 static double uu(const uint32_t r[12], int i) { return or_uniform(r[i]); }
 
+/* R24, SPLIT walk direction: u8 and u9 are the 24-bit integers formed by the
+ * low bytes (left unused by u0..u7) of r0, r1, r2 and of r3, r4, r5. */
+static double u_split(const uint32_t r[12], int which) {
+  const uint32_t* a = r + 3 * which;
+  uint32_t m = ((a[0] & 0xFFu) << 16) | ((a[1] & 0xFFu) << 8) | (a[2] & 0xFFu);
+  return (double)m * (1.0 / 16777216.0);
+}
+
 /* connection along wc from x, medium interval [lo, hi) of that ray.  Returns
  * the contribution (already multiplied by beta * wconn). */
 static double connect(const or_scene* sc, const derived* dv, const pstate* ps, const double wc[3],
@@ -629,8 +637,8 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
       /* R29 SPLIT: the MIS weight stays on the connection; the walk continues
        * with an independent HG direction. */
       wconn = ratio_w;
-      double cth = hg_sample_cos(sc->g, uu(r, 8));
-      double phi = OR_PI * (2.0 * uu(r, 9) - 1.0);
+      double cth = hg_sample_cos(sc->g, u_split(r, 0));
+      double phi = OR_PI * (2.0 * u_split(r, 1) - 1.0);
       from_frame(ps->w, cth, phi, ww);
       if (dbg) dbg->beta_dir = 1.0;
     } else {
@@ -897,7 +905,7 @@ static double darts_path(const or_scene* sc, const derived* dv, const uint16_t* 
     uint32_t r[12];
     draw4(seed, id, (uint32_t)k, 0, r);
     draw4(seed, id, (uint32_t)k, 1, r + 4);
-    draw4(seed, id, (uint32_t)k, 2, r + 8);
+    r[8] = r[9] = r[10] = r[11] = 0u; /* reserved */
     double c;
     alive = darts_vertex(sc, dv, q, &ps, r, &c, NULL, st);
     if (st) st->vertices++;

@@ -81,8 +81,9 @@ __device__ __forceinline__ u4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint
                                      uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;  // IMAD.WIDE.U32
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
     const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
     c0 = n0;
     c1 = lo1;
@@ -96,20 +97,20 @@ __device__ __forceinline__ u4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint
 __device__ __forceinline__ float unif(uint32_t r) { return __uint2float_rn(r >> 8) * 5.9604644775390625e-08f; }
 
 // ----------------------------------------------------------------- accurate small-argument helpers
-// -ln(1 - x) for x in [0, 1): series below 1/32 (relative error < 1e-8),
-// MUFU lg2 above (relative error < 4e-6).
+// -ln(1 - x) for x in [0, 1): series x + x^2/2 + x^3/3 below 1/64 (relative
+// truncation error < x^3/4 < 1e-6), MUFU lg2 above (relative error < 1e-5).
 __device__ __forceinline__ float neg_log1m(float x) {
   const float big = -__log2f(1.0f - x) * kLn2;
-  const float ser = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 0.2f, 0.25f), 0.33333333f), 0.5f), 1.0f);
-  return x < 0.03125f ? ser : big;
+  const float ser = x * fmaf(x, fmaf(x, 0.33333334f, 0.5f), 1.0f);
+  return x < 0.015625f ? ser : big;
 }
 // -ln(1 - x) with 1 - x supplied separately (omx, formed without cancellation
-// by the caller: for x = u p with p = 1 - T, 1 - x = (1 - u) + u T exactly
-// enough even when x -> 1).
+// by the caller: for x = u p with p = 1 - T, 1 - x = (1 - u) + u T stays
+// accurate even when x -> 1).
 __device__ __forceinline__ float neg_log1m2(float x, float omx) {
   const float big = -__log2f(omx) * kLn2;
-  const float ser = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 0.2f, 0.25f), 0.33333333f), 0.5f), 1.0f);
-  return x < 0.03125f ? ser : big;
+  const float ser = x * fmaf(x, fmaf(x, 0.33333334f, 0.5f), 1.0f);
+  return x < 0.015625f ? ser : big;
 }
 // 1 - exp(-y) for y >= 0
 __device__ __forceinline__ float one_m_exp(float y) {
@@ -184,27 +185,20 @@ __device__ __forceinline__ int intersect(const DevScene& S, f3 o, f3 d, float& l
     hi = tf;
     return HIT_OPEN;
   }
-  float tn = -__int_as_float(0x7f800000), tf = __int_as_float(0x7f800000);
-  int ff = -1;
-  const float oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    if (dd[a] == 0.0f) {
-      if (oo[a] < S.bmin[a] || oo[a] > S.bmax[a]) return HIT_MISS;
-      continue;
-    }
-    const float inv = 1.0f / dd[a];
-    const float t1 = (S.bmin[a] - oo[a]) * inv, t2 = (S.bmax[a] - oo[a]) * inv;
-    tn = fmaxf(tn, fminf(t1, t2));
-    const float far = fmaxf(t1, t2);
-    if (far < tf) {
-      tf = far;
-      ff = 2 * a + (dd[a] > 0.0f ? 1 : 0);
-    }
-  }
-  const float l = fmaxf(tn, 0.0f);
-  if (!(tf > l)) return HIT_MISS;
-  lo = l;
+  // branchless slab test; 1/0 = inf and fminf/fmaxf drop the NaN of 0 * inf
+  const float ix = __fdividef(1.0f, d.x), iy = __fdividef(1.0f, d.y), iz = __fdividef(1.0f, d.z);
+  const float ax = (S.bmin[0] - o.x) * ix, bx = (S.bmax[0] - o.x) * ix;
+  const float ay = (S.bmin[1] - o.y) * iy, by = (S.bmax[1] - o.y) * iy;
+  const float az = (S.bmin[2] - o.z) * iz, bz = (S.bmax[2] - o.z) * iz;
+  const float fx = fmaxf(ax, bx), fy = fmaxf(ay, by), fz = fmaxf(az, bz);
+  const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+  const float tf = fminf(fminf(fx, fy), fz);
+  if (!(tf > tn)) return HIT_MISS;
+  // exit face: first axis attaining tf (ties -> lowest axis)
+  const int axis = (fx == tf) ? 0 : ((fy == tf) ? 1 : 2);
+  const float da = axis == 0 ? d.x : (axis == 1 ? d.y : d.z);
+  const int ff = 2 * axis + (da > 0.0f ? 1 : 0);
+  lo = tn;
   hi = tf;
   face = ff;
   return ((S.wall_mask >> ff) & 1u) ? HIT_WALL : HIT_OPEN;
@@ -230,15 +224,12 @@ __device__ __forceinline__ f3 inward_normal(int face) {
 
 // ----------------------------------------------------------------- path state
 struct PathState {
-  f3 x, w;       // position, incoming direction (camera: primary direction)
-  double E;      // elapsed counted time
-  double Rm, RM; // bin residual bounds T_m - tau_e, T_M - tau_e
+  f3 x, w;      // position, incoming direction (camera: primary direction)
+  double resM;  // upper residual R_M - E = T_M - tau_e - elapsed (E5); R_m - E = resM - dt
   float beta;
   int kind, face;
-  int e;         // emitter
+  int e;        // emitter
 };
-
-struct DbgOut;  // = dts_debug_out
 
 // EDA table access: 16-bit CDF, row of 256 per cell (R10)
 template <bool SMEM>
@@ -247,12 +238,19 @@ __device__ __forceinline__ float qload(const uint16_t* q, int i) {
   return (float)__ldg(q + i);
 }
 
+// R24: the SPLIT walk direction uses u8, u9 = the 24-bit integers formed by the
+// low bytes (unused by u0..u7) of r0, r1, r2 and of r3, r4, r5.
+__device__ __forceinline__ float u_split(uint32_t a, uint32_t b, uint32_t c) {
+  const uint32_t m = ((a & 0xFFu) << 16) | ((b & 0xFFu) << 8) | (c & 0xFFu);
+  return (float)m * 5.9604644775390625e-08f;
+}
+
 // ----------------------------------------------------------------- one DARTS vertex
 // Returns true if the walk continues.  contrib receives the vertex's
-// connection (+ wall NEE) contribution.
+// connection (+ wall NEE) contribution; end_reason the DTS_CTR_* of a stop.
 template <bool DBG, bool SMEM>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
-                                             const uint32_t (&r)[12], float& contrib, dts_debug_out* dbg,
+                                             const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason) {
   contrib = 0.0f;
   conn_nonempty = false;
@@ -262,8 +260,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   const float ek = S.em_k[ps.e];
   f3 wc, ww;
   float wconn = 1.0f;
-  const float resM = (float)(ps.RM - ps.E);
-  const float resm = (float)(ps.Rm - ps.E);
+  const float resM = (float)ps.resM;
 
   // ---- step 2: direction ----
   if (ps.kind == KIND_CAMERA) {
@@ -277,30 +274,22 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float alb = S.wall_albedo[ps.face];
     const f3 cv = xe - ps.x;
     const float C = sqrtf(dot(cv, cv));
-    const f3 we = cv * (1.0f / C);
+    const f3 we = cv * __fdividef(1.0f, C);
     const float cw = dot(n, we);
-    const float arrive_lo = resm - C, arrive_hi = resM - C;  // E + C in [Rm, RM)
+    const float resm = (float)(ps.resM - S.dt);
     float nee = 0.0f;
-    if (cw > 0.0f && arrive_lo <= 0.0f && arrive_hi > 0.0f) {
+    if (cw > 0.0f && resm - C <= 0.0f && resM - C > 0.0f) {  // E + C in [Rm, RM)
       // R14: time-checked direct NEE at a wall vertex
-      nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr(S, ps.x, xe, C, we) / (C * C);
+      nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr(S, ps.x, xe, C, we) * __fdividef(1.0f, C * C);
       if (S.r_excl > 0.0f && C < S.r_excl) nee = 0.0f;
       contrib += nee;
       wall_nee = nee > 0.0f;
     }
     if (DBG) dbg->nee = nee;
-    const float u5 = unif(r[5]), u6 = unif(r[6]);
-    const float rr = sqrtf(u5);
-    float sp, cp;
-    __sincosf(2.0f * kPi * u6, &sp, &cp);
-    // cosine hemisphere about n via the frame of R12 (cos = sqrt(1-u5), phi = 2 pi u6)
-    const float sign = copysignf(1.0f, n.z);
-    const float a = -1.0f / (sign + n.z);
-    const float b = n.x * n.y * a;
-    const f3 b1 = mk(1.0f + sign * n.x * n.x * a, sign * b, -sign * n.x);
-    const f3 b2 = mk(b, sign + n.y * n.y * a, -n.y);
-    const float lx = rr * cp, ly = rr * sp, lz = sqrtf(fmaxf(0.0f, 1.0f - u5));
-    wc = ww = mk(b1.x * lx + b2.x * ly + n.x * lz, b1.y * lx + b2.y * ly + n.y * lz, b1.z * lx + b2.z * ly + n.z * lz);
+    // Lambertian: cosine hemisphere about n (1 - cos^2 = u5), beta *= albedo
+    const float u5 = unif(r[5]);
+    const float lz = sqrtf(1.0f - u5);  // cos theta; sin^2 theta = u5 = (1 + lz)(1 - lz)
+    wc = ww = from_frame(n, 1.0f + lz, __fdividef(u5, 1.0f + lz), 2.0f * kPi * unif(r[6]));
     ps.beta *= alb;
     if (DBG) {
       dbg->tech = 3;
@@ -310,62 +299,52 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     // medium vertex: gamma of E19 with the table cell of R10 at S = R_M - E (R11)
     const f3 cv = xe - ps.x;
     const float C = sqrtf(dot(cv, cv));
-    const float Sres = resM;
-    const float ratio = C / Sres;
-    const float ls = (__logf(Sres) - S.ln_smin) * S.inv_dls;
-    const bool valid = (Sres > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < (float)S.ns);
-    const float gamma = valid ? ratio / (ratio + S.alpha) : 0.0f;
-    int cell = 0;
-    if (valid) {
-      const int ir = min((int)(ratio * (float)S.nr), S.nr - 1);
-      const int is = min((int)ls, S.ns - 1);
-      cell = ir * S.ns + is;
-    }
-    const f3 axis = C > 0.0f ? cv * (1.0f / C) : mk(0.0f, 0.0f, 1.0f);
-    const uint16_t* qc = tab + (size_t)cell * DTS_TABLE_COS_BINS;
-    const float u4 = unif(r[4]), u6 = unif(r[6]);
-    const float phi = kPi * (2.0f * u6 - 1.0f);
-    f3 om;
-    float p_eda = 0.0f;
-    int tech;
-    if (u4 < gamma) {
-      // EDA: inverse transform of the cell's 16-bit CDF; T = u5 * 65536 exactly
-      tech = 1;
-      const float T = (float)(r[5] >> 8) * (1.0f / 256.0f);
-      int j = 0;
+    const float ratio = __fdividef(C, resM);
+    const float ls = (__logf(resM) - S.ln_smin) * S.inv_dls;
+    const bool valid = (resM > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < (float)S.ns);
+    const float gamma = valid ? __fdividef(ratio, ratio + S.alpha) : 0.0f;
+    const int ir = min((int)(ratio * (float)S.nr), S.nr - 1);
+    const int is = min(max((int)ls, 0), S.ns - 1);
+    const uint16_t* qc = tab + (valid ? (size_t)(ir * S.ns + is) * DTS_TABLE_COS_BINS : 0);
+    const f3 axis = cv * __fdividef(1.0f, C);
+    const float u4 = unif(r[4]), u5 = unif(r[5]);
+    const float phi = kPi * (2.0f * unif(r[6]) - 1.0f);
+    const bool eda = u4 < gamma;
+    // Both techniques are evaluated by every lane and one is selected, so the
+    // warp never splits into an EDA and an HG branch.
+    // EDA: inverse transform of the cell's 16-bit CDF; T = u5 * 65536 exactly.
+    const float T = (float)(r[5] >> 8) * (1.0f / 256.0f);
+    int j = 0;
 #pragma unroll
-      for (int step = 128; step >= 1; step >>= 1)  // largest j with q_j <= T (q_0 = 0)
-        if (qload<SMEM>(qc, j + step) <= T) j += step;
-      const float qa = qload<SMEM>(qc, j);
-      const float qb = j == 255 ? 65536.0f : qload<SMEM>(qc, j + 1);
-      const float inv = __fdividef(1.0f, qb - qa);
-      // cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts
-      const float opc = ((float)j + (T - qa) * inv) * (1.0f / 128.0f);
-      const float omc = ((float)(255 - j) + (qb - T) * inv) * (1.0f / 128.0f);
-      om = from_frame(axis, opc, omc, phi);
-      p_eda = (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi));
-    } else {
-      tech = 0;
-      float opc, omc;
-      hg_sample(S, unif(r[5]), opc, omc);
-      om = from_frame(ps.w, opc, omc, phi);
-      if (valid) {
-        const int j = min(max((int)floorf((dot(om, axis) + 1.0f) * 128.0f), 0), 255);
-        const float qa = qload<SMEM>(qc, j);
-        const float qb = j == 255 ? 65536.0f : qload<SMEM>(qc, j + 1);
-        p_eda = (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi));
-      }
+    for (int step = 128; step >= 1; step >>= 1)  // largest j with q_j <= T (q_0 = 0)
+      if (qload<SMEM>(qc, j + step) <= T) j += step;
+    float qa = qload<SMEM>(qc, j);
+    float qb = j == 255 ? 65536.0f : qload<SMEM>(qc, j + 1);
+    const float iq = __fdividef(1.0f, qb - qa);
+    // HG about w_{k-1}
+    float opc, omc;
+    hg_sample(S, u5, opc, omc);
+    if (eda) {  // cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts
+      opc = ((float)j + (T - qa) * iq) * (1.0f / 128.0f);
+      omc = ((float)(255 - j) + (qb - T) * iq) * (1.0f / 128.0f);
     }
+    const f3 om = from_frame(eda ? axis : ps.w, opc, omc, phi);
+    if (!eda) {  // EDA pdf of the HG direction: bin of its cos to the emitter axis
+      const int jb = min(max((int)floorf((dot(om, axis) + 1.0f) * 128.0f), 0), 255);
+      qa = qload<SMEM>(qc, jb);
+      qb = jb == 255 ? 65536.0f : qload<SMEM>(qc, jb + 1);
+    }
+    const float p_eda = valid ? (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi)) : 0.0f;
     const float p_hg = hg_eval(S, dot(om, ps.w));
     const float p_mix = gamma * p_eda + (1.0f - gamma) * p_hg;
-    const float ratio_w = p_hg / p_mix;
+    const float ratio_w = __fdividef(p_hg, p_mix);
     wc = om;
     if (S.direction_mode == DTS_DIR_SPLIT) {
       // R29 SPLIT: MIS weight on the connection only; independent HG walk direction
       wconn = ratio_w;
-      float opc, omc;
-      hg_sample(S, unif(r[8]), opc, omc);
-      ww = from_frame(ps.w, opc, omc, kPi * (2.0f * unif(r[9]) - 1.0f));
+      float o2, m2;
+      hg_sample(S, u_split(r[0], r[1], r[2]), o2, m2);
+      ww = from_frame(ps.w, o2, m2, kPi * (2.0f * u_split(r[3], r[4], r[5]) - 1.0f));
       if (DBG) dbg->beta_dir = 1.0f;
     } else {
       ww = om;
@@ -373,7 +352,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       if (DBG) dbg->beta_dir = ratio_w;
     }
     if (DBG) {
-      dbg->tech = tech;
+      dbg->tech = eda ? 1 : 0;
       dbg->gamma = gamma;
       dbg->p_eda = p_eda;
       dbg->p_hg = p_hg;
@@ -409,25 +388,22 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float q = dot(wc, cv);
     const float u7 = unif(r[7]);
     float t = 0.0f, pt = 0.0f, Ssamp = 0.0f;
-    bool ok = false;
     float pSt = 0.0f;  // S - t (= r2 on the ellipse)
+    bool ok = false;
     if (!(S.warped == 0 && ps.kind == KIND_CAMERA)) {
       // S(t) = t + |x + wc t - xe| is non-decreasing; admissible S range
       // [max(Rm - E, S(clo)), min(RM - E, S(chi))) (case I, R14).  Work with
       // S - C, formed without cancellation:
-      //   S(clo) - C = clo + clo (clo - 2q) / (|p_lo - xe| + C),
-      //   (Rm - E) - C evaluated in double.
+      //   S(t) - C = t + t (t - 2q) / (|x + wc t - xe| + C),  (Rm - E) - C in double.
       const f3 plo = fma3(wc, clo, ps.x) - xe;
-      const float rlo = sqrtf(dot(plo, plo));
-      const float lo_m_C = clo + clo * (clo - 2.0f * q) * __fdividef(1.0f, rlo + C);
+      const float lo_m_C = clo + clo * (clo - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(plo, plo)) + C);
       float hi_m_C = __int_as_float(0x7f800000);
       if (isfinite(chi)) {
         const f3 phi_ = fma3(wc, chi, ps.x) - xe;
         hi_m_C = chi + chi * (chi - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(phi_, phi_)) + C);
       }
-      // bin bounds relative to C in double: (Rm - E) - C, (RM - E) - C
-      const double dm_d = ps.Rm - ps.E - (double)C;
-      const double dM_d = ps.RM - ps.E - (double)C;
+      const double dM_d = ps.resM - (double)C;
+      const double dm_d = dM_d - S.dt;
       float dlo = (float)dm_d;
       bool lo_bin = true;
       if (lo_m_C > dlo) { dlo = lo_m_C; lo_bin = false; }
@@ -435,23 +411,15 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const bool hi_bin = (float)dM_d <= hi_m_C;
       const float dhi = hi_bin ? (float)dM_d : hi_m_C;
       // width S_hi - S_lo, exact to rounding when both bounds are bin bounds
-      const float width = (float)((hi_bin ? dM_d : (double)hi_m_C) - (lo_bin ? dm_d : (double)dlo));
-      const float S_lo = C + dlo;
-      const float S_hi = C + dhi;
-      if (DBG) { dbg->S_lo = S_lo; dbg->S_hi = S_hi; }
+      const float width = lo_bin && hi_bin ? (float)S.dt : (float)((hi_bin ? dM_d : (double)hi_m_C) - (lo_bin ? dm_d : (double)dlo));
+      if (DBG) { dbg->S_lo = C + dlo; dbg->S_hi = C + dhi; }
       if (width > 0.0f) {
         ok = true;
         // truncated exponential on [S_lo, S_hi); e^{-st (S-S_lo)} = 1 - u7 span
-        float L, pS;
-        if (isinf(dhi)) {
-          L = neg_log1m(u7) * S.inv_sigma_t;
-          pS = S.sigma_t * (1.0f - u7);
-        } else {
-          const float span = one_m_exp(S.sigma_t * width);
-          const float keep = fmaf(u7, fexp(-S.sigma_t * width), 1.0f - u7);  // 1 - u7 span
-          L = neg_log1m2(u7 * span, keep) * S.inv_sigma_t;
-          pS = S.sigma_t * keep * __fdividef(1.0f, span);
-        }
+        const float span = one_m_exp(S.sigma_t * width);
+        const float keep = fmaf(u7, fexp(-S.sigma_t * width), 1.0f - u7);  // 1 - u7 span
+        const float L = neg_log1m2(u7 * span, keep) * S.inv_sigma_t;
+        const float pS = S.sigma_t * keep * __fdividef(1.0f, span);
         const float dSC = dlo + L;  // S - C
         const float Ssm = C + dSC;
         // S - q = (S - C) + (C - q), C - q = perp^2 / (C + q) for q > 0
@@ -467,6 +435,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       }
     } else {
       // R17: unwarped camera vertex, shell |x(t) - xe| in [Rm, RM): <= 2 t-intervals
+      const float resm = (float)(ps.resM - S.dt);
       float a_lo = clo;
       if (S.s_excess > 0.0f) {
         const float Se = C + S.s_excess;
@@ -503,10 +472,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
         ok = true;
         const float v = u7 * Z;
         const bool second = (m0 <= 0.0f) || (ni == 2 && !(v < m0));
-        const float ia = second ? ia1 : ia0, ib = second ? ib1 : ib0, mm = second ? m1 : m0;
+        const float ia = second ? ia1 : ia0, ib = second ? ib1 : ib0;
         float up = second ? (v - m0) / m1 : v / m0;
         up = fminf(up, 0.99999994f);
-        (void)mm;
         const float span = one_m_exp(S.sigma_t * (ib - ia));
         t = ia + neg_log1m2(up * span, fmaf(up, fexp(-S.sigma_t * (ib - ia)), 1.0f - up)) * S.inv_sigma_t;
         pt = S.sigma_t * fexp(-S.sigma_t * (t - clo)) / Z;
@@ -525,7 +493,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       }
       const float rho = hg_eval(S, dot(wc, we));
       const float tr = fexp(-S.sigma_t * (t - clo)) * segment_tr(S, xell, xe, r2, we);
-      float c = ps.beta * wconn * S.sigma_s * tr * rho * ek / (r2sq * pt);
+      float c = ps.beta * wconn * S.sigma_s * tr * rho * ek * __fdividef(1.0f, r2sq * pt);
       if (S.r_excl > 0.0f && r2 < S.r_excl) c = 0.0f;
       contrib += c;
       if (DBG) {
@@ -555,14 +523,13 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     // candidates: Sobol row r = floor(32 u1) with Cranley-Patterson shift u2 (R6):
     // Q[r][i] = RI2(8r+i) = bitrev3(i)/8 + bitrev5(r)/256, shift and mod 1 done
     // exactly on 24-bit integers.
-    const uint32_t row = r[1] >> 27;
-    const uint32_t br5 = __brev(row) >> 27;
+    const uint32_t br5 = __brev(r[1] >> 27) >> 27;
     const uint32_t m2 = r[2] >> 8;
     const f3 cv = xe - ps.x;
     const float qd = dot(ww, cv);
     const f3 perp = cv - ww * qd;
     const float perp2 = dot(perp, perp);
-    float d[8], e2[8], lw[8];
+    float e2[8], sr[8];
     float emax = -__int_as_float(0x7f800000);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -571,57 +538,59 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const float ui = (float)v * 5.9604644775390625e-08f;
       const float omu = (float)(0x1000000u - v) * 5.9604644775390625e-08f;  // 1 - u_i, exact
       // E14 with the sign of R1: d = t_lo - ln(1 - p_m u) / sigma_t, 1 - p_m u = (1 - u) + u (1 - p_m)
-      d[i] = lo + neg_log1m2(p_m * ui, fmaf(ui, T_m, omu)) * S.inv_sigma_t;
-      const float Delta = resM - counts * d[i];          // R4
-      const float dq = d[i] - qd;
+      const float di = lo + neg_log1m2(p_m * ui, fmaf(ui, T_m, omu)) * S.inv_sigma_t;
+      if (DBG) dbg->cand_d[i] = di;
+      const float Delta = resM - counts * di;  // R4
+      const float dq = di - qd;
       const float r2i = fmaf(dq, dq, perp2);
       const bool valid = (Delta > 0.0f) && (r2i <= Delta * Delta);
-      const float sr = rsqrtf(Delta);
-      const float invD = sr * sr;
+      const float s = rsqrtf(Delta);
       // log2 of Phi' = Delta^{-3/2} exp(-r^2/(4 D Delta) - sigma_a Delta) (E9, constants dropped)
-      const float ex = fmaf(S.neg_inv4D_log2e * r2i, invD, S.neg_sa_log2e * Delta);
+      const float ex = fmaf(S.neg_inv4D_log2e * r2i, s * s, S.neg_sa_log2e * Delta);
       e2[i] = valid ? ex : -__int_as_float(0x7f800000);
-      lw[i] = invD * sr;  // Delta^{-3/2}
+      sr[i] = s;
       emax = fmaxf(emax, e2[i]);
     }
-    float w[8];
     float W = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      w[i] = e2[i] > -__int_as_float(0x7f800000) ? lw[i] * exp2f(e2[i] - emax) : 0.0f;  // R7
-      W += w[i];
+    for (int i = 0; i < 8; ++i) {  // R7: weights relative to the largest exponent
+      e2[i] = e2[i] > -__int_as_float(0x7f800000) ? sr[i] * sr[i] * sr[i] * exp2f(e2[i] - emax) : 0.0f;
+      W += e2[i];
     }
     if (DBG) {
-      for (int i = 0; i < 8; ++i) {
-        dbg->cand_d[i] = d[i];
-        dbg->cand_wn[i] = W > 0.0f ? w[i] / W : 0.0f;
-      }
+      for (int i = 0; i < 8; ++i) dbg->cand_wn[i] = W > 0.0f ? e2[i] / W : 0.0f;
     }
     if (!(W > 0.0f)) {
       if (DBG) { dbg->event = 4; dbg->terminate = 1; dbg->beta_out = ps.beta; }
       end_reason = DTS_CTR_RIS_INVALID;  // R5
       return false;
     }
+    // resample: smallest i with sum_{j<=i} w_j > u3 W (CDF inversion in candidate order)
     const float thr = unif(r[3]) * W;
-    float cum = 0.0f, dsel = d[7], wsel = w[7];
-    int is = 7;
+    float cum = 0.0f, wsel = e2[7];
+    uint32_t is = 7;
     bool found = false;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      cum += w[i];
+      cum += e2[i];
       const bool take = !found && (cum > thr);
-      dsel = take ? d[i] : dsel;
-      wsel = take ? w[i] : wsel;
-      is = take ? i : is;
+      wsel = take ? e2[i] : wsel;
+      is = take ? (uint32_t)i : is;
       found = found || take;
     }
-    const float beta_ris = S.albedo * (W * 0.125f) / wsel;  // E15: a * mean(w) / w*
+    // regenerate the selected candidate's distance (cheaper than keeping all 8)
+    const uint32_t brs = __brev(is) >> 29;
+    const uint32_t vs = (m2 + ((brs * 32u + br5) << 16)) & 0xFFFFFFu;
+    const float us = (float)vs * 5.9604644775390625e-08f;
+    const float dsel = lo + neg_log1m2(p_m * us, fmaf(us, T_m, (float)(0x1000000u - vs) * 5.9604644775390625e-08f)) *
+                                 S.inv_sigma_t;
+    const float beta_ris = S.albedo * (W * 0.125f) * __fdividef(1.0f, wsel);  // E15: a * mean(w) / w*
     ps.beta *= beta_ris;
     ps.x = fma3(ww, dsel, ps.x);
-    ps.E += (double)(counts * dsel);
+    ps.resM -= (double)(counts * dsel);
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
-    if (DBG) { dbg->event = 1; dbg->istar = is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
+    if (DBG) { dbg->event = 1; dbg->istar = (int)is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
   } else {
     if (hit == HIT_WALL) {
       f3 xn = fma3(ww, hi, ps.x);
@@ -629,7 +598,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const float pl = (face & 1) ? S.bmax[a] : S.bmin[a];
       if (a == 0) xn.x = pl; else if (a == 1) xn.y = pl; else xn.z = pl;  // snap onto the wall
       ps.x = xn;
-      ps.E += (double)(counts * hi);
+      ps.resM -= (double)(counts * hi);
       ps.kind = KIND_WALL;
       ps.face = face;
       ps.w = ww;
@@ -642,13 +611,12 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   }
   if (DBG) {
     dbg->x_next[0] = ps.x.x; dbg->x_next[1] = ps.x.y; dbg->x_next[2] = ps.x.z;
-    dbg->E_next = ps.E;
     dbg->beta_out = ps.beta;
   }
-  // early exit
+  // early exit: no later connection can land before R_M
   const f3 dn = ps.x - xe;
   const float Cn = sqrtf(dot(dn, dn));
-  if ((float)(ps.RM - ps.E) - Cn <= 0.0f) {
+  if ((float)ps.resM - Cn <= 0.0f) {
     if (DBG) dbg->terminate = 1;
     end_reason = DTS_CTR_EARLY_EXIT;
     return false;

@@ -132,19 +132,19 @@ __global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n
   PathState ps;
   ps.x = mk(rec.x[0], rec.x[1], rec.x[2]);
   ps.w = mk(rec.w[0], rec.w[1], rec.w[2]);
-  ps.E = rec.E;
   ps.beta = rec.beta;
   ps.kind = rec.kind;
   ps.face = rec.face;
   ps.e = rec.emitter;
-  ps.Rm = S.t0 + (double)rec.bin * S.dt - (double)S.em_t[rec.emitter];
-  ps.RM = S.t0 + (double)(rec.bin + 1) * S.dt - (double)S.em_t[rec.emitter];
-  uint32_t r[12];
-  for (int k = 0; k < 12; ++k) r[k] = rec.r[k];
+  const double RM = S.t0 + (double)(rec.bin + 1) * S.dt - (double)S.em_t[rec.emitter];
+  ps.resM = RM - rec.E;
+  uint32_t r[8];
+  for (int k = 0; k < 8; ++k) r[k] = rec.r[k];
   float c;
   bool cn, wn;
   int reason;
   darts_vertex<true, false>(S, tab, ps, r, c, &o, cn, wn, reason);
+  o.E_next = RM - ps.resM;
   out[i] = o;
 }
 
@@ -165,7 +165,10 @@ struct RenderParams {
   uint32_t table_u4; // table size in 16-byte words
 };
 
-constexpr int kBlock = 512;
+#ifndef DTS_BLOCK
+#define DTS_BLOCK 768
+#endif
+constexpr int kBlock = DTS_BLOCK;
 constexpr uint32_t kChunk = 128;
 
 struct PathCtx {
@@ -246,12 +249,9 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     ps.w = mk(s2 * cp, s2 * sp, z2);
     ps.beta = 4.0f * kPi;
   }
-  ps.E = 0.0;
   ps.kind = KIND_CAMERA;
   ps.face = -1;
-  const double te = (double)S.em_t[e];
-  ps.Rm = S.t0 + (double)b * S.dt - te;
-  ps.RM = S.t0 + (double)(b + 1) * S.dt - te;
+  ps.resM = S.t0 + (double)(b + 1) * S.dt - (double)S.em_t[e];  // R_M - E with E = 0
   float lo, hi;
   int f;
   if (intersect(S, ps.x, ps.w, lo, hi, f) == HIT_MISS) {
@@ -260,7 +260,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   }
   if (S.warped || S.camera_kind == DTS_CAMERA_SPHERE_DETECTOR) {
     const f3 dv = ps.x - ld3(S.em_pos[e]);
-    if (sqrtf(dot(dv, dv)) >= (float)ps.RM) {
+    if (sqrtf(dot(dv, dv)) >= (float)ps.resM) {
       ++ctr_early;
       return false;
     }
@@ -269,7 +269,13 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(kBlock, 1) render_darts_kernel(const RenderParams P) {
+#ifndef DTS_MINB
+#define DTS_MINB 1
+#endif
+#ifndef DTS_TABLE_SMEM
+#define DTS_TABLE_SMEM 1
+#endif
+__global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const RenderParams P) {
   extern __shared__ __align__(16) uint16_t s_tab[];
   const DevScene& S = P.S;
   const uint16_t* tab = P.tab;
@@ -335,16 +341,11 @@ __global__ void __launch_bounds__(kBlock, 1) render_darts_kernel(const RenderPar
     bool cn = false, wn = false, cap = false;
     int reason = 0;
     if (active) {
-      uint32_t r[12];
+      uint32_t r[8];
       const u4 a = philox(pc.id_lo, pc.id_hi, pc.k, 0u, S.seed_lo, S.seed_hi);
       const u4 b = philox(pc.id_lo, pc.id_hi, pc.k, 1u, S.seed_lo, S.seed_hi);
       r[0] = a.a; r[1] = a.b; r[2] = a.c; r[3] = a.d;
       r[4] = b.a; r[5] = b.b; r[6] = b.c; r[7] = b.d;
-      r[8] = r[9] = r[10] = r[11] = 0u;
-      if (S.direction_mode == DTS_DIR_SPLIT && pc.ps.kind == KIND_MEDIUM) {
-        const u4 c = philox(pc.id_lo, pc.id_hi, pc.k, 2u, S.seed_lo, S.seed_hi);
-        r[8] = c.a; r[9] = c.b; r[10] = c.c; r[11] = c.d;
-      }
       float contrib;
       const bool alive = darts_vertex<false, SMEM>(S, tab, pc.ps, r, contrib, nullptr, cn, wn, reason);
       pc.acc += contrib;
@@ -355,11 +356,13 @@ __global__ void __launch_bounds__(kBlock, 1) render_darts_kernel(const RenderPar
     // event counters: every lane takes part in the ballots (warp-uniform sums)
     c_conn += __popc(__ballot_sync(FULL, cn));
     c_nee += __popc(__ballot_sync(FULL, wn));
-    c_ris += __popc(__ballot_sync(FULL, reason == DTS_CTR_RIS_INVALID));
-    c_early += __popc(__ballot_sync(FULL, reason == DTS_CTR_EARLY_EXIT));
-    c_esc += __popc(__ballot_sync(FULL, reason == DTS_CTR_ESCAPES));
-    c_nf += __popc(__ballot_sync(FULL, reason == DTS_CTR_NONFINITE));
-    c_cap += __popc(__ballot_sync(FULL, cap));
+    if (__ballot_sync(FULL, done)) {
+      c_ris += __popc(__ballot_sync(FULL, reason == DTS_CTR_RIS_INVALID));
+      c_early += __popc(__ballot_sync(FULL, reason == DTS_CTR_EARLY_EXIT));
+      c_esc += __popc(__ballot_sync(FULL, reason == DTS_CTR_ESCAPES));
+      c_nf += __popc(__ballot_sync(FULL, reason == DTS_CTR_NONFINITE));
+      c_cap += __popc(__ballot_sync(FULL, cap));
+    }
     c_vert += __popc(act);
     if (done) {
       float v = pc.acc;
@@ -799,7 +802,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix * (uint64_t)d.n_bins * ns : npix * ns;
     const size_t tbytes = s->table_n * sizeof(uint16_t);
     P.table_u4 = (uint32_t)(tbytes / 16);
-    const bool smem = tbytes <= 200 * 1024;
+    const bool smem = DTS_TABLE_SMEM && tbytes <= 200 * 1024;
     int blocks_per_sm = 1;
     if (smem) {
       CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes));

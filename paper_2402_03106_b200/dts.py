@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdts.so")
+# DTS_LIB selects an alternative in-tree build of the same library (launch
+# geometry sweeps); the default is the one __graft_entry__.build() produces.
+LIB_PATH = os.path.join(_HERE, os.environ.get("DTS_LIB", "libdts.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
