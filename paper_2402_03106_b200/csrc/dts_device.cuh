@@ -56,6 +56,7 @@ struct DevScene {
   float r_excl, s_excess;
   // EDA table (R8-R10)
   int32_t nr, ns;
+  uint32_t table_n;        // CDF entries; an 8-bit guide table of the same length follows them
   float ln_smin, inv_dls;  // ns / (ln smax - ln smin)
   uint32_t seed_lo, seed_hi;
 };
@@ -231,11 +232,17 @@ struct PathState {
   int e;        // emitter
 };
 
-// EDA table access: 16-bit CDF, row of 256 per cell (R10)
+// EDA table access (R10): 16-bit CDF rows of 256 per cell, followed by an
+// 8-bit guide row per cell: guide[g] = largest j with q_j <= 256 g.
 template <bool SMEM>
-__device__ __forceinline__ float qload(const uint16_t* q, int i) {
-  if (SMEM) return (float)q[i];
-  return (float)__ldg(q + i);
+__device__ __forceinline__ uint32_t qload(const uint16_t* q, int i) {
+  if (SMEM) return q[i];
+  return __ldg(q + i);
+}
+template <bool SMEM>
+__device__ __forceinline__ uint32_t gload(const uint8_t* g, int i) {
+  if (SMEM) return g[i];
+  return __ldg(g + i);
 }
 
 // R24: the SPLIT walk direction uses u8, u9 = the 24-bit integers formed by the
@@ -312,14 +319,21 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const bool eda = u4 < gamma;
     // Both techniques are evaluated by every lane and one is selected, so the
     // warp never splits into an EDA and an HG branch.
-    // EDA: inverse transform of the cell's 16-bit CDF; T = u5 * 65536 exactly.
+    // EDA: inverse transform of the cell's 16-bit CDF.  T = u5 * 65536 exactly;
+    // the bin is the largest j with q_j <= T, i.e. q_j <= Ti = floor(T): start
+    // from the guide entry of Ti's 1/256 slice and bisect within the slice.
+    const uint32_t Ti = r[5] >> 16;
+    const uint8_t* gc = reinterpret_cast<const uint8_t*>(tab + S.table_n) + (qc - tab);
+    const uint32_t gi = Ti >> 8;
+    int j = (int)gload<SMEM>(gc, gi);
+    int jh = gi == 255u ? 255 : (int)gload<SMEM>(gc, gi + 1);
+    while (j < jh) {
+      const int mid = (j + jh + 1) >> 1;
+      if (qload<SMEM>(qc, mid) <= Ti) j = mid; else jh = mid - 1;
+    }
     const float T = (float)(r[5] >> 8) * (1.0f / 256.0f);
-    int j = 0;
-#pragma unroll
-    for (int step = 128; step >= 1; step >>= 1)  // largest j with q_j <= T (q_0 = 0)
-      if (qload<SMEM>(qc, j + step) <= T) j += step;
-    float qa = qload<SMEM>(qc, j);
-    float qb = j == 255 ? 65536.0f : qload<SMEM>(qc, j + 1);
+    float qa = (float)qload<SMEM>(qc, j);
+    float qb = j == 255 ? 65536.0f : (float)qload<SMEM>(qc, j + 1);
     const float iq = __fdividef(1.0f, qb - qa);
     // HG about w_{k-1}
     float opc, omc;
@@ -331,8 +345,8 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const f3 om = from_frame(eda ? axis : ps.w, opc, omc, phi);
     if (!eda) {  // EDA pdf of the HG direction: bin of its cos to the emitter axis
       const int jb = min(max((int)floorf((dot(om, axis) + 1.0f) * 128.0f), 0), 255);
-      qa = qload<SMEM>(qc, jb);
-      qb = jb == 255 ? 65536.0f : qload<SMEM>(qc, jb + 1);
+      qa = (float)qload<SMEM>(qc, jb);
+      qb = jb == 255 ? 65536.0f : (float)qload<SMEM>(qc, jb + 1);
     }
     const float p_eda = valid ? (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi)) : 0.0f;
     const float p_hg = hg_eval(S, dot(om, ps.w));
@@ -536,9 +550,10 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const uint32_t br3 = __brev((uint32_t)i) >> 29;
       const uint32_t v = (m2 + ((br3 * 32u + br5) << 16)) & 0xFFFFFFu;
       const float ui = (float)v * 5.9604644775390625e-08f;
-      const float omu = (float)(0x1000000u - v) * 5.9604644775390625e-08f;  // 1 - u_i, exact
-      // E14 with the sign of R1: d = t_lo - ln(1 - p_m u) / sigma_t, 1 - p_m u = (1 - u) + u (1 - p_m)
-      const float di = lo + neg_log1m2(p_m * ui, fmaf(ui, T_m, omu)) * S.inv_sigma_t;
+      // E14 with the sign of R1: d = t_lo - ln(1 - p_m u) / sigma_t with
+      // 1 - p_m u = (1 - u) + u (1 - p_m) (1 - u exact); MUFU lg2 keeps the
+      // absolute error of d below ~1e-7 / sigma_t
+      const float di = fmaf(-__log2f(fmaf(ui, T_m, 1.0f - ui)), S.inv_sigma_t * kLn2, lo);
       if (DBG) dbg->cand_d[i] = di;
       const float Delta = resM - counts * di;  // R4
       const float dq = di - qd;
@@ -582,8 +597,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const uint32_t brs = __brev(is) >> 29;
     const uint32_t vs = (m2 + ((brs * 32u + br5) << 16)) & 0xFFFFFFu;
     const float us = (float)vs * 5.9604644775390625e-08f;
-    const float dsel = lo + neg_log1m2(p_m * us, fmaf(us, T_m, (float)(0x1000000u - vs) * 5.9604644775390625e-08f)) *
-                                 S.inv_sigma_t;
+    const float dsel = fmaf(-__log2f(fmaf(us, T_m, 1.0f - us)), S.inv_sigma_t * kLn2, lo);
     const float beta_ris = S.albedo * (W * 0.125f) * __fdividef(1.0f, wsel);  // E15: a * mean(w) / w*
     ps.beta *= beta_ris;
     ps.x = fma3(ww, dsel, ps.x);

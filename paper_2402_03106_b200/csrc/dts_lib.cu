@@ -92,7 +92,7 @@ __device__ double e17_integrand(const TableParams& P, double C, double S, double
 }
 
 // grid = cells, block = 256 (one thread per cos bin)
-__global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_t* __restrict__ q) {
+__global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_t* __restrict__ q, size_t n_total) {
   __shared__ double F[256];
   const int cell = blockIdx.x;
   const int ir = cell / P.ns, is = cell % P.ns;
@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_
   for (int n = 0; n < 8; ++n) acc += 0.5 * dc * kGLw8[n] * e17_integrand(P, C, S, c0 + 0.5 * dc * (1.0 + kGLx8[n]));
   F[j] = acc;
   __syncthreads();
+  __shared__ uint16_t Q[256];
   if (j == 0) {
     double total = 0.0;
     for (int i = 0; i < 256; ++i) total += F[i];
@@ -113,10 +114,21 @@ __global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_
     for (int i = 0; i < 256; ++i) {
       double qv = floor(65536.0 * cdf + 0.5);
       if (qv > 65535.0) qv = 65535.0;
+      Q[i] = (uint16_t)qv;
       q[(size_t)cell * 256 + i] = (uint16_t)qv;
       cdf += F[i] / total;
     }
   }
+  __syncthreads();
+  // guide row (acceleration structure of the same inverse transform):
+  // guide[g] = largest i with Q[i] <= 256 g
+  int lo = 0, hi = 255;
+  const uint32_t key = 256u * (uint32_t)j;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((uint32_t)Q[mid] <= key) lo = mid; else hi = mid - 1;
+  }
+  reinterpret_cast<uint8_t*>(q + n_total)[(size_t)cell * 256 + j] = (uint8_t)lo;
 }
 
 // ============================================================== debug kernel
@@ -163,6 +175,7 @@ struct RenderParams {
   uint32_t npix;     // crop pixels
   uint32_t cw;       // crop width
   uint32_t table_u4; // table size in 16-byte words
+  uint32_t spp_div_b, spp_mod_b;  // SPP_PER_PIXEL cell counts (R21)
 };
 
 #ifndef DTS_BLOCK
@@ -192,15 +205,29 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   float inv_n;
   if (S.spp_mode == DTS_SPP_PER_CELL) {
     // issue order (b descending, pixel, s): long late-bin walks first
-    const uint64_t sl = widx % P.n_s;
-    const uint64_t rest = widx / P.n_s;
-    pl = (uint32_t)(rest % P.npix);
-    b = B - 1u - (uint32_t)(rest / P.npix);
+    uint64_t sl, rest;
+    if (P.total <= 0xFFFFFFFFull) {  // 32-bit divisions when the launch allows
+      const uint32_t w32 = (uint32_t)widx, ns32 = (uint32_t)P.n_s;
+      sl = w32 % ns32;
+      rest = w32 / ns32;
+      pl = (uint32_t)rest % P.npix;
+      b = B - 1u - (uint32_t)rest / P.npix;
+    } else {
+      sl = widx % P.n_s;
+      rest = widx / P.n_s;
+      pl = (uint32_t)(rest % P.npix);
+      b = B - 1u - (uint32_t)(rest / P.npix);
+    }
     s = P.s_begin + sl;
     inv_n = 1.0f / (float)P.spp;
   } else {
-    pl = (uint32_t)(widx % P.npix);
-    s = P.s_begin + widx / P.npix;
+    if (P.total <= 0xFFFFFFFFull) {
+      pl = (uint32_t)widx % P.npix;
+      s = P.s_begin + (uint32_t)widx / P.npix;
+    } else {
+      pl = (uint32_t)(widx % P.npix);
+      s = P.s_begin + widx / P.npix;
+    }
   }
   const uint32_t px = (uint32_t)S.crop[0] + pl % P.cw, py = (uint32_t)S.crop[1] + pl / P.cw;
   const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
@@ -212,7 +239,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     const uint32_t op = min((uint32_t)((float)B * unif(o.a)), B - 1u);
     b = (uint32_t)((s + op) % B);
     const uint32_t rel = (b + B - op) % B;
-    const uint64_t n_pb = P.spp / B + ((uint64_t)rel < P.spp % B ? 1u : 0u);
+    const uint32_t n_pb = P.spp_div_b + (rel < P.spp_mod_b ? 1u : 0u);
     inv_n = 1.0f / (float)n_pb;
     id = s * Npix + p;
   }
@@ -728,7 +755,7 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
     cudaFree(s->d_table);
     s->d_table = nullptr;
     s->table_n = 0;
-    if (cudaMalloc(&s->d_table, n * sizeof(uint16_t)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(table) failed");
+    if (cudaMalloc(&s->d_table, n * 3) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(table) failed");
     s->table_n = n;
   }
   TableParams P;
@@ -740,7 +767,8 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
   P.smax = smax;
   P.nr = nr;
   P.ns = ns;
-  table_build_kernel<<<nr * ns, 256, 0, (cudaStream_t)stream>>>(P, s->d_table);
+  table_build_kernel<<<nr * ns, 256, 0, (cudaStream_t)stream>>>(P, s->d_table, n);
+  s->S.table_n = (uint32_t)n;
   CUDA_TRY(cudaGetLastError());
   s->S.nr = nr;
   s->S.ns = ns;
@@ -797,12 +825,14 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   P.spp = spp;
   P.npix = (uint32_t)npix;
   P.cw = (uint32_t)(d.crop[2] - d.crop[0]);
+  P.spp_div_b = (uint32_t)(spp / (uint64_t)d.n_bins);
+  P.spp_mod_b = (uint32_t)(spp % (uint64_t)d.n_bins);
   cudaStream_t st = (cudaStream_t)stream;
   if (darts) {
     P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix * (uint64_t)d.n_bins * ns : npix * ns;
-    const size_t tbytes = s->table_n * sizeof(uint16_t);
+    const size_t tbytes = s->table_n * 3;  // 16-bit CDF + 8-bit guide
     P.table_u4 = (uint32_t)(tbytes / 16);
-    const bool smem = DTS_TABLE_SMEM && tbytes <= 200 * 1024;
+    const bool smem = DTS_TABLE_SMEM && tbytes <= 220 * 1024;
     int blocks_per_sm = 1;
     if (smem) {
       CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes));
