@@ -106,8 +106,9 @@ typedef struct {
 /* Debug record: one DARTS vertex with caller-fixed state and raw Philox words.
  * kind: 0 camera/detector vertex (k = 0, direction fixed = w), 1 medium vertex
  * (w = incoming direction w_{k-1}), 2 wall vertex (face = wall index).
- * u_i = (r_i >> 8) * 2^-24 (R24): u0 event, u1 Sobol row, u2 CP shift, u3 RIS
- * select, u4 technique, u5 cos/bin, u6 phi, u7 connection, u8/u9 SPLIT walk. */
+ * u_i = (r_i >> 9) * 2^-23 (R24): u0 event, u1 Sobol row, u2 CP shift, u3 RIS
+ * select, u4 technique, u5 cos/bin, u6 phi, u7 connection; the SPLIT walk's
+ * u8/u9 come from the low bits of r0..r2 / r3..r5; r8..r11 are reserved. */
 typedef struct {
   int32_t kind, face, bin, emitter;
   float x[3], w[3];

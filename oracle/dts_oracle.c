@@ -45,8 +45,8 @@ void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
   out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* R24: uint32 -> [0,1) with 24 significant bits; never 1.0. */
-double or_uniform(uint32_t r) { return (double)(r >> 8) * (1.0 / 16777216.0); }
+/* R24: uint32 -> [0,1) with the top 23 bits (an fp32 mantissa); never 1.0. */
+double or_uniform(uint32_t r) { return (double)(r >> 9) * (1.0 / 8388608.0); }
 
 static void draw4(uint64_t seed, uint64_t id, uint32_t bounce, uint32_t block, uint32_t out[4]) {
   uint32_t ctr[4] = {(uint32_t)id, (uint32_t)(id >> 32), bounce, block};
@@ -392,12 +392,13 @@ typedef struct {
 
 static double uu(const uint32_t r[12], int i) { return or_uniform(r[i]); }
 
-/* R24, SPLIT walk direction: u8 and u9 are the 24-bit integers formed by the
- * low bytes (left unused by u0..u7) of r0, r1, r2 and of r3, r4, r5. */
+/* R24, SPLIT walk direction: u8 and u9 are the 23-bit integers formed by the
+ * low bits (left unused by u0..u7) of r0, r1, r2 and of r3, r4, r5:
+ * (r_a & 0x7F) << 16 | (r_b & 0xFF) << 8 | (r_c & 0xFF). */
 static double u_split(const uint32_t r[12], int which) {
   const uint32_t* a = r + 3 * which;
-  uint32_t m = ((a[0] & 0xFFu) << 16) | ((a[1] & 0xFFu) << 8) | (a[2] & 0xFFu);
-  return (double)m * (1.0 / 16777216.0);
+  uint32_t m = ((a[0] & 0x7Fu) << 16) | ((a[1] & 0xFFu) << 8) | (a[2] & 0xFFu);
+  return (double)m * (1.0 / 8388608.0);
 }
 
 /* connection along wc from x, medium interval [lo, hi) of that ray.  Returns
@@ -612,7 +613,7 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
     if (u4 < gamma) {
       /* EDA: inverse transform of the cell's cos(theta) CDF */
       tech = 1;
-      double T = (double)(r[5] >> 8) / 256.0; /* = u5 * 65536 */
+      double T = (double)(r[5] >> 9) / 128.0; /* = u5 * 65536 */
       int j = 0;
       for (int jj = 0; jj < 256; ++jj)
         if ((double)qc[jj] <= T) j = jj;

@@ -95,7 +95,9 @@ __device__ __forceinline__ u4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint
   }
   return u4{c0, c1, c2, c3};
 }
-__device__ __forceinline__ float unif(uint32_t r) { return __uint2float_rn(r >> 8) * 5.9604644775390625e-08f; }
+// R24: u = (r >> 9) 2^-23, built as a float in [1, 2) minus one (no int->float conversion)
+__device__ __forceinline__ float mant01(uint32_t m23) { return __uint_as_float(0x3f800000u | m23) - 1.0f; }
+__device__ __forceinline__ float unif(uint32_t r) { return mant01(r >> 9); }
 
 // ----------------------------------------------------------------- accurate small-argument helpers
 // -ln(1 - x) for x in [0, 1): series x + x^2/2 + x^3/3 below 1/64 (relative
@@ -245,11 +247,10 @@ __device__ __forceinline__ uint32_t gload(const uint8_t* g, int i) {
   return __ldg(g + i);
 }
 
-// R24: the SPLIT walk direction uses u8, u9 = the 24-bit integers formed by the
-// low bytes (unused by u0..u7) of r0, r1, r2 and of r3, r4, r5.
+// R24: the SPLIT walk direction uses u8, u9 = the 23-bit integers formed by the
+// low bits (unused by u0..u7) of r0, r1, r2 and of r3, r4, r5.
 __device__ __forceinline__ float u_split(uint32_t a, uint32_t b, uint32_t c) {
-  const uint32_t m = ((a & 0xFFu) << 16) | ((b & 0xFFu) << 8) | (c & 0xFFu);
-  return (float)m * 5.9604644775390625e-08f;
+  return mant01(((a & 0x7Fu) << 16) | ((b & 0xFFu) << 8) | (c & 0xFFu));
 }
 
 // ----------------------------------------------------------------- one DARTS vertex
@@ -331,7 +332,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const int mid = (j + jh + 1) >> 1;
       if (qload<SMEM>(qc, mid) <= Ti) j = mid; else jh = mid - 1;
     }
-    const float T = (float)(r[5] >> 8) * (1.0f / 256.0f);
+    const float T = (float)(r[5] >> 9) * (1.0f / 128.0f);
     float qa = (float)qload<SMEM>(qc, j);
     float qb = j == 255 ? 65536.0f : (float)qload<SMEM>(qc, j + 1);
     const float iq = __fdividef(1.0f, qb - qa);
@@ -536,9 +537,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   if (u0 < p_m) {
     // candidates: Sobol row r = floor(32 u1) with Cranley-Patterson shift u2 (R6):
     // Q[r][i] = RI2(8r+i) = bitrev3(i)/8 + bitrev5(r)/256, shift and mod 1 done
-    // exactly on 24-bit integers.
+    // exactly on 23-bit integers.
     const uint32_t br5 = __brev(r[1] >> 27) >> 27;
-    const uint32_t m2 = r[2] >> 8;
+    const uint32_t m2 = r[2] >> 9;
     const f3 cv = xe - ps.x;
     const float qd = dot(ww, cv);
     const f3 perp = cv - ww * qd;
@@ -548,8 +549,8 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t br3 = __brev((uint32_t)i) >> 29;
-      const uint32_t v = (m2 + ((br3 * 32u + br5) << 16)) & 0xFFFFFFu;
-      const float ui = (float)v * 5.9604644775390625e-08f;
+      const uint32_t v = (m2 + ((br3 * 32u + br5) << 15)) & 0x7FFFFFu;
+      const float ui = mant01(v);
       // E14 with the sign of R1: d = t_lo - ln(1 - p_m u) / sigma_t with
       // 1 - p_m u = (1 - u) + u (1 - p_m) (1 - u exact); MUFU lg2 keeps the
       // absolute error of d below ~1e-7 / sigma_t
@@ -595,8 +596,8 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     }
     // regenerate the selected candidate's distance (cheaper than keeping all 8)
     const uint32_t brs = __brev(is) >> 29;
-    const uint32_t vs = (m2 + ((brs * 32u + br5) << 16)) & 0xFFFFFFu;
-    const float us = (float)vs * 5.9604644775390625e-08f;
+    const uint32_t vs = (m2 + ((brs * 32u + br5) << 15)) & 0x7FFFFFu;
+    const float us = mant01(vs);
     const float dsel = fmaf(-__log2f(fmaf(us, T_m, 1.0f - us)), S.inv_sigma_t * kLn2, lo);
     const float beta_ris = S.albedo * (W * 0.125f) * __fdividef(1.0f, wsel);  // E15: a * mean(w) / w*
     ps.beta *= beta_ris;
