@@ -207,12 +207,47 @@ __device__ __forceinline__ int intersect(const DevScene& S, f3 o, f3 d, float& l
   return ((S.wall_mask >> ff) & 1u) ? HIT_WALL : HIT_OPEN;
 }
 
+// Exit of a ray that starts inside the medium (medium and wall vertices,
+// control vertices): lo = 0 and only the far root / the nearest exit plane is
+// needed.  Same result as intersect() for an inside origin.
+__device__ __forceinline__ int intersect_inside(const DevScene& S, f3 o, f3 d, float& lo, float& hi, int& face) {
+  lo = 0.0f;
+  face = -1;
+  if (S.medium_shape == DTS_MEDIUM_INFINITE) {
+    hi = __int_as_float(0x7f800000);
+    return HIT_NONE;
+  }
+  if (S.medium_shape == DTS_MEDIUM_SPHERE) {
+    const f3 oc = o - ld3(S.center);
+    const float b = dot(oc, d);
+    const float c = dot(oc, oc) - S.radius2;
+    const float disc = b * b - c;
+    if (!(disc > 0.0f)) return HIT_MISS;
+    const float s = sqrtf(disc);
+    const float tf = b > 0.0f ? -c * __fdividef(1.0f, b + s) : s - b;
+    if (!(tf > 0.0f)) return HIT_MISS;
+    hi = tf;
+    return HIT_OPEN;
+  }
+  const float tx = ((d.x > 0.0f ? S.bmax[0] : S.bmin[0]) - o.x) * __fdividef(1.0f, d.x);
+  const float ty = ((d.y > 0.0f ? S.bmax[1] : S.bmin[1]) - o.y) * __fdividef(1.0f, d.y);
+  const float tz = ((d.z > 0.0f ? S.bmax[2] : S.bmin[2]) - o.z) * __fdividef(1.0f, d.z);
+  const float tf = fminf(fminf(tx, ty), tz);  // NaN (0 * inf) of an axis-parallel ray is dropped
+  if (!(tf > 0.0f)) return HIT_MISS;
+  const int axis = (tx == tf) ? 0 : ((ty == tf) ? 1 : 2);
+  const float da = axis == 0 ? d.x : (axis == 1 ? d.y : d.z);
+  const int ff = 2 * axis + (da > 0.0f ? 1 : 0);
+  hi = tf;
+  face = ff;
+  return ((S.wall_mask >> ff) & 1u) ? HIT_WALL : HIT_OPEN;
+}
+
 // medium length and visibility of the segment p -> xe (p inside the medium)
 __device__ __forceinline__ float segment_tr(const DevScene& S, f3 p, f3 xe, float r, f3 dir) {
   if (S.medium_shape == DTS_MEDIUM_INFINITE) return fexp(-S.sigma_t * r);
   float lo, hi;
   int face;
-  const int hit = intersect(S, p, dir, lo, hi, face);
+  const int hit = intersect_inside(S, p, dir, lo, hi, face);
   if (hit == HIT_MISS) return 1.0f;
   if (hit == HIT_WALL && hi < r) return 0.0f;  // occluded by a wall (R15)
   const float len = fmaxf(0.0f, fminf(hi, r) - lo);
@@ -383,12 +418,13 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   // ---- intersection, reused by the connection and the walk ----
   float lo = 0.0f, hi = 0.0f;
   int face = -1;
-  const int hit = intersect(S, ps.x, ww, lo, hi, face);
+  const int hit = ps.kind == KIND_CAMERA ? intersect(S, ps.x, ww, lo, hi, face)
+                                         : intersect_inside(S, ps.x, ww, lo, hi, face);
   float clo = lo, chi = hi;
   int hitc = hit;
   if (S.direction_mode == DTS_DIR_SPLIT && ps.kind == KIND_MEDIUM) {
     int fc;
-    hitc = intersect(S, ps.x, wc, clo, chi, fc);
+    hitc = intersect_inside(S, ps.x, wc, clo, chi, fc);
   }
   if (DBG) {
     dbg->t_lo = lo; dbg->t_hi = hi; dbg->hit = hit; dbg->face_hit = face;
@@ -560,7 +596,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const float dq = di - qd;
       const float r2i = fmaf(dq, dq, perp2);
       const bool valid = (Delta > 0.0f) && (r2i <= Delta * Delta);
-      const float s = rsqrtf(Delta);
+      const float s = rsqrtf(fmaxf(Delta, 1e-20f));  // s^3 stays finite for invalid candidates
       // log2 of Phi' = Delta^{-3/2} exp(-r^2/(4 D Delta) - sigma_a Delta) (E9, constants dropped)
       const float ex = fmaf(S.neg_inv4D_log2e * r2i, s * s, S.neg_sa_log2e * Delta);
       e2[i] = valid ? ex : -__int_as_float(0x7f800000);
@@ -568,9 +604,10 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       emax = fmaxf(emax, e2[i]);
     }
     float W = 0.0f;
+    if (emax == -__int_as_float(0x7f800000)) emax = 0.0f;  // all invalid: exp2(-inf) = 0, not NaN
 #pragma unroll
     for (int i = 0; i < 8; ++i) {  // R7: weights relative to the largest exponent
-      e2[i] = e2[i] > -__int_as_float(0x7f800000) ? sr[i] * sr[i] * sr[i] * exp2f(e2[i] - emax) : 0.0f;
+      e2[i] = sr[i] * sr[i] * sr[i] * exp2f(e2[i] - emax);
       W += e2[i];
     }
     if (DBG) {
