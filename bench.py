@@ -111,7 +111,8 @@ def _dist_env():
 
 
 def _shard(spp: int, rank: int, world: int):
-    return spp * rank // world, spp * (rank + 1) // world
+    from paper_2402_03106_b200.shard import shard_range
+    return shard_range(spp, rank, world)
 
 
 # --------------------------------------------------------------------------- GPU arm
