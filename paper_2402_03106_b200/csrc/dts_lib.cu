@@ -176,6 +176,7 @@ struct RenderParams {
   uint32_t cw;       // crop width
   uint32_t table_u4; // table size in 16-byte words
   uint32_t spp_div_b, spp_mod_b;  // SPP_PER_PIXEL cell counts (R21)
+  uint32_t priv_cells;            // > 0: the CTA privatises the whole histogram in shared memory
 };
 
 #ifndef DTS_BLOCK
@@ -183,6 +184,7 @@ struct RenderParams {
 #endif
 constexpr int kBlock = DTS_BLOCK;
 constexpr uint32_t kChunk = 128;
+constexpr size_t kPrivMaxCells = 4096;  // histograms up to 16 KiB are privatised per CTA
 
 struct PathCtx {
   PathState ps;
@@ -295,24 +297,100 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   return true;
 }
 
-template <bool SMEM>
+// ---------------------------------------------------------------- TMA 1-D bulk staging
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Copies `bytes` (multiple of 16, both addresses 16-byte aligned) from global
+// to shared memory with cp.async.bulk (the TMA unit's non-tensor mode), one
+// elected thread issuing, completion tracked by an mbarrier transaction count;
+// every thread of the CTA returns once the data has landed.
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = smem_u32(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    constexpr uint32_t kPiece = 32768;
+    for (uint32_t off = 0; off < bytes; off += kPiece) {
+      const uint32_t n = bytes - off < kPiece ? bytes - off : kPiece;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(static_cast<char*>(dst) + off)),
+                   "l"(static_cast<const char*>(src) + off), "r"(n), "r"(b)
+                   : "memory");
+    }
+  }
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(b)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- histogram splat (step 4)
+// Per-bin dedicated paths: a retiring path adds its whole
+// contribution to its own cell.  Lanes that retire in the same iteration on the
+// same cell (consecutive sample ids of one cell) are combined first
+// (__match_any_sync + shuffles, one RED per distinct cell and warp); the RED
+// goes to a shared-memory copy of the histogram when the CTA privatises it
+// (small histograms, flushed once at kernel end), else to HBM/L2.
+__device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, float v, float v2, float* g_hist,
+                                      float* g_sq, float* s_hist, float* s_sq, int lane) {
+  if (!done) return;
+  const unsigned peers = __match_any_sync(dmask, cell);
+  const int leader = __ffs(peers) - 1;
+  const int n = __popc(peers);
+  const int nmax = __reduce_max_sync(dmask, n);
+  unsigned m = peers & (peers - 1u);  // peers above the leader, consumed one per step
+  for (int i = 1; i < nmax; ++i) {
+    const int src = (lane == leader && m) ? __ffs(m) - 1 : lane;
+    const float o = __shfl_sync(dmask, v, src);
+    const float o2 = __shfl_sync(dmask, v2, src);
+    if (lane == leader && m) {
+      v += o;
+      v2 += o2;
+      m &= m - 1u;
+    }
+  }
+  if (lane != leader || v == 0.0f) return;
+  if (s_hist) {
+    atomicAdd(s_hist + cell, v);
+    if (s_sq) atomicAdd(s_sq + cell, v2);
+  } else {
+    atomicAdd(g_hist + cell, v);
+    if (g_sq) atomicAdd(g_sq + cell, v2);
+  }
+}
+
 #ifndef DTS_MINB
 #define DTS_MINB 1
 #endif
 #ifndef DTS_TABLE_SMEM
 #define DTS_TABLE_SMEM 1
 #endif
+template <bool SMEM>
 __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const RenderParams P) {
-  extern __shared__ __align__(16) uint16_t s_tab[];
+  extern __shared__ __align__(16) uint16_t s_dyn[];
+  __shared__ uint64_t s_bar;
   const DevScene& S = P.S;
   const uint16_t* tab = P.tab;
-  if (SMEM) {
-    const uint4* src = reinterpret_cast<const uint4*>(P.tab);
-    uint4* dst = reinterpret_cast<uint4*>(s_tab);
-    for (uint32_t i = threadIdx.x; i < P.table_u4; i += blockDim.x) dst[i] = __ldg(src + i);
-    __syncthreads();
-    tab = s_tab;
+  // dynamic shared memory: [EDA table (SMEM)] [private histogram] [private hist_sq]
+  float* s_hist = nullptr;
+  float* s_sq = nullptr;
+  {
+    char* base = reinterpret_cast<char*>(s_dyn) + (SMEM ? (size_t)P.table_u4 * 16 : 0);
+    if (P.priv_cells) {
+      s_hist = reinterpret_cast<float*>(base);
+      if (P.hist_sq) s_sq = s_hist + P.priv_cells;
+      const uint32_t n = P.priv_cells * (P.hist_sq ? 2u : 1u);
+      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s_hist[i] = 0.0f;
+    }
   }
+  if (SMEM) {
+    bulk_stage(s_dyn, P.tab, P.table_u4 * 16u, &s_bar);
+    tab = s_dyn;
+  }
+  __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -391,15 +469,18 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       c_cap += __popc(__ballot_sync(FULL, cap));
     }
     c_vert += __popc(act);
-    if (done) {
-      float v = pc.acc;
-      if (isfinite(v)) {
-        if (v != 0.0f) {
-          atomicAdd(P.hist + pc.cell, v * pc.inv_n);
-          if (P.hist_sq) atomicAdd(P.hist_sq + pc.cell, v * v * pc.inv_n);
-        }
-      }
-      active = false;
+    const unsigned dmask = __ballot_sync(FULL, done);
+    if (dmask) {
+      const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
+      splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane);
+      if (done) active = false;
+    }
+  }
+  if (P.priv_cells) {  // flush the CTA's private histogram (coalesced REDs of its non-zero cells)
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < P.priv_cells; i += blockDim.x) {
+      if (s_hist[i] != 0.0f) atomicAdd(P.hist + i, s_hist[i]);
+      if (s_sq && s_sq[i] != 0.0f) atomicAdd(P.hist_sq + i, s_sq[i]);
     }
   }
   // c_paths was counted per lane; reduce across the warp
@@ -833,12 +914,19 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     const size_t tbytes = s->table_n * 3;  // 16-bit CDF + 8-bit guide
     P.table_u4 = (uint32_t)(tbytes / 16);
     const bool smem = DTS_TABLE_SMEM && tbytes <= 220 * 1024;
+    // privatise small histograms (config 1: 128 cells) in shared memory
+    const size_t cells = dts_hist_cells(s);
+    const size_t pbytes = cells * sizeof(float) * (d_hist_sq ? 2 : 1);
+    const size_t kSmemCap = 227 * 1024 - 64;
+    if (cells <= kPrivMaxCells && (smem ? tbytes : 0) + pbytes <= kSmemCap) P.priv_cells = (uint32_t)cells;
+    const size_t dyn = (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0);
     int blocks_per_sm = 1;
     if (smem) {
-      CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<true>, kBlock, tbytes));
+      CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<true>, kBlock, dyn));
     } else {
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<false>, kBlock, 0));
+      CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<false>, kBlock, dyn));
     }
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     uint64_t grid = (uint64_t)s->num_sms * blocks_per_sm;
@@ -846,14 +934,14 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     if (grid > need) grid = need;
     CUDA_TRY(cudaMemsetAsync(s->d_work, 0, sizeof(unsigned long long), st));
     if (smem)
-      render_darts_kernel<true><<<(unsigned)grid, kBlock, tbytes, st>>>(P);
+      render_darts_kernel<true><<<(unsigned)grid, kBlock, dyn, st>>>(P);
     else
-      render_darts_kernel<false><<<(unsigned)grid, kBlock, 0, st>>>(P);
+      render_darts_kernel<false><<<(unsigned)grid, kBlock, dyn, st>>>(P);
     CUDA_TRY(cudaGetLastError());
     g_last_launches = 1;
     g_last_grid = (int)grid;
     g_last_block = kBlock;
-    g_last_smem = smem ? (int)tbytes : 0;
+    g_last_smem = (int)dyn;
   } else {
     P.total = npix * ns;
     int bps = 1;
