@@ -59,6 +59,7 @@ struct DevScene {
   uint32_t table_n;        // CDF entries; an 8-bit guide table of the same length follows them
   float ln_smin, inv_dls;  // ns / (ln smax - ln smin)
   uint32_t seed_lo, seed_hi;
+  uint32_t rk[20];  // Philox round keys (k0_r, k1_r), r = 0..9, of the launch's seed
 };
 
 // ----------------------------------------------------------------- vectors
@@ -75,23 +76,23 @@ __device__ __forceinline__ f3 ld3(const float* p) { return mk(p[0], p[1], p[2]);
 
 // ----------------------------------------------------------------- RNG (R24)
 // Philox4x32-10 (Salmon et al. 2011); counter = (id_lo, id_hi, bounce, block).
+// The key schedule depends only on the seed: the 10 round keys are computed
+// once per launch on the host (DevScene::rk) and read from the constant bank,
+// so a round is 2 IMAD.WIDE.U32 + 2 LOP3.
 struct u4 {
   uint32_t a, b, c, d;
 };
-__device__ __forceinline__ u4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
-                                     uint32_t k1) {
+__device__ __forceinline__ u4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const uint32_t* rk) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;  // IMAD.WIDE.U32
     const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
     const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r], n2 = hi0 ^ c3 ^ rk[2 * r + 1];
     c0 = n0;
     c1 = lo1;
     c2 = n2;
     c3 = lo0;
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
   }
   return u4{c0, c1, c2, c3};
 }
@@ -166,14 +167,15 @@ __device__ __forceinline__ void hg_sample(const DevScene& S, float u, float& opc
 }
 
 // ----------------------------------------------------------------- medium bounds (R15)
+template <int SH, bool WALLS>
 __device__ __forceinline__ int intersect(const DevScene& S, f3 o, f3 d, float& lo, float& hi, int& face) {
   face = -1;
-  if (S.medium_shape == DTS_MEDIUM_INFINITE) {
+  if (SH == DTS_MEDIUM_INFINITE) {
     lo = 0.0f;
     hi = __int_as_float(0x7f800000);
     return HIT_NONE;
   }
-  if (S.medium_shape == DTS_MEDIUM_SPHERE) {
+  if (SH == DTS_MEDIUM_SPHERE) {
     const f3 oc = o - ld3(S.center);
     const float b = dot(oc, d);
     const float c = dot(oc, oc) - S.radius2;
@@ -204,20 +206,21 @@ __device__ __forceinline__ int intersect(const DevScene& S, f3 o, f3 d, float& l
   lo = tn;
   hi = tf;
   face = ff;
-  return ((S.wall_mask >> ff) & 1u) ? HIT_WALL : HIT_OPEN;
+  return (WALLS && ((S.wall_mask >> ff) & 1u)) ? HIT_WALL : HIT_OPEN;
 }
 
 // Exit of a ray that starts inside the medium (medium and wall vertices,
 // control vertices): lo = 0 and only the far root / the nearest exit plane is
 // needed.  Same result as intersect() for an inside origin.
+template <int SH, bool WALLS>
 __device__ __forceinline__ int intersect_inside(const DevScene& S, f3 o, f3 d, float& lo, float& hi, int& face) {
   lo = 0.0f;
   face = -1;
-  if (S.medium_shape == DTS_MEDIUM_INFINITE) {
+  if (SH == DTS_MEDIUM_INFINITE) {
     hi = __int_as_float(0x7f800000);
     return HIT_NONE;
   }
-  if (S.medium_shape == DTS_MEDIUM_SPHERE) {
+  if (SH == DTS_MEDIUM_SPHERE) {
     const f3 oc = o - ld3(S.center);
     const float b = dot(oc, d);
     const float c = dot(oc, oc) - S.radius2;
@@ -234,22 +237,24 @@ __device__ __forceinline__ int intersect_inside(const DevScene& S, f3 o, f3 d, f
   const float tz = ((d.z > 0.0f ? S.bmax[2] : S.bmin[2]) - o.z) * __fdividef(1.0f, d.z);
   const float tf = fminf(fminf(tx, ty), tz);  // NaN (0 * inf) of an axis-parallel ray is dropped
   if (!(tf > 0.0f)) return HIT_MISS;
+  hi = tf;
+  if (!WALLS) return HIT_OPEN;  // the exit face only matters when some face is a wall
   const int axis = (tx == tf) ? 0 : ((ty == tf) ? 1 : 2);
   const float da = axis == 0 ? d.x : (axis == 1 ? d.y : d.z);
   const int ff = 2 * axis + (da > 0.0f ? 1 : 0);
-  hi = tf;
   face = ff;
   return ((S.wall_mask >> ff) & 1u) ? HIT_WALL : HIT_OPEN;
 }
 
 // medium length and visibility of the segment p -> xe (p inside the medium)
+template <int SH, bool WALLS>
 __device__ __forceinline__ float segment_tr(const DevScene& S, f3 p, f3 xe, float r, f3 dir) {
-  if (S.medium_shape == DTS_MEDIUM_INFINITE) return fexp(-S.sigma_t * r);
+  if (SH == DTS_MEDIUM_INFINITE) return fexp(-S.sigma_t * r);
   float lo, hi;
   int face;
-  const int hit = intersect_inside(S, p, dir, lo, hi, face);
+  const int hit = intersect_inside<SH, WALLS>(S, p, dir, lo, hi, face);
   if (hit == HIT_MISS) return 1.0f;
-  if (hit == HIT_WALL && hi < r) return 0.0f;  // occluded by a wall (R15)
+  if (WALLS && hit == HIT_WALL && hi < r) return 0.0f;  // occluded by a wall (R15)
   const float len = fmaxf(0.0f, fminf(hi, r) - lo);
   return fexp(-S.sigma_t * len);
 }
@@ -288,13 +293,133 @@ __device__ __forceinline__ float u_split(uint32_t a, uint32_t b, uint32_t c) {
   return mant01(((a & 0x7Fu) << 16) | ((b & 0xFFu) << 8) | (c & 0xFFu));
 }
 
+// ----------------------------------------------------------------- elliptical connection (E20-E22)
+// Samples S on [C + dlo, C + dlo + width) from the truncated exponential of
+// PAPER.md:295 and maps it to the polar distance t of E21; p_t is E22 with the
+// Jacobian of R2.  cv = xe - x, C = |cv|, q = wc . cv.
+struct EllSample {
+  float t, pt, pSt, S;  // pSt = S - t (= r2 on the ellipse)
+};
+__device__ __forceinline__ EllSample ell_sample(const DevScene& S, f3 cv, float C, float q, f3 wc, float dlo,
+                                                float width, float u7) {
+  // truncated exponential on [S_lo, S_hi); e^{-st (S-S_lo)} = 1 - u7 span
+  const float span = one_m_exp(S.sigma_t * width);
+  const float keep = fmaf(u7, fexp(-S.sigma_t * width), 1.0f - u7);  // 1 - u7 span
+  const float L = neg_log1m2(u7 * span, keep) * S.inv_sigma_t;
+  const float pS = S.sigma_t * keep * __fdividef(1.0f, span);
+  const float dSC = dlo + L;  // S - C
+  const float Ssm = C + dSC;
+  // S - q = (S - C) + (C - q), C - q = perp^2 / (C + q) for q > 0
+  const f3 pv = cv - wc * q;
+  const float perp2 = dot(pv, pv);
+  const float Cmq = q > 0.0f ? perp2 * __fdividef(1.0f, C + q) : C - q;
+  const float Smq = dSC + Cmq;
+  const float inv2Smq = __fdividef(0.5f, Smq);
+  EllSample e;
+  e.S = Ssm;
+  e.t = dSC * (Ssm + C) * inv2Smq;        // E21: (S^2 - C^2) / (2 (S - q))
+  e.pSt = (Smq * Smq + perp2) * inv2Smq;  // S - t
+  e.pt = pS * Smq * __fdividef(1.0f, e.pSt);  // E22 with the Jacobian of R2
+  return e;
+}
+
+// Admissible S range of a connection along wc (case I, R14): S(t) = t +
+// |x + wc t - xe| is non-decreasing, so the range is
+// [max(Rm - E, S(clo)), min(RM - E, S(chi))).  Returned relative to C (S - C),
+// formed without cancellation: S(t) - C = t + t (t - 2q) / (|x + wc t - xe| + C),
+// (Rm - E) - C in double.  width = S_hi - S_lo, exact to rounding when both
+// bounds are bin bounds.
+struct SRange {
+  float dlo, dhi, width;
+};
+__device__ __forceinline__ SRange conn_range(const DevScene& S, f3 x, f3 wc, f3 xe, float C, float q, float clo,
+                                             float chi, double resM) {
+  const f3 plo = fma3(wc, clo, x) - xe;
+  const float lo_m_C = clo + clo * (clo - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(plo, plo)) + C);
+  float hi_m_C = __int_as_float(0x7f800000);
+  if (isfinite(chi)) {
+    const f3 phi_ = fma3(wc, chi, x) - xe;
+    hi_m_C = chi + chi * (chi - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(phi_, phi_)) + C);
+  }
+  const double dM_d = resM - (double)C;
+  const double dm_d = dM_d - S.dt;
+  SRange r;
+  r.dlo = (float)dm_d;
+  bool lo_bin = true;
+  if (lo_m_C > r.dlo) { r.dlo = lo_m_C; lo_bin = false; }
+  if (S.s_excess > 0.0f && S.s_excess > r.dlo) { r.dlo = S.s_excess; lo_bin = false; }
+  const bool hi_bin = (float)dM_d <= hi_m_C;
+  r.dhi = hi_bin ? (float)dM_d : hi_m_C;
+  r.width = lo_bin && hi_bin ? (float)S.dt
+                             : (float)((hi_bin ? dM_d : (double)hi_m_C) - (lo_bin ? dm_d : (double)r.dlo));
+  return r;
+}
+
+// Contribution of the control vertex x_ell = x + wc t connected to the emitter
+// (E2 throughput: sigma_s, transmittance of both legs, HG at x_ell, inverse
+// square, pulse intensity), divided by p_t.  coef = beta (x the MIS/SPLIT
+// connection weight, x 1/n_cell for a deferred splat).  pSt > 0: r2 = S - t.
+template <int SH, bool WALLS>
+__device__ __forceinline__ float conn_contrib(const DevScene& S, f3 x, f3 wc, f3 xe, float ek, float t, float pt,
+                                              float pSt, float clo, float coef, f3* xell_out, float* r2_out) {
+  const f3 xell = fma3(wc, t, x);
+  const f3 de = xe - xell;
+  float r2sq = dot(de, de);
+  float r2 = sqrtf(r2sq);
+  const f3 we = de * __fdividef(1.0f, r2);
+  if (pSt > 0.0f) {  // on the ellipse r2 = S - t, formed without cancellation
+    r2 = pSt;
+    r2sq = pSt * pSt;
+  }
+  const float rho = hg_eval(S, dot(wc, we));
+  const float tr = fexp(-S.sigma_t * (t - clo)) * segment_tr<SH, WALLS>(S, xell, xe, r2, we);
+  float c = coef * S.sigma_s * tr * rho * ek * __fdividef(1.0f, r2sq * pt);
+  if (S.r_excl > 0.0f && r2 < S.r_excl) c = 0.0f;
+  if (xell_out) *xell_out = xell;
+  if (r2_out) *r2_out = r2;
+  return c;
+}
+
+// Runs a queued connection from an inside vertex (clo = 0) whose S range
+// [C + dlo, C + dlo + width) is known and non-empty: S sample (E21-E22) and
+// contribution (coef included).  m7e = u7's 23 bits | emitter << 23.
+template <int SH, bool WALLS>
+__device__ __forceinline__ float conn_job_run(const DevScene& S, f3 x, f3 wc, float dlo, float width, float coef,
+                                              uint32_t m7e) {
+  const int e = (int)(m7e >> 23);
+  const f3 xe = ld3(S.em_pos[e]);
+  const f3 cv = xe - x;
+  const float C = sqrtf(dot(cv, cv));
+  const float q = dot(wc, cv);
+  const EllSample es = ell_sample(S, cv, C, q, wc, dlo, width, mant01(m7e & 0x7FFFFFu));
+  return conn_contrib<SH, WALLS>(S, x, wc, xe, S.em_k[e], es.t, es.pt, es.pSt, 0.0f, coef, nullptr, nullptr);
+}
+
+// Deferred connections (render kernel only): a medium or wall vertex whose
+// connection S range is non-empty writes a job into its warp's shared-memory
+// queue; the warp later runs up to 32 queued jobs at once, one per lane
+// (conn_job_run), so the ~5-10 % of vertices that connect no longer run the
+// S sample and contribution at a few active lanes.
+constexpr int kJobWords = 11;  // x[3] w[3] dlo width coef m7e cell
+constexpr int kQueue = 32;     // slots per warp
+struct Defer {
+  float* q;           // this warp's queue: word f of slot j at q[f * qstride + j]
+  uint32_t qstride;   // words between fields (= kQueue * warps per CTA)
+  uint32_t qn;        // jobs queued (warp-uniform)
+  unsigned act;       // lanes executing darts_vertex
+  uint32_t lane_lt;   // lanes below this one
+  uint32_t cell;      // the path's histogram cell
+  float inv_n;        // 1 / paths of the cell
+};
+
 // ----------------------------------------------------------------- one DARTS vertex
 // Returns true if the walk continues.  contrib receives the vertex's
 // connection (+ wall NEE) contribution; end_reason the DTS_CTR_* of a stop.
-template <bool DBG, bool SMEM>
+template <bool DBG, bool SMEM, int SH, bool WALLS, bool SPLIT>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
-                                             bool& conn_nonempty, bool& wall_nee, int& end_reason) {
+                                             bool& conn_nonempty, bool& wall_nee, int& end_reason,
+                                             const Defer* df = nullptr, bool* pushed = nullptr) {
   contrib = 0.0f;
   conn_nonempty = false;
   wall_nee = false;
@@ -312,7 +437,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       dbg->tech = 2;
       dbg->beta_dir = 1.0f;
     }
-  } else if (ps.kind == KIND_WALL) {
+  } else if (WALLS && ps.kind == KIND_WALL) {
     const f3 n = inward_normal(ps.face);
     const float alb = S.wall_albedo[ps.face];
     const f3 cv = xe - ps.x;
@@ -323,7 +448,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     float nee = 0.0f;
     if (cw > 0.0f && resm - C <= 0.0f && resM - C > 0.0f) {  // E + C in [Rm, RM)
       // R14: time-checked direct NEE at a wall vertex
-      nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr(S, ps.x, xe, C, we) * __fdividef(1.0f, C * C);
+      nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr<SH, WALLS>(S, ps.x, xe, C, we) * __fdividef(1.0f, C * C);
       if (S.r_excl > 0.0f && C < S.r_excl) nee = 0.0f;
       contrib += nee;
       wall_nee = nee > 0.0f;
@@ -389,7 +514,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float p_mix = gamma * p_eda + (1.0f - gamma) * p_hg;
     const float ratio_w = __fdividef(p_hg, p_mix);
     wc = om;
-    if (S.direction_mode == DTS_DIR_SPLIT) {
+    if (SPLIT) {
       // R29 SPLIT: MIS weight on the connection only; independent HG walk direction
       wconn = ratio_w;
       float o2, m2;
@@ -418,13 +543,17 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   // ---- intersection, reused by the connection and the walk ----
   float lo = 0.0f, hi = 0.0f;
   int face = -1;
-  const int hit = ps.kind == KIND_CAMERA ? intersect(S, ps.x, ww, lo, hi, face)
-                                         : intersect_inside(S, ps.x, ww, lo, hi, face);
+  const int hit = ps.kind == KIND_CAMERA ? intersect<SH, WALLS>(S, ps.x, ww, lo, hi, face)
+                                         : intersect_inside<SH, WALLS>(S, ps.x, ww, lo, hi, face);
+  // render kernel: non-empty connections of medium/wall vertices are queued (df)
+  const bool defer = !DBG && df && ps.kind != KIND_CAMERA;
+  bool want_job = false;
+  float job_dlo = 0.0f, job_width = 0.0f;
   float clo = lo, chi = hi;
   int hitc = hit;
-  if (S.direction_mode == DTS_DIR_SPLIT && ps.kind == KIND_MEDIUM) {
+  if (SPLIT && ps.kind == KIND_MEDIUM) {
     int fc;
-    hitc = intersect_inside(S, ps.x, wc, clo, chi, fc);
+    hitc = intersect_inside<SH, WALLS>(S, ps.x, wc, clo, chi, fc);
   }
   if (DBG) {
     dbg->t_lo = lo; dbg->t_hi = hi; dbg->hit = hit; dbg->face_hit = face;
@@ -442,47 +571,20 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     float pSt = 0.0f;  // S - t (= r2 on the ellipse)
     bool ok = false;
     if (!(S.warped == 0 && ps.kind == KIND_CAMERA)) {
-      // S(t) = t + |x + wc t - xe| is non-decreasing; admissible S range
-      // [max(Rm - E, S(clo)), min(RM - E, S(chi))) (case I, R14).  Work with
-      // S - C, formed without cancellation:
-      //   S(t) - C = t + t (t - 2q) / (|x + wc t - xe| + C),  (Rm - E) - C in double.
-      const f3 plo = fma3(wc, clo, ps.x) - xe;
-      const float lo_m_C = clo + clo * (clo - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(plo, plo)) + C);
-      float hi_m_C = __int_as_float(0x7f800000);
-      if (isfinite(chi)) {
-        const f3 phi_ = fma3(wc, chi, ps.x) - xe;
-        hi_m_C = chi + chi * (chi - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(phi_, phi_)) + C);
-      }
-      const double dM_d = ps.resM - (double)C;
-      const double dm_d = dM_d - S.dt;
-      float dlo = (float)dm_d;
-      bool lo_bin = true;
-      if (lo_m_C > dlo) { dlo = lo_m_C; lo_bin = false; }
-      if (S.s_excess > 0.0f && S.s_excess > dlo) { dlo = S.s_excess; lo_bin = false; }
-      const bool hi_bin = (float)dM_d <= hi_m_C;
-      const float dhi = hi_bin ? (float)dM_d : hi_m_C;
-      // width S_hi - S_lo, exact to rounding when both bounds are bin bounds
-      const float width = lo_bin && hi_bin ? (float)S.dt : (float)((hi_bin ? dM_d : (double)hi_m_C) - (lo_bin ? dm_d : (double)dlo));
-      if (DBG) { dbg->S_lo = C + dlo; dbg->S_hi = C + dhi; }
-      if (width > 0.0f) {
+      const SRange rg = conn_range(S, ps.x, wc, xe, C, q, clo, chi, ps.resM);
+      if (DBG) { dbg->S_lo = C + rg.dlo; dbg->S_hi = C + rg.dhi; }
+      if (rg.width > 0.0f && defer) {
+        conn_nonempty = true;
+        want_job = true;
+        job_dlo = rg.dlo;
+        job_width = rg.width;
+      } else if (rg.width > 0.0f) {
         ok = true;
-        // truncated exponential on [S_lo, S_hi); e^{-st (S-S_lo)} = 1 - u7 span
-        const float span = one_m_exp(S.sigma_t * width);
-        const float keep = fmaf(u7, fexp(-S.sigma_t * width), 1.0f - u7);  // 1 - u7 span
-        const float L = neg_log1m2(u7 * span, keep) * S.inv_sigma_t;
-        const float pS = S.sigma_t * keep * __fdividef(1.0f, span);
-        const float dSC = dlo + L;  // S - C
-        const float Ssm = C + dSC;
-        // S - q = (S - C) + (C - q), C - q = perp^2 / (C + q) for q > 0
-        const f3 pv = cv - wc * q;
-        const float perp2 = dot(pv, pv);
-        const float Cmq = q > 0.0f ? perp2 * __fdividef(1.0f, C + q) : C - q;
-        const float Smq = dSC + Cmq;
-        const float inv2Smq = __fdividef(0.5f, Smq);
-        Ssamp = Ssm;
-        t = dSC * (Ssm + C) * inv2Smq;                 // E21: (S^2 - C^2) / (2 (S - q))
-        pSt = (Smq * Smq + perp2) * inv2Smq;           // S - t
-        pt = pS * Smq * __fdividef(1.0f, pSt);         // E22 with the Jacobian of R2
+        const EllSample es = ell_sample(S, cv, C, q, wc, rg.dlo, rg.width, u7);
+        Ssamp = es.S;
+        t = es.t;
+        pSt = es.pSt;
+        pt = es.pt;
       }
     } else {
       // R17: unwarped camera vertex, shell |x(t) - xe| in [Rm, RM): <= 2 t-intervals
@@ -533,19 +635,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     }
     if (ok) {
       conn_nonempty = true;
-      const f3 xell = fma3(wc, t, ps.x);
-      const f3 de = xe - xell;
-      float r2sq = dot(de, de);
-      float r2 = sqrtf(r2sq);
-      const f3 we = de * __fdividef(1.0f, r2);
-      if (pSt > 0.0f) {  // on the ellipse r2 = S - t, formed without cancellation
-        r2 = pSt;
-        r2sq = pSt * pSt;
-      }
-      const float rho = hg_eval(S, dot(wc, we));
-      const float tr = fexp(-S.sigma_t * (t - clo)) * segment_tr(S, xell, xe, r2, we);
-      float c = ps.beta * wconn * S.sigma_s * tr * rho * ek * __fdividef(1.0f, r2sq * pt);
-      if (S.r_excl > 0.0f && r2 < S.r_excl) c = 0.0f;
+      f3 xell;
+      float r2;
+      const float c = conn_contrib<SH, WALLS>(S, ps.x, wc, xe, ek, t, pt, pSt, clo, ps.beta * wconn, &xell, &r2);
       contrib += c;
       if (DBG) {
         dbg->S = (S.warped == 0 && ps.kind == KIND_CAMERA) ? t + r2 : Ssamp;
@@ -554,6 +646,31 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
         dbg->p_t = pt;
         dbg->contrib = c;
         dbg->conn_valid = 1;
+      }
+    }
+  }
+  if (!DBG && df) {
+    // queue the job in a free slot; a lane that finds the queue full runs its
+    // connection now (the same arithmetic)
+    const unsigned jm = __ballot_sync(df->act, want_job);
+    const uint32_t slot = df->qn + __popc(jm & df->lane_lt);
+    *pushed = false;
+    if (want_job) {
+      const float coef = ps.beta * wconn;
+      const uint32_t m7e = (r[7] >> 9) | ((uint32_t)ps.e << 23);
+      if (slot < (uint32_t)kQueue) {
+        float* qq = df->q + slot;
+        const uint32_t st = df->qstride;
+        qq[0 * st] = ps.x.x; qq[1 * st] = ps.x.y; qq[2 * st] = ps.x.z;
+        qq[3 * st] = wc.x; qq[4 * st] = wc.y; qq[5 * st] = wc.z;
+        qq[6 * st] = job_dlo;
+        qq[7 * st] = job_width;
+        qq[8 * st] = coef * df->inv_n;
+        qq[9 * st] = __uint_as_float(m7e);
+        qq[10 * st] = __uint_as_float(df->cell);
+        *pushed = true;
+      } else {
+        contrib += conn_job_run<SH, WALLS>(S, ps.x, wc, job_dlo, job_width, coef, m7e);
       }
     }
   }
@@ -595,7 +712,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const float Delta = resM - counts * di;  // R4
       const float dq = di - qd;
       const float r2i = fmaf(dq, dq, perp2);
-      const bool valid = (Delta > 0.0f) && (r2i <= Delta * Delta);
+      // Delta > 0 and r <= Delta in one test (Delta |Delta| < 0 when Delta < 0;
+      // the boundary cases r = Delta, Delta = 0 have measure zero)
+      const bool valid = r2i < Delta * fabsf(Delta);
       const float s = rsqrtf(fmaxf(Delta, 1e-20f));  // s^3 stays finite for invalid candidates
       // log2 of Phi' = Delta^{-3/2} exp(-r^2/(4 D Delta) - sigma_a Delta) (E9, constants dropped)
       const float ex = fmaf(S.neg_inv4D_log2e * r2i, s * s, S.neg_sa_log2e * Delta);
@@ -644,7 +763,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     ps.w = ww;
     if (DBG) { dbg->event = 1; dbg->istar = (int)is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
   } else {
-    if (hit == HIT_WALL) {
+    if (WALLS && hit == HIT_WALL) {
       f3 xn = fma3(ww, hi, ps.x);
       const int a = face >> 1;
       const float pl = (face & 1) ? S.bmax[a] : S.bmin[a];
@@ -679,6 +798,16 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     return false;
   }
   return true;
+}
+
+// Runs queued connection job (fields at q[f * st]).  Returns the contribution
+// already scaled by 1 / n_cell, and its cell.
+template <int SH, bool WALLS>
+__device__ __forceinline__ float conn_job_eval(const DevScene& S, const float* q, uint32_t st, uint32_t& cell) {
+  const f3 x = mk(q[0 * st], q[1 * st], q[2 * st]);
+  const f3 wc = mk(q[3 * st], q[4 * st], q[5 * st]);
+  cell = __float_as_uint(q[10 * st]);
+  return conn_job_run<SH, WALLS>(S, x, wc, q[6 * st], q[7 * st], q[8 * st], __float_as_uint(q[9 * st]));
 }
 
 }  // namespace dts

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_
 }
 
 // ============================================================== debug kernel
-template <bool DUMMY>
+template <int SH, bool WALLS, bool SPLIT>
 __global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n, const dts_debug_in* __restrict__ in,
                              dts_debug_out* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -155,7 +155,7 @@ __global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n
   float c;
   bool cn, wn;
   int reason;
-  darts_vertex<true, false>(S, tab, ps, r, c, &o, cn, wn, reason);
+  darts_vertex<true, false, SH, WALLS, SPLIT>(S, tab, ps, r, c, &o, cn, wn, reason);
   o.E_next = RM - ps.resM;
   out[i] = o;
 }
@@ -177,6 +177,9 @@ struct RenderParams {
   uint32_t table_u4; // table size in 16-byte words
   uint32_t spp_div_b, spp_mod_b;  // SPP_PER_PIXEL cell counts (R21)
   uint32_t priv_cells;            // > 0: the CTA privatises the whole histogram in shared memory
+  uint32_t defer;                 // 1: connections are queued per warp and evaluated in batches
+  uint32_t flush_at;              // queue length that triggers a batch
+  uint32_t refill_k;              // idle lane-iterations that trigger a refill
 };
 
 #ifndef DTS_BLOCK
@@ -196,6 +199,7 @@ struct PathCtx {
 };
 
 // decode a work index into a path (returns false if the path retires at start)
+template <int SH, bool WALLS>
 __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx, PathCtx& pc, uint32_t& ctr_miss,
                                            uint32_t& ctr_early) {
   const DevScene& S = P.S;
@@ -237,7 +241,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     id = (s * Npix + p) * (uint64_t)B + b;
   } else {
     // R21: bin = (s + o_p) mod B with a per-pixel Philox offset
-    const u4 o = philox((uint32_t)p, (uint32_t)(p >> 32), 0xFFFFFFFEu, 0u, S.seed_lo, S.seed_hi);
+    const u4 o = philox_rk((uint32_t)p, (uint32_t)(p >> 32), 0xFFFFFFFEu, 0u, S.rk);
     const uint32_t op = min((uint32_t)((float)B * unif(o.a)), B - 1u);
     b = (uint32_t)((s + op) % B);
     const uint32_t rel = (b + B - op) % B;
@@ -251,7 +255,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   pc.cell = pl * B + b;
   pc.inv_n = inv_n;
   pc.acc = 0.0f;
-  const u4 a = philox(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 0u, S.seed_lo, S.seed_hi);
+  const u4 a = philox_rk(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 0u, S.rk);
   int e = min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1);
   PathState& ps = pc.ps;
   ps.e = e;
@@ -264,8 +268,8 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     ps.x = ld3(S.cam_pos);
     ps.beta = 1.0f;
   } else {
-    const u4 bb = philox(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 1u, S.seed_lo, S.seed_hi);
-    const u4 cc = philox(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 2u, S.seed_lo, S.seed_hi);
+    const u4 bb = philox_rk(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 1u, S.rk);
+    const u4 cc = philox_rk(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 2u, S.rk);
     const float rad = S.det_radius * cbrtf(unif(bb.a));
     const float z = 1.0f - 2.0f * unif(bb.b);
     const float sz = sqrtf(fmaxf(0.0f, 1.0f - z * z));
@@ -283,7 +287,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   ps.resM = S.t0 + (double)(b + 1) * S.dt - (double)S.em_t[e];  // R_M - E with E = 0
   float lo, hi;
   int f;
-  if (intersect(S, ps.x, ps.w, lo, hi, f) == HIT_MISS) {
+  if (intersect<SH, WALLS>(S, ps.x, ps.w, lo, hi, f) == HIT_MISS) {
     ++ctr_miss;
     return false;
   }
@@ -368,15 +372,16 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
 #ifndef DTS_TABLE_SMEM
 #define DTS_TABLE_SMEM 1
 #endif
-template <bool SMEM>
+template <bool SMEM, int SH, bool WALLS, bool SPLIT>
 __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const RenderParams P) {
   extern __shared__ __align__(16) uint16_t s_dyn[];
   __shared__ uint64_t s_bar;
   const DevScene& S = P.S;
   const uint16_t* tab = P.tab;
-  // dynamic shared memory: [EDA table (SMEM)] [private histogram] [private hist_sq]
+  // dynamic shared memory: [EDA table (SMEM)] [private histogram] [private hist_sq] [job queues]
   float* s_hist = nullptr;
   float* s_sq = nullptr;
+  float* s_queue = nullptr;
   {
     char* base = reinterpret_cast<char*>(s_dyn) + (SMEM ? (size_t)P.table_u4 * 16 : 0);
     if (P.priv_cells) {
@@ -384,7 +389,9 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       if (P.hist_sq) s_sq = s_hist + P.priv_cells;
       const uint32_t n = P.priv_cells * (P.hist_sq ? 2u : 1u);
       for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s_hist[i] = 0.0f;
+      base += (size_t)n * sizeof(float);
     }
+    if (P.defer) s_queue = reinterpret_cast<float*>(base);
   }
   if (SMEM) {
     bulk_stage(s_dyn, P.tab, P.table_u4 * 16u, &s_bar);
@@ -394,25 +401,56 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
-  // warp-uniform work queue [qn, qe)
-  uint64_t qn = 0, qe = 0;
+  // this warp's connection-job queue: field f of slot j at q[f * qstride + j]
+  const uint32_t qstride = (uint32_t)kQueue * (kBlock / 32);
+  Defer df;
+  df.q = s_queue ? s_queue + (threadIdx.x >> 5) * kQueue : nullptr;
+  df.qstride = qstride;
+  df.qn = 0;
+  df.lane_lt = lt_mask;
+  // warp-uniform work queue [wn, we)
+  uint64_t wn = 0, we = 0;
   bool exhausted = false;
   bool active = false;
   PathCtx pc;
-  // per-warp counters (identical in every lane)
-  uint32_t c_paths = 0, c_miss = 0, c_vert = 0, c_conn = 0, c_ris = 0, c_early = 0, c_esc = 0, c_cap = 0, c_nf = 0,
-           c_nee = 0;
-  uint32_t l_miss = 0, l_early = 0;  // per-lane start-time retirements
+  // per-lane event counters, summed over the warp at the end
+  uint32_t c_paths = 0, c_vert = 0, c_conn = 0, c_ris = 0, c_early = 0, c_esc = 0, c_cap = 0, c_nf = 0, c_nee = 0;
+  uint32_t l_miss = 0, l_early = 0;  // start-time retirements
+  uint32_t waste = 0;                // idle lane-iterations since the last refill
+  // evaluates the queued jobs, one per lane, and splats them (cells differ per job)
+  auto flush = [&]() {
+    float c = 0.0f;
+    uint32_t cell = 0;
+    if ((uint32_t)lane < df.qn) {
+      c = conn_job_eval<SH, WALLS>(S, df.q + lane, qstride, cell);
+      if (!isfinite(c)) {
+        ++c_nf;
+        c = 0.0f;
+      }
+    }
+    const bool has = c != 0.0f;
+    const unsigned m = __ballot_sync(FULL, has);
+    if (m) splat(m, has, cell, c, 0.0f, P.hist, nullptr, s_hist, nullptr, lane);
+    df.qn = 0;
+    __syncwarp();
+  };
   while (true) {
+    // Lanes retire one at a time, and a path start (+ its camera vertex) runs
+    // at a few active lanes.  Refill when the idle lane-iterations accumulated
+    // since the last refill reach refill_k (ski rental: an idle lane costs
+    // ~1/32 of an iteration, a start ~refill_k of those), so long-walk scenes
+    // start paths in small batches and short-walk scenes in large ones.
     const unsigned idle = __ballot_sync(FULL, !active);
-    if (idle && !exhausted) {
+    waste += __popc(idle);
+    if (idle && !exhausted && (waste >= P.refill_k || idle == FULL)) {
+      waste = 0;
       const uint32_t nidle = __popc(idle);
       const uint32_t rank = __popc(idle & lt_mask);
-      const uint64_t avail = qe - qn;
+      const uint64_t avail = we - wn;
       uint64_t my = ~0ull;
       if (avail >= nidle) {
-        my = qn + rank;
-        qn += nidle;
+        my = wn + rank;
+        wn += nidle;
       } else {
         unsigned long long nb = 0;
         if (lane == 0) nb = atomicAdd(P.work, (unsigned long long)kChunk);
@@ -423,18 +461,18 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
           ne = nb;
         }
         if (rank < avail) {
-          my = qn + rank;
+          my = wn + rank;
         } else {
           const uint64_t cand = nb + (rank - avail);
           my = cand < ne ? cand : ~0ull;
         }
         const uint64_t nq = nb + (nidle - avail);
-        qn = nq < ne ? nq : ne;
-        qe = ne;
+        wn = nq < ne ? nq : ne;
+        we = ne;
       }
       if (!active && my != ~0ull && my < P.total) {
-        active = start_path(P, my, pc, l_miss, l_early);
-        ++c_paths;  // counted per lane below via ballot
+        active = start_path<SH, WALLS>(P, my, pc, l_miss, l_early);
+        ++c_paths;
       }
     }
     const unsigned act = __ballot_sync(FULL, active);
@@ -442,33 +480,39 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       if (exhausted) break;
       continue;
     }
+    if (s_queue && df.qn >= P.flush_at) flush();
     bool done = false;
-    bool cn = false, wn = false, cap = false;
-    int reason = 0;
+    bool pushed = false;
     if (active) {
+      bool cn = false, wnee = false, cap = false;
+      int reason = 0;
       uint32_t r[8];
-      const u4 a = philox(pc.id_lo, pc.id_hi, pc.k, 0u, S.seed_lo, S.seed_hi);
-      const u4 b = philox(pc.id_lo, pc.id_hi, pc.k, 1u, S.seed_lo, S.seed_hi);
+      const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
+      const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
       r[0] = a.a; r[1] = a.b; r[2] = a.c; r[3] = a.d;
       r[4] = b.a; r[5] = b.b; r[6] = b.c; r[7] = b.d;
       float contrib;
-      const bool alive = darts_vertex<false, SMEM>(S, tab, pc.ps, r, contrib, nullptr, cn, wn, reason);
+      df.act = act;
+      df.cell = pc.cell;
+      df.inv_n = pc.inv_n;
+      const bool alive = darts_vertex<false, SMEM, SH, WALLS, SPLIT>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee,
+                                                                     reason, s_queue ? &df : nullptr, &pushed);
       pc.acc += contrib;
       ++pc.k;
       cap = alive && pc.k >= (uint32_t)S.max_bounces;
       done = !alive || cap;
+      ++c_vert;
+      c_conn += cn ? 1u : 0u;
+      if (WALLS) c_nee += wnee ? 1u : 0u;
+      if (done) {
+        c_ris += reason == DTS_CTR_RIS_INVALID ? 1u : 0u;
+        c_early += reason == DTS_CTR_EARLY_EXIT ? 1u : 0u;
+        c_esc += reason == DTS_CTR_ESCAPES ? 1u : 0u;
+        c_nf += reason == DTS_CTR_NONFINITE ? 1u : 0u;
+        c_cap += cap ? 1u : 0u;
+      }
     }
-    // event counters: every lane takes part in the ballots (warp-uniform sums)
-    c_conn += __popc(__ballot_sync(FULL, cn));
-    c_nee += __popc(__ballot_sync(FULL, wn));
-    if (__ballot_sync(FULL, done)) {
-      c_ris += __popc(__ballot_sync(FULL, reason == DTS_CTR_RIS_INVALID));
-      c_early += __popc(__ballot_sync(FULL, reason == DTS_CTR_EARLY_EXIT));
-      c_esc += __popc(__ballot_sync(FULL, reason == DTS_CTR_ESCAPES));
-      c_nf += __popc(__ballot_sync(FULL, reason == DTS_CTR_NONFINITE));
-      c_cap += __popc(__ballot_sync(FULL, cap));
-    }
-    c_vert += __popc(act);
+    if (s_queue) df.qn += __popc(__ballot_sync(FULL, pushed));
     const unsigned dmask = __ballot_sync(FULL, done);
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
@@ -476,6 +520,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       if (done) active = false;
     }
   }
+  if (s_queue && df.qn) flush();
   if (P.priv_cells) {  // flush the CTA's private histogram (coalesced REDs of its non-zero cells)
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < P.priv_cells; i += blockDim.x) {
@@ -483,16 +528,22 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       if (s_sq && s_sq[i] != 0.0f) atomicAdd(P.hist_sq + i, s_sq[i]);
     }
   }
-  // c_paths was counted per lane; reduce across the warp
-  uint32_t lp = c_paths;
   for (int o = 16; o > 0; o >>= 1) {
-    lp += __shfl_xor_sync(FULL, lp, o);
+    c_paths += __shfl_xor_sync(FULL, c_paths, o);
     l_miss += __shfl_xor_sync(FULL, l_miss, o);
     l_early += __shfl_xor_sync(FULL, l_early, o);
+    c_vert += __shfl_xor_sync(FULL, c_vert, o);
+    c_conn += __shfl_xor_sync(FULL, c_conn, o);
+    c_ris += __shfl_xor_sync(FULL, c_ris, o);
+    c_early += __shfl_xor_sync(FULL, c_early, o);
+    c_esc += __shfl_xor_sync(FULL, c_esc, o);
+    c_cap += __shfl_xor_sync(FULL, c_cap, o);
+    c_nf += __shfl_xor_sync(FULL, c_nf, o);
+    c_nee += __shfl_xor_sync(FULL, c_nee, o);
   }
   if (lane == 0 && P.counters) {
     unsigned long long* C = P.counters;
-    atomicAdd(C + DTS_CTR_PATHS, (unsigned long long)lp);
+    atomicAdd(C + DTS_CTR_PATHS, (unsigned long long)c_paths);
     atomicAdd(C + DTS_CTR_CAMERA_MISS, (unsigned long long)l_miss);
     atomicAdd(C + DTS_CTR_VERTICES, (unsigned long long)c_vert);
     atomicAdd(C + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
@@ -514,6 +565,7 @@ __device__ __forceinline__ void vanilla_splat(const RenderParams& P, uint32_t pl
   atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, c / (float)P.spp);
 }
 
+template <int SH, bool WALLS>
 __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderParams P) {
   const DevScene& S = P.S;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -526,7 +578,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     const uint64_t id = s * ((uint64_t)S.width * (uint64_t)S.height) + p;
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
     ++c_paths;
-    const u4 a = philox(id_lo, id_hi, 0xFFFFFFFFu, 0u, S.seed_lo, S.seed_hi);
+    const u4 a = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 0u, S.rk);
     const int e = min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1);
     const f3 xe = ld3(S.em_pos[e]);
     const double te = (double)S.em_t[e];
@@ -542,8 +594,8 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
       x = ld3(S.cam_pos);
       beta = 1.0f;
     } else {
-      const u4 bb = philox(id_lo, id_hi, 0xFFFFFFFFu, 1u, S.seed_lo, S.seed_hi);
-      const u4 cc = philox(id_lo, id_hi, 0xFFFFFFFFu, 2u, S.seed_lo, S.seed_hi);
+      const u4 bb = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 1u, S.rk);
+      const u4 cc = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 2u, S.rk);
       const float rad = S.det_radius * cbrtf(unif(bb.a));
       const float z = 1.0f - 2.0f * unif(bb.b);
       const float sz = sqrtf(fmaxf(0.0f, 1.0f - z * z));
@@ -559,7 +611,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     {
       float lo, hi;
       int f;
-      if (intersect(S, x, w, lo, hi, f) == HIT_MISS) {
+      if (intersect<SH, WALLS>(S, x, w, lo, hi, f) == HIT_MISS) {
         ++c_miss;
         continue;
       }
@@ -569,7 +621,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     bool alive = true;
     int k;
     for (k = 0; k < S.max_bounces && alive; ++k) {
-      const u4 r = philox(id_lo, id_hi, (uint32_t)k, 0u, S.seed_lo, S.seed_hi);
+      const u4 r = philox_rk(id_lo, id_hi, (uint32_t)k, 0u, S.rk);
       ++c_vert;
       if (kind == KIND_MEDIUM) {
         float opc, omc;
@@ -592,7 +644,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
       }
       float lo, hi;
       int hf;
-      const int hit = intersect(S, x, w, lo, hi, hf);
+      const int hit = intersect<SH, WALLS>(S, x, w, lo, hi, hf);
       if (hit == HIT_MISS) { ++c_esc; alive = false; break; }
       const float counts = (S.warped || kind != KIND_CAMERA) ? 1.0f : 0.0f;
       const f3 d0 = x - xe;
@@ -603,7 +655,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
         E += (double)(counts * d);
         beta *= S.albedo;
         kind = KIND_MEDIUM;
-      } else if (hit == HIT_WALL) {
+      } else if (WALLS && hit == HIT_WALL) {
         d = hi;
         f3 xn = fma3(w, hi, x);
         const int ax = hf >> 1;
@@ -626,7 +678,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
       } else {
         c = beta * (S.wall_albedo[face] * (1.0f / kPi)) * fmaxf(0.0f, dot(inward_normal(face), we));
       }
-      c *= segment_tr(S, x, xe, C, we) * ek / (C * C);
+      c *= segment_tr<SH, WALLS>(S, x, xe, C, we) * ek / (C * C);
       if (S.r_excl > 0.0f && C < S.r_excl) c = 0.0f;
       vanilla_splat(P, pl, arrive, c);
     }
@@ -648,6 +700,69 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     atomicAdd(P.counters + DTS_CTR_EARLY_EXIT, (unsigned long long)c_early);
     atomicAdd(P.counters + DTS_CTR_ESCAPES, (unsigned long long)c_esc);
     atomicAdd(P.counters + DTS_CTR_CAP_HITS, (unsigned long long)c_cap);
+  }
+}
+
+// ============================================================== kernel selection
+// Render and debug kernels are specialised at compile time on the medium
+// shape, the presence of walls and the direction mode (R29), so no launch
+// carries the branches or registers of the other scene kinds.
+template <bool SMEM>
+static const void* darts_kernel_ptr_t(int shape, bool walls, bool split) {
+  if (shape == DTS_MEDIUM_INFINITE)
+    return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_INFINITE, false, true>
+                 : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_INFINITE, false, false>;
+  if (shape == DTS_MEDIUM_SPHERE)
+    return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, false, true>
+                 : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, false, false>;
+  if (shape == DTS_MEDIUM_BOX) {
+    if (walls)
+      return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, true, true>
+                   : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, true, false>;
+    return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, false, true>
+                 : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, false, false>;
+  }
+  return nullptr;
+}
+static const void* darts_kernel_ptr(bool smem, int shape, bool walls, bool split) {
+  return smem ? darts_kernel_ptr_t<true>(shape, walls, split) : darts_kernel_ptr_t<false>(shape, walls, split);
+}
+static const void* vanilla_kernel_ptr(int shape, bool walls) {
+  if (shape == DTS_MEDIUM_INFINITE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_INFINITE, false>;
+  if (shape == DTS_MEDIUM_SPHERE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_SPHERE, false>;
+  if (shape == DTS_MEDIUM_BOX)
+    return walls ? (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, true>
+                 : (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, false>;
+  return nullptr;
+}
+static const void* debug_kernel_ptr(int shape, bool walls, bool split) {
+  if (shape == DTS_MEDIUM_INFINITE)
+    return split ? (const void*)debug_kernel<DTS_MEDIUM_INFINITE, false, true>
+                 : (const void*)debug_kernel<DTS_MEDIUM_INFINITE, false, false>;
+  if (shape == DTS_MEDIUM_SPHERE)
+    return split ? (const void*)debug_kernel<DTS_MEDIUM_SPHERE, false, true>
+                 : (const void*)debug_kernel<DTS_MEDIUM_SPHERE, false, false>;
+  if (shape == DTS_MEDIUM_BOX) {
+    if (walls)
+      return split ? (const void*)debug_kernel<DTS_MEDIUM_BOX, true, true>
+                   : (const void*)debug_kernel<DTS_MEDIUM_BOX, true, false>;
+    return split ? (const void*)debug_kernel<DTS_MEDIUM_BOX, false, true>
+                 : (const void*)debug_kernel<DTS_MEDIUM_BOX, false, false>;
+  }
+  return nullptr;
+}
+
+// Philox4x32-10 key schedule of a seed (R24): round r uses
+// (k0 + r 0x9E3779B9, k1 + r 0xBB67AE85) mod 2^32.
+static void set_round_keys(DevScene& S, uint64_t seed) {
+  S.seed_lo = (uint32_t)seed;
+  S.seed_hi = (uint32_t)(seed >> 32);
+  uint32_t k0 = S.seed_lo, k1 = S.seed_hi;
+  for (int r = 0; r < 10; ++r) {
+    S.rk[2 * r] = k0;
+    S.rk[2 * r + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
   }
 }
 
@@ -894,8 +1009,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   RenderParams P;
   memset(&P, 0, sizeof P);
   P.S = s->S;
-  P.S.seed_lo = (uint32_t)seed;
-  P.S.seed_hi = (uint32_t)(seed >> 32);
+  set_round_keys(P.S, seed);
   P.tab = s->d_table;
   P.hist = d_hist;
   P.hist_sq = d_hist_sq;
@@ -917,26 +1031,33 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     // privatise small histograms (config 1: 128 cells) in shared memory
     const size_t cells = dts_hist_cells(s);
     const size_t pbytes = cells * sizeof(float) * (d_hist_sq ? 2 : 1);
-    const size_t kSmemCap = 227 * 1024 - 64;
+    const size_t kSmemCap = 227 * 1024 - 64;  // opt-in per-block maximum less the static mbarrier
     if (cells <= kPrivMaxCells && (smem ? tbytes : 0) + pbytes <= kSmemCap) P.priv_cells = (uint32_t)cells;
-    const size_t dyn = (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0);
+    // per-warp connection-job queues (not with hist_sq: its per-path squares need whole-path sums)
+    const size_t qbytes = (size_t)kJobWords * kQueue * (kBlock / 32) * sizeof(float);
+    const char* nd = getenv("DTS_NO_DEFER");
+    const bool defer = !d_hist_sq && !(nd && nd[0] == '1') &&
+                       (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + qbytes <= kSmemCap;
+    P.defer = defer ? 1u : 0u;
+    const char* rk = getenv("DTS_REFILL_K");
+    P.refill_k = rk ? (uint32_t)atoi(rk) : 16u;
+    if (P.refill_k < 1 || P.refill_k > 4096) P.refill_k = 16u;
+    const char* fa = getenv("DTS_FLUSH_AT");
+    P.flush_at = fa ? (uint32_t)atoi(fa) : 28u;
+    if (P.flush_at < 1 || P.flush_at > (uint32_t)kQueue) P.flush_at = 28u;
+    const size_t dyn = (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + (defer ? qbytes : 0);
+    const void* kfn = darts_kernel_ptr(smem, d.medium_shape, d.wall_mask != 0u, d.direction_mode == DTS_DIR_SPLIT);
+    if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
     int blocks_per_sm = 1;
-    if (smem) {
-      CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<true>, kBlock, dyn));
-    } else {
-      CUDA_TRY(cudaFuncSetAttribute(render_darts_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, render_darts_kernel<false>, kBlock, dyn));
-    }
+    CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, kBlock, dyn));
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     uint64_t grid = (uint64_t)s->num_sms * blocks_per_sm;
     const uint64_t need = (P.total + 31) / 32 / (kBlock / 32) + 1;
     if (grid > need) grid = need;
     CUDA_TRY(cudaMemsetAsync(s->d_work, 0, sizeof(unsigned long long), st));
-    if (smem)
-      render_darts_kernel<true><<<(unsigned)grid, kBlock, dyn, st>>>(P);
-    else
-      render_darts_kernel<false><<<(unsigned)grid, kBlock, dyn, st>>>(P);
+    void* args[] = {&P};
+    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(kBlock), args, dyn, st));
     CUDA_TRY(cudaGetLastError());
     g_last_launches = 1;
     g_last_grid = (int)grid;
@@ -945,11 +1066,14 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   } else {
     P.total = npix * ns;
     int bps = 1;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, render_vanilla_kernel, kBlock, 0));
+    const void* kfn = vanilla_kernel_ptr(d.medium_shape, d.wall_mask != 0u);
+    if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, kBlock, 0));
     uint64_t grid = (uint64_t)s->num_sms * (bps < 1 ? 1 : bps) * 4;
     const uint64_t need = (P.total + kBlock - 1) / kBlock;
     if (grid > need) grid = need;
-    render_vanilla_kernel<<<(unsigned)grid, kBlock, 0, st>>>(P);
+    void* args[] = {&P};
+    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(kBlock), args, 0, st));
     CUDA_TRY(cudaGetLastError());
     g_last_launches = 1;
     g_last_grid = (int)grid;
@@ -995,7 +1119,12 @@ dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, 
     CUDA_TRY(cudaMemsetAsync(d_dummy, 0, 256 * sizeof(uint16_t), (cudaStream_t)stream));
     tab = d_dummy;
   }
-  debug_kernel<true><<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(s->S, tab, n, d_in, d_out);
+  const void* kfn = debug_kernel_ptr(s->desc.medium_shape, s->desc.wall_mask != 0u, s->desc.direction_mode == DTS_DIR_SPLIT);
+  if (!kfn) return fail(DTS_E_INVALID_ARG, "no debug kernel for this scene shape");
+  DevScene S = s->S;
+  set_round_keys(S, 0);
+  void* args[] = {&S, &tab, &n, &d_in, &d_out};
+  CUDA_TRY(cudaLaunchKernel(kfn, dim3((n + 127) / 128), dim3(128), args, 0, (cudaStream_t)stream));
   CUDA_TRY(cudaGetLastError());
   return DTS_OK;
 }
