@@ -21,6 +21,8 @@ constexpr float kLn2 = 0.693147180559945309f;
 
 enum { HIT_NONE = 0, HIT_OPEN = 1, HIT_WALL = 2, HIT_MISS = 3 };
 enum { KIND_CAMERA = 0, KIND_MEDIUM = 1, KIND_WALL = 2 };
+// compile-time scene variant flags of the render / debug kernels
+enum { FL_WALLS = 1, FL_SPLIT = 2, FL_MULTI_E = 4 };
 
 // Launch-uniform scene constants, passed by value as a kernel parameter (lives
 // in the constant bank: every lane reads the same address).
@@ -50,12 +52,14 @@ struct DevScene {
   float det_radius;
   int32_t crop[4];
   double t0, dt;
+  float dt_f;  // (float) dt
   int32_t n_bins, warped;
   int32_t strategy, direction_mode, spp_mode, max_bounces;
   float alpha;
   float r_excl, s_excess;
   // EDA table (R8-R10)
   int32_t nr, ns;
+  float nr_f, ns_f;
   uint32_t table_n;        // CDF entries; an 8-bit guide table of the same length follows them
   float ln_smin, inv_dls;  // ns / (ln smax - ln smin)
   uint32_t seed_lo, seed_hi;
@@ -73,6 +77,18 @@ __device__ __forceinline__ f3 operator*(f3 a, float s) { return mk(a.x * s, a.y 
 __device__ __forceinline__ float dot(f3 a, f3 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z)); }
 __device__ __forceinline__ f3 fma3(f3 d, float t, f3 o) { return mk(fmaf(d.x, t, o.x), fmaf(d.y, t, o.y), fmaf(d.z, t, o.z)); }
 __device__ __forceinline__ f3 ld3(const float* p) { return mk(p[0], p[1], p[2]); }
+// double <-> float conversions as single F2F instructions (a C cast under
+// --ftz adds a denormal test and a rescale; the values here are never denormal)
+__device__ __forceinline__ float d2f(double x) {
+  float r;
+  asm("cvt.rn.f32.f64 %0, %1;" : "=f"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double f2d(float x) {
+  double r;
+  asm("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(x));
+  return r;
+}
 
 // ----------------------------------------------------------------- RNG (R24)
 // Philox4x32-10 (Salmon et al. 2011); counter = (id_lo, id_hi, bounce, block).
@@ -341,17 +357,17 @@ __device__ __forceinline__ SRange conn_range(const DevScene& S, f3 x, f3 wc, f3 
     const f3 phi_ = fma3(wc, chi, x) - xe;
     hi_m_C = chi + chi * (chi - 2.0f * q) * __fdividef(1.0f, sqrtf(dot(phi_, phi_)) + C);
   }
-  const double dM_d = resM - (double)C;
+  const double dM_d = resM - f2d(C);
   const double dm_d = dM_d - S.dt;
   SRange r;
-  r.dlo = (float)dm_d;
+  r.dlo = d2f(dm_d);
   bool lo_bin = true;
   if (lo_m_C > r.dlo) { r.dlo = lo_m_C; lo_bin = false; }
   if (S.s_excess > 0.0f && S.s_excess > r.dlo) { r.dlo = S.s_excess; lo_bin = false; }
-  const bool hi_bin = (float)dM_d <= hi_m_C;
-  r.dhi = hi_bin ? (float)dM_d : hi_m_C;
-  r.width = lo_bin && hi_bin ? (float)S.dt
-                             : (float)((hi_bin ? dM_d : (double)hi_m_C) - (lo_bin ? dm_d : (double)r.dlo));
+  const float dM_f = d2f(dM_d);
+  const bool hi_bin = dM_f <= hi_m_C;
+  r.dhi = hi_bin ? dM_f : hi_m_C;
+  r.width = lo_bin && hi_bin ? S.dt_f : d2f((hi_bin ? dM_d : f2d(hi_m_C)) - (lo_bin ? dm_d : f2d(r.dlo)));
   return r;
 }
 
@@ -383,10 +399,11 @@ __device__ __forceinline__ float conn_contrib(const DevScene& S, f3 x, f3 wc, f3
 // Runs a queued connection from an inside vertex (clo = 0) whose S range
 // [C + dlo, C + dlo + width) is known and non-empty: S sample (E21-E22) and
 // contribution (coef included).  m7e = u7's 23 bits | emitter << 23.
-template <int SH, bool WALLS>
+template <int SH, int FL>
 __device__ __forceinline__ float conn_job_run(const DevScene& S, f3 x, f3 wc, float dlo, float width, float coef,
                                               uint32_t m7e) {
-  const int e = (int)(m7e >> 23);
+  constexpr bool WALLS = (FL & FL_WALLS) != 0;
+  const int e = (FL & FL_MULTI_E) ? (int)(m7e >> 23) : 0;
   const f3 xe = ld3(S.em_pos[e]);
   const f3 cv = xe - x;
   const float C = sqrtf(dot(cv, cv));
@@ -415,7 +432,7 @@ struct Defer {
 // ----------------------------------------------------------------- one DARTS vertex
 // Returns true if the walk continues.  contrib receives the vertex's
 // connection (+ wall NEE) contribution; end_reason the DTS_CTR_* of a stop.
-template <bool DBG, bool SMEM, int SH, bool WALLS, bool SPLIT>
+template <bool DBG, bool SMEM, int SH, int FL>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason,
@@ -424,11 +441,13 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   conn_nonempty = false;
   wall_nee = false;
   end_reason = 0;
-  const f3 xe = ld3(S.em_pos[ps.e]);
-  const float ek = S.em_k[ps.e];
+  constexpr bool WALLS = (FL & FL_WALLS) != 0, SPLIT = (FL & FL_SPLIT) != 0;
+  const int e = (FL & FL_MULTI_E) ? ps.e : 0;  // one emitter: constant-bank operands
+  const f3 xe = ld3(S.em_pos[e]);
+  const float ek = S.em_k[e];
   f3 wc, ww;
   float wconn = 1.0f;
-  const float resM = (float)ps.resM;
+  const float resM = d2f(ps.resM);
 
   // ---- step 2: direction ----
   if (ps.kind == KIND_CAMERA) {
@@ -444,7 +463,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float C = sqrtf(dot(cv, cv));
     const f3 we = cv * __fdividef(1.0f, C);
     const float cw = dot(n, we);
-    const float resm = (float)(ps.resM - S.dt);
+    const float resm = d2f(ps.resM - S.dt);
     float nee = 0.0f;
     if (cw > 0.0f && resm - C <= 0.0f && resM - C > 0.0f) {  // E + C in [Rm, RM)
       // R14: time-checked direct NEE at a wall vertex
@@ -469,9 +488,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float C = sqrtf(dot(cv, cv));
     const float ratio = __fdividef(C, resM);
     const float ls = (__logf(resM) - S.ln_smin) * S.inv_dls;
-    const bool valid = (resM > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < (float)S.ns);
+    const bool valid = (resM > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < S.ns_f);
     const float gamma = valid ? __fdividef(ratio, ratio + S.alpha) : 0.0f;
-    const int ir = min((int)(ratio * (float)S.nr), S.nr - 1);
+    const int ir = min((int)(ratio * S.nr_f), S.nr - 1);
     const int is = min(max((int)ls, 0), S.ns - 1);
     const uint16_t* qc = tab + (valid ? (size_t)(ir * S.ns + is) * DTS_TABLE_COS_BINS : 0);
     const f3 axis = cv * __fdividef(1.0f, C);
@@ -588,7 +607,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       }
     } else {
       // R17: unwarped camera vertex, shell |x(t) - xe| in [Rm, RM): <= 2 t-intervals
-      const float resm = (float)(ps.resM - S.dt);
+      const float resm = d2f(ps.resM - S.dt);
       float a_lo = clo;
       if (S.s_excess > 0.0f) {
         const float Se = C + S.s_excess;
@@ -670,7 +689,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
         qq[10 * st] = __uint_as_float(df->cell);
         *pushed = true;
       } else {
-        contrib += conn_job_run<SH, WALLS>(S, ps.x, wc, job_dlo, job_width, coef, m7e);
+        contrib += conn_job_run<SH, FL>(S, ps.x, wc, job_dlo, job_width, coef, m7e);
       }
     }
   }
@@ -739,16 +758,19 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     }
     // resample: smallest i with sum_{j<=i} w_j > u3 W (CDF inversion in candidate order)
     const float thr = unif(r[3]) * W;
+    // the partial sums are monotone, so candidate i is taken iff it is the
+    // first whose partial sum exceeds thr
     float cum = 0.0f, wsel = e2[7];
     uint32_t is = 7;
-    bool found = false;
+    bool gt_prev = false;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 7; ++i) {
       cum += e2[i];
-      const bool take = !found && (cum > thr);
+      const bool gt = cum > thr;
+      const bool take = gt && !gt_prev;
       wsel = take ? e2[i] : wsel;
       is = take ? (uint32_t)i : is;
-      found = found || take;
+      gt_prev = gt;
     }
     // regenerate the selected candidate's distance (cheaper than keeping all 8)
     const uint32_t brs = __brev(is) >> 29;
@@ -758,7 +780,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float beta_ris = S.albedo * (W * 0.125f) * __fdividef(1.0f, wsel);  // E15: a * mean(w) / w*
     ps.beta *= beta_ris;
     ps.x = fma3(ww, dsel, ps.x);
-    ps.resM -= (double)(counts * dsel);
+    ps.resM -= f2d(counts * dsel);
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
     if (DBG) { dbg->event = 1; dbg->istar = (int)is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
@@ -769,7 +791,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const float pl = (face & 1) ? S.bmax[a] : S.bmin[a];
       if (a == 0) xn.x = pl; else if (a == 1) xn.y = pl; else xn.z = pl;  // snap onto the wall
       ps.x = xn;
-      ps.resM -= (double)(counts * hi);
+      ps.resM -= f2d(counts * hi);
       ps.kind = KIND_WALL;
       ps.face = face;
       ps.w = ww;
@@ -787,7 +809,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   // early exit: no later connection can land before R_M
   const f3 dn = ps.x - xe;
   const float Cn = sqrtf(dot(dn, dn));
-  if ((float)ps.resM - Cn <= 0.0f) {
+  if (d2f(ps.resM) - Cn <= 0.0f) {
     if (DBG) dbg->terminate = 1;
     end_reason = DTS_CTR_EARLY_EXIT;
     return false;
@@ -802,12 +824,12 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
 
 // Runs queued connection job (fields at q[f * st]).  Returns the contribution
 // already scaled by 1 / n_cell, and its cell.
-template <int SH, bool WALLS>
+template <int SH, int FL>
 __device__ __forceinline__ float conn_job_eval(const DevScene& S, const float* q, uint32_t st, uint32_t& cell) {
   const f3 x = mk(q[0 * st], q[1 * st], q[2 * st]);
   const f3 wc = mk(q[3 * st], q[4 * st], q[5 * st]);
   cell = __float_as_uint(q[10 * st]);
-  return conn_job_run<SH, WALLS>(S, x, wc, q[6 * st], q[7 * st], q[8 * st], __float_as_uint(q[9 * st]));
+  return conn_job_run<SH, FL>(S, x, wc, q[6 * st], q[7 * st], q[8 * st], __float_as_uint(q[9 * st]));
 }
 
 }  // namespace dts

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_
 }
 
 // ============================================================== debug kernel
-template <int SH, bool WALLS, bool SPLIT>
+template <int SH, int FL>
 __global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n, const dts_debug_in* __restrict__ in,
                              dts_debug_out* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -155,7 +155,7 @@ __global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n
   float c;
   bool cn, wn;
   int reason;
-  darts_vertex<true, false, SH, WALLS, SPLIT>(S, tab, ps, r, c, &o, cn, wn, reason);
+  darts_vertex<true, false, SH, FL>(S, tab, ps, r, c, &o, cn, wn, reason);
   o.E_next = RM - ps.resM;
   out[i] = o;
 }
@@ -199,7 +199,7 @@ struct PathCtx {
 };
 
 // decode a work index into a path (returns false if the path retires at start)
-template <int SH, bool WALLS>
+template <int SH, int FL>
 __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx, PathCtx& pc, uint32_t& ctr_miss,
                                            uint32_t& ctr_early) {
   const DevScene& S = P.S;
@@ -256,7 +256,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   pc.inv_n = inv_n;
   pc.acc = 0.0f;
   const u4 a = philox_rk(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 0u, S.rk);
-  int e = min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1);
+  const int e = (FL & FL_MULTI_E) ? min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1) : 0;
   PathState& ps = pc.ps;
   ps.e = e;
   if (S.camera_kind == DTS_CAMERA_PINHOLE) {
@@ -287,13 +287,13 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   ps.resM = S.t0 + (double)(b + 1) * S.dt - (double)S.em_t[e];  // R_M - E with E = 0
   float lo, hi;
   int f;
-  if (intersect<SH, WALLS>(S, ps.x, ps.w, lo, hi, f) == HIT_MISS) {
+  if (intersect<SH, (FL & FL_WALLS) != 0>(S, ps.x, ps.w, lo, hi, f) == HIT_MISS) {
     ++ctr_miss;
     return false;
   }
   if (S.warped || S.camera_kind == DTS_CAMERA_SPHERE_DETECTOR) {
     const f3 dv = ps.x - ld3(S.em_pos[e]);
-    if (sqrtf(dot(dv, dv)) >= (float)ps.resM) {
+    if (sqrtf(dot(dv, dv)) >= d2f(ps.resM)) {
       ++ctr_early;
       return false;
     }
@@ -372,8 +372,9 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
 #ifndef DTS_TABLE_SMEM
 #define DTS_TABLE_SMEM 1
 #endif
-template <bool SMEM, int SH, bool WALLS, bool SPLIT>
+template <bool SMEM, int SH, int FL>
 __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const RenderParams P) {
+  constexpr bool WALLS = (FL & FL_WALLS) != 0;
   extern __shared__ __align__(16) uint16_t s_dyn[];
   __shared__ uint64_t s_bar;
   const DevScene& S = P.S;
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
     float c = 0.0f;
     uint32_t cell = 0;
     if ((uint32_t)lane < df.qn) {
-      c = conn_job_eval<SH, WALLS>(S, df.q + lane, qstride, cell);
+      c = conn_job_eval<SH, FL>(S, df.q + lane, qstride, cell);
       if (!isfinite(c)) {
         ++c_nf;
         c = 0.0f;
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
         we = ne;
       }
       if (!active && my != ~0ull && my < P.total) {
-        active = start_path<SH, WALLS>(P, my, pc, l_miss, l_early);
+        active = start_path<SH, FL>(P, my, pc, l_miss, l_early);
         ++c_paths;
       }
     }
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       df.act = act;
       df.cell = pc.cell;
       df.inv_n = pc.inv_n;
-      const bool alive = darts_vertex<false, SMEM, SH, WALLS, SPLIT>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee,
+      const bool alive = darts_vertex<false, SMEM, SH, FL>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee,
                                                                      reason, s_queue ? &df : nullptr, &pushed);
       pc.acc += contrib;
       ++pc.k;
@@ -705,50 +706,67 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
 
 // ============================================================== kernel selection
 // Render and debug kernels are specialised at compile time on the medium
-// shape, the presence of walls and the direction mode (R29), so no launch
-// carries the branches or registers of the other scene kinds.
-template <bool SMEM>
-static const void* darts_kernel_ptr_t(int shape, bool walls, bool split) {
-  if (shape == DTS_MEDIUM_INFINITE)
-    return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_INFINITE, false, true>
-                 : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_INFINITE, false, false>;
-  if (shape == DTS_MEDIUM_SPHERE)
-    return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, false, true>
-                 : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, false, false>;
+// shape and the variant flags FL_WALLS, FL_SPLIT (direction mode, R29) and
+// FL_MULTI_E (more than one emitter), so no launch carries the branches,
+// registers or constant-bank indexing of the other scene kinds.  Walls exist
+// only in BOX media (validated), so the other shapes instantiate the even FLs.
+template <bool SMEM, int SH, int FL>
+static const void* rk_ptr() { return (const void*)render_darts_kernel<SMEM, SH, FL>; }
+template <int SH, int FL>
+static const void* dk_ptr() { return (const void*)debug_kernel<SH, FL>; }
+
+template <template <int> class Pick>
+static const void* pick_fl(int shape, int fl) {
   if (shape == DTS_MEDIUM_BOX) {
-    if (walls)
-      return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, true, true>
-                   : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, true, false>;
-    return split ? (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, false, true>
-                 : (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, false, false>;
+    switch (fl) {
+      case 0: return Pick<0>::box(); case 1: return Pick<1>::box();
+      case 2: return Pick<2>::box(); case 3: return Pick<3>::box();
+      case 4: return Pick<4>::box(); case 5: return Pick<5>::box();
+      case 6: return Pick<6>::box(); case 7: return Pick<7>::box();
+    }
+    return nullptr;
+  }
+  if (fl & FL_WALLS) return nullptr;
+  const bool inf = shape == DTS_MEDIUM_INFINITE;
+  if (!inf && shape != DTS_MEDIUM_SPHERE) return nullptr;
+  switch (fl) {
+    case 0: return inf ? Pick<0>::inf() : Pick<0>::sph();
+    case 2: return inf ? Pick<2>::inf() : Pick<2>::sph();
+    case 4: return inf ? Pick<4>::inf() : Pick<4>::sph();
+    case 6: return inf ? Pick<6>::inf() : Pick<6>::sph();
   }
   return nullptr;
 }
-static const void* darts_kernel_ptr(bool smem, int shape, bool walls, bool split) {
-  return smem ? darts_kernel_ptr_t<true>(shape, walls, split) : darts_kernel_ptr_t<false>(shape, walls, split);
+template <int FL> struct PickRenderSmem {
+  static const void* box() { return rk_ptr<true, DTS_MEDIUM_BOX, FL>(); }
+  static const void* inf() { return rk_ptr<true, DTS_MEDIUM_INFINITE, FL>(); }
+  static const void* sph() { return rk_ptr<true, DTS_MEDIUM_SPHERE, FL>(); }
+};
+template <int FL> struct PickRenderGlobal {
+  static const void* box() { return rk_ptr<false, DTS_MEDIUM_BOX, FL>(); }
+  static const void* inf() { return rk_ptr<false, DTS_MEDIUM_INFINITE, FL>(); }
+  static const void* sph() { return rk_ptr<false, DTS_MEDIUM_SPHERE, FL>(); }
+};
+template <int FL> struct PickDebug {
+  static const void* box() { return dk_ptr<DTS_MEDIUM_BOX, FL>(); }
+  static const void* inf() { return dk_ptr<DTS_MEDIUM_INFINITE, FL>(); }
+  static const void* sph() { return dk_ptr<DTS_MEDIUM_SPHERE, FL>(); }
+};
+static int scene_flags(const dts_scene_desc& d) {
+  return (d.wall_mask ? FL_WALLS : 0) | (d.direction_mode == DTS_DIR_SPLIT ? FL_SPLIT : 0) |
+         (d.n_emitters > 1 ? FL_MULTI_E : 0);
 }
+static const void* darts_kernel_ptr(bool smem, const dts_scene_desc& d) {
+  return smem ? pick_fl<PickRenderSmem>(d.medium_shape, scene_flags(d))
+              : pick_fl<PickRenderGlobal>(d.medium_shape, scene_flags(d));
+}
+static const void* debug_kernel_ptr(const dts_scene_desc& d) { return pick_fl<PickDebug>(d.medium_shape, scene_flags(d)); }
 static const void* vanilla_kernel_ptr(int shape, bool walls) {
   if (shape == DTS_MEDIUM_INFINITE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_INFINITE, false>;
   if (shape == DTS_MEDIUM_SPHERE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_SPHERE, false>;
   if (shape == DTS_MEDIUM_BOX)
     return walls ? (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, true>
                  : (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, false>;
-  return nullptr;
-}
-static const void* debug_kernel_ptr(int shape, bool walls, bool split) {
-  if (shape == DTS_MEDIUM_INFINITE)
-    return split ? (const void*)debug_kernel<DTS_MEDIUM_INFINITE, false, true>
-                 : (const void*)debug_kernel<DTS_MEDIUM_INFINITE, false, false>;
-  if (shape == DTS_MEDIUM_SPHERE)
-    return split ? (const void*)debug_kernel<DTS_MEDIUM_SPHERE, false, true>
-                 : (const void*)debug_kernel<DTS_MEDIUM_SPHERE, false, false>;
-  if (shape == DTS_MEDIUM_BOX) {
-    if (walls)
-      return split ? (const void*)debug_kernel<DTS_MEDIUM_BOX, true, true>
-                   : (const void*)debug_kernel<DTS_MEDIUM_BOX, true, false>;
-    return split ? (const void*)debug_kernel<DTS_MEDIUM_BOX, false, true>
-                 : (const void*)debug_kernel<DTS_MEDIUM_BOX, false, false>;
-  }
   return nullptr;
 }
 
@@ -864,6 +882,7 @@ static void derive(const dts_scene_desc& d, DevScene& S) {
   for (int i = 0; i < 4; ++i) S.crop[i] = d.crop[i];
   S.t0 = d.t0;
   S.dt = ((double)d.t1 - (double)d.t0) / d.n_bins;
+  S.dt_f = (float)S.dt;
   S.n_bins = d.n_bins;
   S.warped = d.warped ? 1 : 0;
   S.strategy = d.strategy;
@@ -968,6 +987,8 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
   CUDA_TRY(cudaGetLastError());
   s->S.nr = nr;
   s->S.ns = ns;
+  s->S.nr_f = (float)nr;
+  s->S.ns_f = (float)ns;
   s->S.ln_smin = (float)std::log(smin);
   s->S.inv_dls = (float)(ns / (std::log(smax) - std::log(smin)));
   return DTS_OK;
@@ -1046,7 +1067,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     P.flush_at = fa ? (uint32_t)atoi(fa) : 28u;
     if (P.flush_at < 1 || P.flush_at > (uint32_t)kQueue) P.flush_at = 28u;
     const size_t dyn = (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + (defer ? qbytes : 0);
-    const void* kfn = darts_kernel_ptr(smem, d.medium_shape, d.wall_mask != 0u, d.direction_mode == DTS_DIR_SPLIT);
+    const void* kfn = darts_kernel_ptr(smem, d);
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
     int blocks_per_sm = 1;
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
@@ -1119,7 +1140,7 @@ dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, 
     CUDA_TRY(cudaMemsetAsync(d_dummy, 0, 256 * sizeof(uint16_t), (cudaStream_t)stream));
     tab = d_dummy;
   }
-  const void* kfn = debug_kernel_ptr(s->desc.medium_shape, s->desc.wall_mask != 0u, s->desc.direction_mode == DTS_DIR_SPLIT);
+  const void* kfn = debug_kernel_ptr(s->desc);
   if (!kfn) return fail(DTS_E_INVALID_ARG, "no debug kernel for this scene shape");
   DevScene S = s->S;
   set_round_keys(S, 0);

@@ -1,0 +1,12 @@
+# bench lines (c5 full with cpu baseline, c3) + ncu full captures of the render kernel (tag = $1)
+TAG=${1:-dev}
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench_c5_$TAG.json 2> gpurun_out/bench_c5_$TAG.err; echo "bench5 rc=$?"
+timeout 600 python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_c3_$TAG.json 2> gpurun_out/bench_c3_$TAG.err; echo "bench3 rc=$?"
+for spec in "5 16" "3 4"; do
+  set -- $spec
+  PCMD="python bench.py --config $1 --spp $2 --steps 1 --warmup 3 --no-cpu-baseline"
+  $PCMD > gpurun_out/plain_prof_c$1.log 2>&1 && \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_darts -s 3 -c 1 \
+      -o gpurun_out/prof_${TAG}_c$1 $PCMD > gpurun_out/ncu_full_c$1.log 2>&1; echo "ncu c$1 rc=$?"
+done
