@@ -28,7 +28,7 @@ __device__ __forceinline__ void step(float (&a)[kChains], uint32_t (&u)[kChains]
     if (OP == 2) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
     if (OP == 3) asm volatile("lg2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
     if (OP == 4) asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
-    if (OP == 5) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+    if (OP == 5) asm volatile("rcp.approx.ftz.f32 %0, %0;\n\tadd.ftz.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(c));  // + FADD: ptxas folds rcp(rcp(x))
     if (OP == 6) asm volatile("sin.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
     if (OP == 7) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(u[i]) : "r"(__float_as_uint(b)), "r"(__float_as_uint(c)));
     if (OP == 8) {
