@@ -429,6 +429,41 @@ struct Defer {
   float inv_n;        // 1 / paths of the cell
 };
 
+// A medium event whose RIS distance is drawn later by the warp-collective
+// sampler (RIS layout B); the vertex state is kept in PathState
+// (x, w = the walk direction, resM, beta).
+struct RisReq {
+  bool need;
+  float lo, T_m, counts;
+};
+
+// Applies a selected RIS candidate (E15): beta *= a mean(w) / w*, moves to
+// x + w d and spends the counted time.
+__device__ __forceinline__ void ris_apply(const DevScene& S, PathState& ps, float dsel, float W, float wsel,
+                                          float counts) {
+  const float beta_ris = S.albedo * (W * 0.125f) * __fdividef(1.0f, wsel);
+  ps.beta *= beta_ris;
+  ps.x = fma3(ps.w, dsel, ps.x);
+  ps.resM -= f2d(counts * dsel);
+  ps.kind = KIND_MEDIUM;
+}
+
+// End-of-vertex termination tests: early exit (no later
+// connection can land before R_M) and non-finite throughput.
+__device__ __forceinline__ bool vertex_tail(const PathState& ps, f3 xe, int& end_reason) {
+  const f3 dn = ps.x - xe;
+  const float Cn = sqrtf(dot(dn, dn));
+  if (d2f(ps.resM) - Cn <= 0.0f) {
+    end_reason = DTS_CTR_EARLY_EXIT;
+    return false;
+  }
+  if (!isfinite(ps.beta)) {
+    end_reason = DTS_CTR_NONFINITE;
+    return false;
+  }
+  return true;
+}
+
 // ----------------------------------------------------------------- one DARTS vertex
 // Returns true if the walk continues.  contrib receives the vertex's
 // connection (+ wall NEE) contribution; end_reason the DTS_CTR_* of a stop.
@@ -436,7 +471,8 @@ template <bool DBG, bool SMEM, int SH, int FL>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason,
-                                             const Defer* df = nullptr, bool* pushed = nullptr) {
+                                             const Defer* df = nullptr, bool* pushed = nullptr,
+                                             RisReq* rq = nullptr) {
   contrib = 0.0f;
   conn_nonempty = false;
   wall_nee = false;
@@ -706,6 +742,16 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   const float T_m = inf_hi ? 0.0f : fexp(-S.sigma_t * (hi - lo));      // 1 - p_m
   const float u0 = unif(r[0]);
   if (DBG) dbg->p_m = p_m;
+  if (rq) rq->need = false;
+  if (!DBG && rq && u0 < p_m) {
+    // RIS layout B: the warp draws the distance after this call
+    rq->need = true;
+    rq->lo = lo;
+    rq->T_m = T_m;
+    rq->counts = counts;
+    ps.w = ww;
+    return true;
+  }
   if (u0 < p_m) {
     // candidates: Sobol row r = floor(32 u1) with Cranley-Patterson shift u2 (R6):
     // Q[r][i] = RI2(8r+i) = bitrev3(i)/8 + bitrev5(r)/256, shift and mod 1 done
@@ -806,20 +852,103 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     dbg->x_next[0] = ps.x.x; dbg->x_next[1] = ps.x.y; dbg->x_next[2] = ps.x.z;
     dbg->beta_out = ps.beta;
   }
-  // early exit: no later connection can land before R_M
-  const f3 dn = ps.x - xe;
-  const float Cn = sqrtf(dot(dn, dn));
-  if (d2f(ps.resM) - Cn <= 0.0f) {
-    if (DBG) dbg->terminate = 1;
-    end_reason = DTS_CTR_EARLY_EXIT;
-    return false;
+  const bool alive = vertex_tail(ps, xe, end_reason);
+  if (DBG && !alive) dbg->terminate = 1;
+  return alive;
+}
+
+// RIS layout B (SURVEY 8(a) "8-lane groups"): the warp draws the distances of
+// every lane with a pending medium event (RisReq), four paths per round, one
+// 8-lane group per path and one candidate per lane.  Per-path inputs are
+// broadcast with shuffles; the group max-normalises the log weights (R7),
+// scans them in candidate order (inclusive, 3 shuffles) and takes the first
+// candidate whose partial sum exceeds u3 W -- CDF inversion in the candidate
+// order of layout A / the oracle (E13-E15, R6).  All 32 lanes must call it.
+// Returns, to each requesting lane, dsel, W and w*; W = 0 means all invalid (R5).
+__device__ __forceinline__ void ris_warp(const DevScene& S, const PathState& ps, const RisReq& rq, f3 xe,
+                                         uint32_t r1, uint32_t r2, uint32_t r3, int lane, float& dsel, float& W,
+                                         float& wsel) {
+  const unsigned FULL = 0xffffffffu;
+  unsigned pend = __ballot_sync(FULL, rq.need);
+  // per-path inputs, prepared by the owner lane
+  float qd = 0.0f, perp2 = 0.0f;
+  if (rq.need) {
+    const f3 cv = xe - ps.x;
+    qd = dot(ps.w, cv);
+    const f3 perp = cv - ps.w * qd;
+    perp2 = dot(perp, perp);
   }
-  if (!isfinite(ps.beta)) {
-    if (DBG) dbg->terminate = 1;
-    end_reason = DTS_CTR_NONFINITE;
-    return false;
+  const float resM_o = d2f(ps.resM);
+  const uint32_t m2_o = r2 >> 9, br5_o = __brev(r1 >> 27) >> 27;
+  const float u3_o = unif(r3);
+  const int g = lane >> 3, c = lane & 7;
+  const uint32_t br3 = __brev((uint32_t)c) >> 29;
+  dsel = 0.0f;
+  W = 0.0f;
+  wsel = 1.0f;
+  while (pend) {
+    // the (g+1)-th pending lane of this round is group g's path
+    unsigned m = pend;
+    for (int k = 0; k < g && m; ++k) m &= m - 1u;
+    const int owner = m ? __ffs(m) - 1 : -1;
+    const int src = owner >= 0 ? owner : lane;
+    const float lo = __shfl_sync(FULL, rq.lo, src);
+    const float T_m = __shfl_sync(FULL, rq.T_m, src);
+    const float counts = __shfl_sync(FULL, rq.counts, src);
+    const float resM = __shfl_sync(FULL, resM_o, src);
+    const float q = __shfl_sync(FULL, qd, src);
+    const float p2 = __shfl_sync(FULL, perp2, src);
+    const uint32_t m2 = __shfl_sync(FULL, m2_o, src);
+    const uint32_t br5 = __shfl_sync(FULL, br5_o, src);
+    const float u3 = __shfl_sync(FULL, u3_o, src);
+    // candidate c of the group's path (identical arithmetic to layout A)
+    const uint32_t v = (m2 + ((br3 * 32u + br5) << 15)) & 0x7FFFFFu;
+    const float ui = mant01(v);
+    const float di = fmaf(-__log2f(fmaf(ui, T_m, 1.0f - ui)), S.inv_sigma_t * kLn2, lo);
+    const float Delta = resM - counts * di;
+    const float dq = di - q;
+    const float r2i = fmaf(dq, dq, p2);
+    const bool valid = owner >= 0 && r2i < Delta * fabsf(Delta);
+    const float sr = rsqrtf(fmaxf(Delta, 1e-20f));
+    const float ex = valid ? fmaf(S.neg_inv4D_log2e * r2i, sr * sr, S.neg_sa_log2e * Delta)
+                           : -__int_as_float(0x7f800000);
+    float emax = ex;
+    emax = fmaxf(emax, __shfl_xor_sync(FULL, emax, 1));
+    emax = fmaxf(emax, __shfl_xor_sync(FULL, emax, 2));
+    emax = fmaxf(emax, __shfl_xor_sync(FULL, emax, 4));
+    if (emax == -__int_as_float(0x7f800000)) emax = 0.0f;
+    const float w = sr * sr * sr * exp2f(ex - emax);
+    float cum = w;  // inclusive scan within the group
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const float t = __shfl_up_sync(FULL, cum, o, 8);
+      if (c >= o) cum += t;
+    }
+    const float Wg = __shfl_sync(FULL, cum, 7, 8);
+    const bool gt = cum > u3 * Wg;
+    const unsigned gb = (__ballot_sync(FULL, gt) >> (8 * g)) & 0xFFu;
+    const int is = gb ? __ffs(gb) - 1 : 7;
+    const float ws = __shfl_sync(FULL, w, is, 8);
+    const float ds = __shfl_sync(FULL, di, is, 8);
+    // return to the owners: owner of group k reads lane 8k
+    const unsigned here = pend;
+    int k = -1;
+    if (rq.need && ((here >> lane) & 1u)) {
+      const int rank = __popc(here & ((1u << lane) - 1u));
+      if (rank < 4) k = rank;
+    }
+    const int from = k >= 0 ? 8 * k : lane;
+    const float Wr = __shfl_sync(FULL, Wg, from);
+    const float wr = __shfl_sync(FULL, ws, from);
+    const float dr = __shfl_sync(FULL, ds, from);
+    if (k >= 0) {
+      W = Wr;
+      wsel = wr;
+      dsel = dr;
+    }
+    // retire this round's (up to) four paths
+    for (int j = 0; j < 4 && pend; ++j) pend &= pend - 1u;
   }
-  return true;
 }
 
 // Runs queued connection job (fields at q[f * st]).  Returns the contribution

@@ -187,6 +187,12 @@ struct RenderParams {
 #endif
 constexpr int kBlock = DTS_BLOCK;
 constexpr uint32_t kChunk = 128;
+#ifndef DTS_RIS_WARP
+#define DTS_RIS_WARP 0
+#endif
+// RIS layout: A = lane per path, 8 candidates in registers
+// (default); B = warp-collective 8-lane groups with shuffle scan/selection.
+constexpr bool kRisWarp = DTS_RIS_WARP != 0;
 constexpr size_t kPrivMaxCells = 4096;  // histograms up to 16 KiB are privatised per CTA
 
 struct PathCtx {
@@ -484,23 +490,42 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
     if (s_queue && df.qn >= P.flush_at) flush();
     bool done = false;
     bool pushed = false;
+    bool cn = false, wnee = false, alive = false;
+    int reason = 0;
+    uint32_t r[8];
+    float contrib = 0.0f;
+    RisReq rq;
+    rq.need = false;
     if (active) {
-      bool cn = false, wnee = false, cap = false;
-      int reason = 0;
-      uint32_t r[8];
       const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
       const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
       r[0] = a.a; r[1] = a.b; r[2] = a.c; r[3] = a.d;
       r[4] = b.a; r[5] = b.b; r[6] = b.c; r[7] = b.d;
-      float contrib;
       df.act = act;
       df.cell = pc.cell;
       df.inv_n = pc.inv_n;
-      const bool alive = darts_vertex<false, SMEM, SH, FL>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee,
-                                                                     reason, s_queue ? &df : nullptr, &pushed);
+      alive = darts_vertex<false, SMEM, SH, FL>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
+                                                s_queue ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr);
+    }
+    if (kRisWarp) {
+      // RIS layout B: the warp draws every pending medium event's distance
+      const f3 xe = ld3(S.em_pos[(FL & FL_MULTI_E) ? pc.ps.e : 0]);
+      float dsel, Wr, wsel;
+      ris_warp(S, pc.ps, rq, xe, r[1], r[2], r[3], lane, dsel, Wr, wsel);
+      if (rq.need) {
+        if (Wr > 0.0f) {
+          ris_apply(S, pc.ps, dsel, Wr, wsel, rq.counts);
+          alive = vertex_tail(pc.ps, xe, reason);
+        } else {
+          alive = false;
+          reason = DTS_CTR_RIS_INVALID;  // R5
+        }
+      }
+    }
+    if (active) {
       pc.acc += contrib;
       ++pc.k;
-      cap = alive && pc.k >= (uint32_t)S.max_bounces;
+      const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
       done = !alive || cap;
       ++c_vert;
       c_conn += cn ? 1u : 0u;
