@@ -83,6 +83,7 @@ _DEFAULTS = dict(
     fov_y_deg=45.0, det_radius=0.0, strategy="darts", n_ris=8, alpha=0.5,
     parity_r_excl=0.0, parity_s_excess=0.0, table_nr=16, table_ns=16,
     crop=None, table_smin=None, table_smax=None,
+    conn_sampling="exp",   # "exp": truncated exponential P of S; "uniform": ablation
 )
 
 

@@ -433,9 +433,14 @@ static double connect(const or_scene* sc, const derived* dv, const pstate* ps, c
     if (sc->parity_s_excess > 0.0) S_lo = fmax(S_lo, C + sc->parity_s_excess);
     if (dbg) { dbg->S_lo = S_lo; dbg->S_hi = S_hi; dbg->m_conn = fabs(S_hi - S_lo) / fmax(1.0, fabs(S_hi)); }
     if (!(S_hi > S_lo)) return 0.0;
-    /* truncated exponential P on [S_m, S_M) */
+    /* truncated exponential P on [S_m, S_M); or, as the
+     * ablation of the same passage, P uniform ("will degrade to one of the
+     * sampling method proposed by Jarabo et al.") */
     double S, pS;
-    if (isinf(S_hi)) {
+    if (sc->conn_sampling == OR_CONN_UNIFORM_S) {
+      S = S_lo + u7 * (S_hi - S_lo);
+      pS = 1.0 / (S_hi - S_lo);
+    } else if (isinf(S_hi)) {
       S = S_lo - log(1.0 - u7) / dv->sigma_t;
       pS = dv->sigma_t * exp(-dv->sigma_t * (S - S_lo));
     } else {
@@ -599,7 +604,9 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
     double S = ps->RM - ps->E; /* R11: upper residual */
     int cell = 0;
     double mcell;
-    int valid = table_cell(sc, C, S, &cell, &mcell);
+    /* DA_ONLY ablation: phase-function directions only (gamma = 0) */
+    int valid = sc->strategy == OR_STRATEGY_DA_ONLY ? 0 : table_cell(sc, C, S, &cell, &mcell);
+    if (sc->strategy == OR_STRATEGY_DA_ONLY) mcell = INFINITY;
     double ratio = C / S;
     double gamma = valid ? ratio / (ratio + sc->alpha) : 0.0; /* E19 */
     double axis[3] = {0, 0, 1};
@@ -687,7 +694,17 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
   double p_m = isinf(hi) ? 1.0 : 1.0 - exp(-dv->sigma_t * (hi - lo)); /* E12, R28 */
   double u0 = uu(r, 0);
   if (dbg) { dbg->p_m = p_m; dbg->m_event = (p_m < 1.0) ? fabs(u0 - p_m) : INFINITY; }
-  if (u0 < p_m) {
+  if (u0 < p_m && sc->strategy == OR_STRATEGY_EDA_ONLY) {
+    /* EDA_ONLY ablation: one truncated-exponential distance (E13-E14, R1)
+     * with epsilon = u2; weight sigma_s e^{-st(d-lo)} / (p_cand p_m) = sigma_s / sigma_t */
+    double d = lo - log(1.0 - p_m * uu(r, 2)) / dv->sigma_t;
+    madd3(ps->x, ww, d, ps->x);
+    ps->beta *= sc->sigma_s / dv->sigma_t;
+    ps->E += counts * d;
+    ps->kind = OR_KIND_MEDIUM;
+    memcpy(ps->w, ww, sizeof ps->w);
+    if (dbg) { dbg->event = 1; dbg->istar = 0; dbg->d = d; dbg->beta_ris = sc->sigma_s / dv->sigma_t; dbg->m_select = INFINITY; dbg->m_valid = INFINITY; }
+  } else if (u0 < p_m) {
     int N = sc->n_ris;
     int row = (int)floor(32.0 * uu(r, 1));
     double eps0 = uu(r, 2);
@@ -1105,7 +1122,7 @@ int or_render(const or_scene* sc, const uint16_t* q, uint64_t spp, uint64_t seed
               uint64_t s_end, double* hist, double* hist_sq, double* order_hist, int n_orders,
               or_stats* stats, int nthreads) {
   if (!hist || s_end < s_begin) return -1;
-  if (sc->strategy == OR_STRATEGY_DARTS && !q) return -2;
+  if ((sc->strategy == OR_STRATEGY_DARTS || sc->strategy == OR_STRATEGY_EDA_ONLY) && !q) return -2;
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   int cw = sc->crop[2] - sc->crop[0], ch = sc->crop[3] - sc->crop[1];

@@ -21,7 +21,12 @@ extern "C" {
 
 enum { OR_MEDIUM_INFINITE = 0, OR_MEDIUM_SPHERE = 1, OR_MEDIUM_BOX = 2 };
 enum { OR_CAMERA_PINHOLE = 0, OR_CAMERA_SPHERE_DETECTOR = 1 };
-enum { OR_STRATEGY_DARTS = 0, OR_STRATEGY_VANILLA = 1 };
+/* DA_ONLY: DA-RIS distances + phase-function directions; EDA_ONLY: exponential
+ * distances + EDA/HG MIS directions; both keep the elliptical connection
+ * (ablation). */
+enum { OR_STRATEGY_DARTS = 0, OR_STRATEGY_VANILLA = 1, OR_STRATEGY_DA_ONLY = 2, OR_STRATEGY_EDA_ONLY = 3 };
+/* distribution P of S in the elliptical sampling of E21 */
+enum { OR_CONN_TRUNC_EXP = 0, OR_CONN_UNIFORM_S = 1 };
 enum { OR_DIR_REUSE = 0, OR_DIR_SPLIT = 1 };
 enum { OR_SPP_PER_CELL = 0, OR_SPP_PER_PIXEL = 1 };
 enum { OR_KIND_CAMERA = 0, OR_KIND_MEDIUM = 1, OR_KIND_WALL = 2 };
@@ -48,6 +53,7 @@ typedef struct {
   double parity_r_excl, parity_s_excess;
   int32_t table_nr, table_ns;
   double table_smin, table_smax;
+  int32_t conn_sampling; /* OR_CONN_* */
 } or_scene;
 
 /* 16-bit quantised per-cell CDF of the EDA direction table (R8-R10):

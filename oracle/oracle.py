@@ -70,6 +70,7 @@ class OrScene(ctypes.Structure):
         ("parity_r_excl", ctypes.c_double), ("parity_s_excess", ctypes.c_double),
         ("table_nr", ctypes.c_int32), ("table_ns", ctypes.c_int32),
         ("table_smin", ctypes.c_double), ("table_smax", ctypes.c_double),
+        ("conn_sampling", ctypes.c_int32),
     ]
 
 
@@ -108,7 +109,8 @@ DEBUG_OUT = np.dtype([
 
 _MED = {"infinite": 0, "sphere": 1, "box": 2}
 _CAM = {"pinhole": 0, "detector": 1}
-_STRAT = {"darts": 0, "vanilla": 1}
+_STRAT = {"darts": 0, "vanilla": 1, "da_only": 2, "eda_only": 3}
+_CONN = {"exp": 0, "uniform": 1}
 _DIR = {"reuse": 0, "split": 1}
 _SPP = {"cell": 0, "pixel": 1}
 
@@ -147,6 +149,7 @@ def scene(c: dict) -> OrScene:
     s.parity_r_excl, s.parity_s_excess = c["parity_r_excl"], c["parity_s_excess"]
     s.table_nr, s.table_ns = c["table_nr"], c["table_ns"]
     s.table_smin, s.table_smax = c["table_smin"], c["table_smax"]
+    s.conn_sampling = _CONN[c.get("conn_sampling", "exp")]
     return s
 
 
