@@ -58,14 +58,23 @@ typedef enum {
 
 enum { DTS_MEDIUM_INFINITE = 0, DTS_MEDIUM_SPHERE = 1, DTS_MEDIUM_BOX = 2 };
 enum { DTS_CAMERA_PINHOLE = 0, DTS_CAMERA_SPHERE_DETECTOR = 1 };
-enum { DTS_STRATEGY_DARTS = 0, DTS_STRATEGY_VANILLA = 1 };
+/* DARTS: full method.  VANILLA: exponential flight + phase sampling + direct
+ * shadow connection.  Ablations of PAPER.md:426-435, both
+ * with the elliptical connection: DA_ONLY = DA-RIS distances + phase-function
+ * directions; EDA_ONLY = exponential distances + EDA/HG MIS directions. */
+enum { DTS_STRATEGY_DARTS = 0, DTS_STRATEGY_VANILLA = 1, DTS_STRATEGY_DA_ONLY = 2, DTS_STRATEGY_EDA_ONLY = 3 };
+/* Distribution P of S in the elliptical sampling E21: the
+ * paper's truncated exponential, or uniform (the Jarabo et al. variant). */
+enum { DTS_CONN_TRUNC_EXP = 0, DTS_CONN_UNIFORM_S = 1 };
 enum { DTS_DIR_REUSE = 0, DTS_DIR_SPLIT = 1 };     /* R29 */
 enum { DTS_SPP_PER_CELL = 0, DTS_SPP_PER_PIXEL = 1 }; /* R21 */
 
 /* Scene description.  Validation (dts_scene_create): sigma_s > 0, sigma_a >= 0,
  * -1 < g < 1; 1 <= n_emitters <= 8; width, height >= 1; crop
  * inside the image and non-empty; t1 > t0; n_bins >= 1; n_ris == 8;
- * alpha >= 0 (E19); 1 <= max_bounces <= 65536; box bmax > bmin; radius > 0. */
+ * alpha >= 0 (E19); 1 <= max_bounces <= 65536; box bmax > bmin; radius > 0;
+ * strategy and conn_sampling one of their enums.  Every strategy but VANILLA
+ * needs dts_table_build before dts_render (DA_ONLY does not read the table). */
 typedef struct {
   float sigma_s, sigma_a, g; /* homogeneous medium, HG phase */
   int32_t medium_shape;      /* DTS_MEDIUM_*; the medium is index-matched, vacuum outside */
@@ -93,6 +102,7 @@ typedef struct {
   int32_t spp_mode;                  /* DTS_SPP_* (R21) */
   float parity_r_excl;               /* TEST ONLY: drop contributions whose last segment < r (0 = off) */
   float parity_s_excess;             /* TEST ONLY: require S - C >= eps for medium-last paths (0 = off) */
+  int32_t conn_sampling;             /* DTS_CONN_* (0 = paper) */
 } dts_scene_desc;
 
 /* EDA table axes (R8): n_ratio uniform bins of C/S in [0,1), n_s log-spaced

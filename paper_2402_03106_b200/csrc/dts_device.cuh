@@ -55,6 +55,7 @@ struct DevScene {
   float dt_f;  // (float) dt
   int32_t n_bins, warped;
   int32_t strategy, direction_mode, spp_mode, max_bounces;
+  int32_t conn_uniform;  // 1: P of S uniform (ablation of PAPER.md:295)
   float alpha;
   float r_excl, s_excess;
   // EDA table (R8-R10)
@@ -319,10 +320,16 @@ struct EllSample {
 __device__ __forceinline__ EllSample ell_sample(const DevScene& S, f3 cv, float C, float q, f3 wc, float dlo,
                                                 float width, float u7) {
   // truncated exponential on [S_lo, S_hi); e^{-st (S-S_lo)} = 1 - u7 span
-  const float span = one_m_exp(S.sigma_t * width);
-  const float keep = fmaf(u7, fexp(-S.sigma_t * width), 1.0f - u7);  // 1 - u7 span
-  const float L = neg_log1m2(u7 * span, keep) * S.inv_sigma_t;
-  const float pS = S.sigma_t * keep * __fdividef(1.0f, span);
+  float L, pS;
+  if (S.conn_uniform) {  // ablation: P uniform on [S_lo, S_hi)
+    L = u7 * width;
+    pS = __fdividef(1.0f, width);
+  } else {
+    const float span = one_m_exp(S.sigma_t * width);
+    const float keep = fmaf(u7, fexp(-S.sigma_t * width), 1.0f - u7);  // 1 - u7 span
+    L = neg_log1m2(u7 * span, keep) * S.inv_sigma_t;
+    pS = S.sigma_t * keep * __fdividef(1.0f, span);
+  }
   const float dSC = dlo + L;  // S - C
   const float Ssm = C + dSC;
   // S - q = (S - C) + (C - q), C - q = perp^2 / (C + q) for q > 0
@@ -524,7 +531,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float C = sqrtf(dot(cv, cv));
     const float ratio = __fdividef(C, resM);
     const float ls = (__logf(resM) - S.ln_smin) * S.inv_dls;
-    const bool valid = (resM > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < S.ns_f);
+    // DA_ONLY ablation: phase-function directions only (gamma = 0)
+    const bool valid = (resM > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < S.ns_f) &&
+                       S.strategy != DTS_STRATEGY_DA_ONLY;
     const float gamma = valid ? __fdividef(ratio, ratio + S.alpha) : 0.0f;
     const int ir = min((int)(ratio * S.nr_f), S.nr - 1);
     const int is = min(max((int)ls, 0), S.ns - 1);
@@ -743,7 +752,18 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   const float u0 = unif(r[0]);
   if (DBG) dbg->p_m = p_m;
   if (rq) rq->need = false;
-  if (!DBG && rq && u0 < p_m) {
+  if (u0 < p_m && S.strategy == DTS_STRATEGY_EDA_ONLY) {
+    // EDA_ONLY ablation: one truncated-exponential distance (E13-E14, R1), eps = u2;
+    // weight sigma_s e^{-st (d - lo)} / (p_cand p_m) = a
+    const float u2 = unif(r[2]);
+    const float d = fmaf(-__log2f(fmaf(u2, T_m, 1.0f - u2)), S.inv_sigma_t * kLn2, lo);
+    ps.beta *= S.albedo;
+    ps.x = fma3(ww, d, ps.x);
+    ps.resM -= f2d(counts * d);
+    ps.kind = KIND_MEDIUM;
+    ps.w = ww;
+    if (DBG) { dbg->event = 1; dbg->istar = 0; dbg->d = d; dbg->beta_ris = S.albedo; }
+  } else if (!DBG && rq && u0 < p_m) {
     // RIS layout B: the warp draws the distance after this call
     rq->need = true;
     rq->lo = lo;
@@ -751,8 +771,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     rq->counts = counts;
     ps.w = ww;
     return true;
-  }
-  if (u0 < p_m) {
+  } else if (u0 < p_m) {
     // candidates: Sobol row r = floor(32 u1) with Cranley-Patterson shift u2 (R6):
     // Q[r][i] = RI2(8r+i) = bitrev3(i)/8 + bitrev5(r)/256, shift and mod 1 done
     // exactly on 23-bit integers.

@@ -841,7 +841,8 @@ static dts_status validate(const dts_scene_desc& d) {
       d.crop[3] <= d.crop[1])
     return bad("crop must be a non-empty sub-rectangle of the image");
   if (!(d.t1 > d.t0) || d.n_bins < 1) return bad("need t1 > t0 and n_bins >= 1");
-  if (d.strategy != DTS_STRATEGY_DARTS && d.strategy != DTS_STRATEGY_VANILLA) return bad("unknown strategy");
+  if (d.strategy < DTS_STRATEGY_DARTS || d.strategy > DTS_STRATEGY_EDA_ONLY) return bad("unknown strategy");
+  if (d.conn_sampling != DTS_CONN_TRUNC_EXP && d.conn_sampling != DTS_CONN_UNIFORM_S) return bad("unknown conn_sampling");
   if (d.n_ris != 8) return bad("n_ris must be 8 (PAPER.md:240)");
   if (!(d.alpha >= 0.0f)) return bad("alpha must be >= 0");
   if (d.max_bounces < 1 || d.max_bounces > 65536) return bad("max_bounces must be 1..65536");
@@ -911,6 +912,7 @@ static void derive(const dts_scene_desc& d, DevScene& S) {
   S.n_bins = d.n_bins;
   S.warped = d.warped ? 1 : 0;
   S.strategy = d.strategy;
+  S.conn_uniform = d.conn_sampling == DTS_CONN_UNIFORM_S ? 1 : 0;
   S.direction_mode = d.direction_mode;
   S.spp_mode = d.spp_mode;
   S.max_bounces = d.max_bounces;
@@ -1044,7 +1046,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   if (spp == 0 || se > spp || sb > se) return fail(DTS_E_RANGE, "need 0 <= sample_begin <= sample_end <= spp, spp > 0");
   if (sb == se) return DTS_OK;
   const dts_scene_desc& d = s->desc;
-  const bool darts = d.strategy == DTS_STRATEGY_DARTS;
+  const bool darts = d.strategy != DTS_STRATEGY_VANILLA;  // DARTS and its ablations
   if (darts && !s->d_table) return fail(DTS_E_STATE, "dts_table_build must run before a DARTS render");
   const uint64_t npix = (uint64_t)(d.crop[2] - d.crop[0]) * (uint64_t)(d.crop[3] - d.crop[1]);
   const uint64_t ns = se - sb;
@@ -1157,7 +1159,7 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
 dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, dts_debug_out* d_out, void* stream) {
   if (!s || (n > 0 && (!d_in || !d_out)) || n < 0) return fail(DTS_E_INVALID_ARG, "bad arguments");
   if (n == 0) return DTS_OK;
-  if (s->desc.strategy == DTS_STRATEGY_DARTS && !s->d_table) return fail(DTS_E_STATE, "table not built");
+  if (s->desc.strategy != DTS_STRATEGY_VANILLA && !s->d_table) return fail(DTS_E_STATE, "table not built");
   static uint16_t* d_dummy = nullptr;
   const uint16_t* tab = s->d_table;
   if (!tab) {

@@ -47,6 +47,7 @@ class SceneDesc(ctypes.Structure):
         ("strategy", ctypes.c_int32), ("n_ris", ctypes.c_int32), ("alpha", ctypes.c_float),
         ("max_bounces", ctypes.c_int32), ("direction_mode", ctypes.c_int32), ("spp_mode", ctypes.c_int32),
         ("parity_r_excl", ctypes.c_float), ("parity_s_excess", ctypes.c_float),
+        ("conn_sampling", ctypes.c_int32),
     ]
 
 
@@ -134,7 +135,8 @@ def _stream(stream) -> int | None:
 
 _MED = {"infinite": 0, "sphere": 1, "box": 2}
 _CAM = {"pinhole": 0, "detector": 1}
-_STRAT = {"darts": 0, "vanilla": 1}
+_STRAT = {"darts": 0, "vanilla": 1, "da_only": 2, "eda_only": 3}
+_CONN = {"exp": 0, "uniform": 1}
 _DIR = {"reuse": 0, "split": 1}
 _SPP = {"cell": 0, "pixel": 1}
 
@@ -172,6 +174,7 @@ def scene_desc(c: dict) -> SceneDesc:
     d.direction_mode = _DIR[c["direction_mode"]]
     d.spp_mode = _SPP[c["spp_mode"]]
     d.parity_r_excl, d.parity_s_excess = c["parity_r_excl"], c["parity_s_excess"]
+    d.conn_sampling = _CONN[c.get("conn_sampling", "exp")]
     return d
 
 

@@ -1,12 +1,14 @@
 #!/usr/bin/env python
-"""Equal-time MSE of GPU DARTS vs the GPU vanilla baseline (same kernels,
-north_star "MSE vs oracle at equal time").
+"""Equal-time MSE of GPU DARTS vs its ablations (DA-only, EDA-only,
+PAPER.md:426-435), uniform-S elliptical sampling and the GPU
+vanilla baseline -- same kernels (north_star "MSE vs oracle at equal time";
+SURVEY 8(d.4) (i), 8(f) #1).
 
 Per config (a centre crop for the large ones):
   1. reference = GPU DARTS at ref_mult x the config's spp (independent seeds);
   2. DARTS at the config's spp: device time T (CUDA events) and MSE vs the reference;
-  3. vanilla with its spp calibrated so its render takes ~T, MSE vs the reference;
-  4. repeated over `reps` seeds; MSE normalised to DARTS = 1.
+  3. every other strategy with its spp calibrated so its render takes ~T;
+  4. repeated over `reps` seeds; MSE x time normalised to DARTS = 1.
 For configs 3 and 5 both direction modes (REUSE, SPLIT) are measured (R29).
 Writes gpurun_out/mse_equal_time.json.
 
@@ -31,7 +33,7 @@ CROPS = {1: None, 2: None, 3: 32, 4: 128, 5: 32}
 
 def _render(dts, torch, c, spp, seed):
     sc = dts.Scene(c)
-    if c["strategy"] == "darts":
+    if c["strategy"] != "vanilla":
         sc.table_build()
     h = torch.zeros(sc.hist_shape(), dtype=torch.float32, device="cuda")
     ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
@@ -46,41 +48,53 @@ def _render(dts, torch, c, spp, seed):
     return h.double(), ms, dts.counters_dict(ctr)
 
 
-def run_config(dts, torch, idx, mode, reps, ref_mult):
+def run_config(dts, torch, idx, mode, nreps, ref_mult, strategies):
     c = I.as_f32(I.config(idx, direction_mode=mode))
     if CROPS[idx]:
         c = I.crop_center(c, CROPS[idx], CROPS[idx])
     spp = c["spp"]
-    # reference: ref_mult x spp, rendered in chunks of spp with distinct seeds
+    # reference: DARTS in the config's own direction mode (SPLIT for the
+    # strongly forward configs 3 and 5, R29) at ref_mult x spp, rendered in
+    # chunks of spp with distinct seeds
+    cref = dict(c, direction_mode=I.config(idx)["direction_mode"])
     ref = None
     for k in range(ref_mult):
-        h, _, _ = _render(dts, torch, c, spp, 10_000 + k)
+        h, _, _ = _render(dts, torch, cref, spp, 10_000 + k)
         ref = h if ref is None else ref + h
     ref /= ref_mult
-    out = {"config": idx, "mode": mode, "crop": c["crop"], "spp": spp, "ref_mult": ref_mult, "reps": []}
-    cv = dict(c, strategy="vanilla")
-    # vanilla spp per pixel: start at the DARTS paths per pixel, calibrate on time
-    paths_px = spp * (c["n_bins"] if c["spp_mode"] == "cell" else 1)
+    out = {"config": idx, "mode": mode, "crop": c["crop"], "spp": spp, "ref_mult": ref_mult, "strategies": {}}
+    # equal time: every strategy's spp is calibrated so that its render takes
+    # about as long as DARTS at the config's spp
     _, ms_d0, _ = _render(dts, torch, c, spp, 1)
-    _, ms_v0, _ = _render(dts, torch, cv, paths_px, 2)
-    spp_v = max(1, int(round(paths_px * ms_d0 / max(ms_v0, 1e-3))))
-    for r in range(reps):
-        hd, ms_d, cd = _render(dts, torch, c, spp, 100 + r)
-        hv, ms_v, cvv = _render(dts, torch, cv, spp_v, 200 + r)
-        mse_d = float(((hd - ref) ** 2).mean())
-        mse_v = float(((hv - ref) ** 2).mean())
-        out["reps"].append({"ms_darts": ms_d, "ms_vanilla": ms_v, "mse_darts": mse_d, "mse_vanilla": mse_v,
-                            "vertices_darts": cd["vertices"], "vertices_vanilla": cvv["vertices"]})
-    ms_d = np.mean([x["ms_darts"] for x in out["reps"]])
-    ms_v = np.mean([x["ms_vanilla"] for x in out["reps"]])
-    md = np.mean([x["mse_darts"] for x in out["reps"]])
-    mv = np.mean([x["mse_vanilla"] for x in out["reps"]])
-    out.update({"spp_vanilla_per_pixel": spp_v, "ms_darts": ms_d, "ms_vanilla": ms_v, "mse_darts": md,
-                "mse_vanilla": mv, "mse_ratio_vanilla_over_darts": mv / md if md > 0 else None,
-                "equal_time_mse_ratio": (mv * ms_v) / (md * ms_d) if md > 0 else None,
-                "ref_signal_ms": float((ref ** 2).mean())})
-    print(f"cfg{idx}/{mode}: DARTS {ms_d:.1f} ms MSE {md:.3e} | vanilla spp {spp_v} {ms_v:.1f} ms MSE {mv:.3e} "
-          f"| ratio {out['mse_ratio_vanilla_over_darts']:.2f} (time-adjusted {out['equal_time_mse_ratio']:.2f})",
+    paths_px = spp * (c["n_bins"] if c["spp_mode"] == "cell" else 1)
+    for strat in strategies:
+        if strat == "vanilla":
+            cs = dict(c, strategy="vanilla")
+            s0 = paths_px
+        elif strat == "uniform_s":
+            cs = dict(c, conn_sampling="uniform")
+            s0 = spp
+        else:
+            cs = dict(c, strategy=strat)
+            s0 = spp
+        if strat == "darts":
+            sk = spp
+        else:
+            _, ms0, _ = _render(dts, torch, cs, s0, 2)
+            sk = max(1, int(round(s0 * ms_d0 / max(ms0, 1e-3))))
+        reps = []
+        for r in range(nreps):
+            h, ms, cnt = _render(dts, torch, cs, sk, 100 + r)
+            reps.append({"ms": ms, "mse": float(((h - ref) ** 2).mean()), "vertices": cnt["vertices"]})
+        ms = float(np.mean([x["ms"] for x in reps]))
+        mse = float(np.mean([x["mse"] for x in reps]))
+        out["strategies"][strat] = {"spp": sk, "ms": ms, "mse": mse, "mse_x_ms": mse * ms, "reps": reps}
+    base = out["strategies"]["darts"]["mse_x_ms"]
+    for strat, v in out["strategies"].items():
+        v["rel_mse_time_adjusted"] = v["mse_x_ms"] / base if base > 0 else None
+    out["ref_signal_ms"] = float((ref ** 2).mean())
+    print(f"cfg{idx}/{mode}: " + " | ".join(f"{k} spp {v['spp']} {v['ms']:.1f} ms MSE {v['mse']:.3e} "
+                                          f"(x{v['rel_mse_time_adjusted']:.2f})" for k, v in out["strategies"].items()),
           flush=True)
     return out
 
@@ -90,6 +104,8 @@ def main():
     ap.add_argument("--configs", type=int, nargs="+", default=[1, 2, 3, 4, 5])
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--ref-mult", type=int, default=64)
+    ap.add_argument("--strategies", nargs="+", default=["darts", "da_only", "eda_only", "uniform_s", "vanilla"],
+                    help="darts first; MSE is reported relative to it at equal time (PAPER.md:433)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "mse_equal_time.json"))
     args = ap.parse_args()
     import torch
@@ -99,7 +115,7 @@ def main():
     for idx in args.configs:
         modes = ["reuse", "split"] if idx in (3, 5) else [I.config(idx)["direction_mode"]]
         for m in modes:
-            res.append(run_config(dts, torch, idx, m, args.reps, args.ref_mult))
+            res.append(run_config(dts, torch, idx, m, args.reps, args.ref_mult, args.strategies))
             os.makedirs(os.path.dirname(args.out), exist_ok=True)
             with open(args.out, "w") as f:
                 json.dump(res, f, indent=1)

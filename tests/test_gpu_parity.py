@@ -32,7 +32,7 @@ def dts():
 
 def _scene(dts, c):
     sc = dts.Scene(c)
-    if c["strategy"] == "darts":
+    if c["strategy"] != "vanilla":
         sc.table_build()
     return sc
 
@@ -57,10 +57,17 @@ def _rel(a, b, floor):
     return np.abs(a - b) / np.maximum(np.abs(b), floor)
 
 
-@pytest.mark.parametrize("cfg,mode", [(1, "reuse"), (2, "reuse"), (3, "split"), (3, "reuse"), (4, "reuse"),
-                                      (5, "split")])
-def test_sample_debug_parity(dts, oracle, cfg, mode):
-    c = I.as_f32(I.config(cfg, direction_mode=mode))
+DEBUG_CASES = [(1, "reuse", {}), (2, "reuse", {}), (3, "split", {}), (3, "reuse", {}), (4, "reuse", {}),
+               (5, "split", {}),
+               # ablations and uniform-S elliptical sampling
+               (2, "reuse", {"strategy": "da_only"}), (4, "reuse", {"strategy": "eda_only"}),
+               (5, "split", {"strategy": "eda_only"}), (3, "split", {"conn_sampling": "uniform"})]
+
+
+@pytest.mark.parametrize("cfg,mode,extra", DEBUG_CASES,
+                         ids=[f"cfg{a}-{b}" + "".join(f"-{v}" for v in c.values()) for a, b, c in DEBUG_CASES])
+def test_sample_debug_parity(dts, oracle, cfg, mode, extra):
+    c = I.as_f32(I.config(cfg, direction_mode=mode, **extra))
     sc = _scene(dts, c)
     n = 100_000
     recs = I.debug_records(c, n, seed=100 + cfg)
@@ -150,6 +157,10 @@ SAME_KEY = [
     ("cfg4_full", lambda: I.config(4, spp=16), None),
     ("cfg5_small_pixelmode", lambda: I.small(I.config(5), 7, 9, n_bins=120, t1=12.0), 150),
     ("cfg3_reuse", lambda: I.small(I.config(3, direction_mode="reuse"), 4, 4, n_bins=32, t1=6.0), 16),
+    ("cfg4_da_only", lambda: I.config(4, spp=16, strategy="da_only"), None),
+    ("cfg4_eda_only", lambda: I.config(4, spp=16, strategy="eda_only"), None),
+    ("cfg3_small_uniform_s", lambda: I.small(I.config(3, conn_sampling="uniform"), 6, 5, n_bins=64, t1=8.5), 8),
+    ("cfg5_small_da_only", lambda: I.small(I.config(5, strategy="da_only"), 7, 9, n_bins=120, t1=12.0), 150),
     ("cfg1_vanilla", lambda: I.config(1, strategy="vanilla"), 4096),
     ("cfg4_vanilla", lambda: I.small(I.config(4, strategy="vanilla"), 16, 16), 256),
 ]
@@ -160,7 +171,7 @@ def _same_key(dts, oracle, c, spp, seed):
     h, _, ctr = dts.render_to_tensor(sc, spp, seed)
     torch.cuda.synchronize()
     g = h.cpu().numpy().astype(np.float64)
-    q = oracle.build_table(c)[0] if c["strategy"] == "darts" else None
+    q = oracle.build_table(c)[0] if c["strategy"] != "vanilla" else None
     o = oracle.render(c, q, spp, seed, sq=False)
     return g, o, dts.counters_dict(ctr)
 
