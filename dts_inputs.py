@@ -82,7 +82,7 @@ _DEFAULTS = dict(
     wall_mask=0, wall_albedo=(0.0,) * 6, look_at=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0),
     fov_y_deg=45.0, det_radius=0.0, strategy="darts", n_ris=8, alpha=0.5,
     parity_r_excl=0.0, parity_s_excess=0.0, table_nr=16, table_ns=16,
-    crop=None, table_smin=None, table_smax=None,
+    crop=None, table_smin=None, table_smax=None, response=None,
     conn_sampling="exp",   # "exp": truncated exponential P of S; "uniform": ablation
 )
 
@@ -126,6 +126,31 @@ def crop_center(c: dict, w: int, h: int) -> dict:
     y0 = (c["height"] - h) // 2
     out["crop"] = (x0, y0, x0 + w, y0 + h)
     return out
+
+
+def two_peak_response(n_bins: int, t0: float, t1: float, peaks=((5.0, 0.15, 1.0), (7.0, 0.15, 0.6)),
+                      floor: float = 1e-3) -> np.ndarray:
+    """A two-peak sensor response W(t) (the setting of PAPER.md:302-310, Fig. 6:
+    "the temporal response weight comprises two peaks"), tabulated at the bin
+    centres as a sum of Gaussians (centre, sigma, height), zeroed where it is
+    below floor x its maximum so that it has exact zeros between the peaks.
+    Rounded to float32 (what the device sees)."""
+    tc = t0 + (np.arange(n_bins) + 0.5) * (t1 - t0) / n_bins
+    w = np.zeros(n_bins)
+    for mu, sg, h in peaks:
+        w += h * np.exp(-0.5 * ((tc - mu) / sg) ** 2)
+    w[w < floor * w.max()] = 0.0
+    return w.astype(np.float32).astype(np.float64)
+
+
+def response_config(**overrides) -> dict:
+    """The rejection experiment: config 4's cube with walls and
+    two emitters, a 3..9 time window of 120 bins and the two-peak W; spp paths
+    per pixel, each drawing its bin with probability ~ W (R31)."""
+    c = config(4, t0=3.0, t1=9.0, n_bins=120, spp=64, spp_mode="response", name="cfg4_two_peak_response")
+    c.update(overrides)
+    c["response"] = two_peak_response(c["n_bins"], c["t0"], c["t1"])
+    return c
 
 
 def small(c: dict, width: int, height: int, n_bins: int | None = None, t1: float | None = None) -> dict:

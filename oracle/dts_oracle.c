@@ -388,6 +388,7 @@ typedef struct {
   /* per path */
   double Rm, RM, xe[3], Pe;
   int Ne;
+  int bin; /* the path's time bin */
 } pstate;
 
 static double uu(const uint32_t r[12], int i) { return or_uniform(r[i]); }
@@ -683,6 +684,12 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
   double c = connect(sc, dv, ps, wc, wconn, clo, chi, hitc, uu(r, 7), dbg, &nonempty);
   *contrib += c;
   if (st && nonempty) st->conn_nonempty++;
+  /* every connection lands in the path's own bin (exact length control): a
+   * path sample is rejected only if W is zero there */
+  if (st && c != 0.0) {
+    st->samples++;
+    if (sc->spp_mode == OR_SPP_RESPONSE && sc->response[ps->bin] == 0.0) st->rejected++;
+  }
 
   /* ---- step 1 (next vertex): DA distance sampling by RIS ---- */
   if (hit == OR_HIT_MISS) {
@@ -814,6 +821,7 @@ void or_debug(const or_scene* sc, const uint16_t* q, int n, const or_debug_in* i
     memcpy(ps.xe, sc->em_pos[e], sizeof ps.xe);
     ps.Pe = sc->em_energy[e];
     ps.Ne = sc->n_emitters;
+    ps.bin = in[i].bin;
     double c;
     darts_vertex(sc, &dv, q, &ps, in[i].r, &c, &out[i], NULL);
   }
@@ -883,6 +891,34 @@ static uint64_t cell_count(const or_scene* sc, uint64_t spp, int o_p, int b) {
   return spp / B + (rel < spp % B ? 1 : 0);
 }
 
+/* R31: the sensor response W (piecewise constant over the bins) is importance
+ * sampled: a path's bin is b with probability pi_b = (c_{b+1} - c_b) / 2^23,
+ * c_k = round(2^23 sum_{j<k} W_j / sum_j W_j) (sums in bin order), picked by the
+ * 23-bit integer m of its start uniform as the b with c_b <= m < c_{b+1}; its
+ * contribution is weighted by W_b / pi_b ("sample one time interval per path",
+ * PAPER.md:258; rejection-free length control). */
+static void response_cdf(const or_scene* sc, uint32_t* cdf) {
+  double tot = 0.0;
+  for (int b = 0; b < sc->n_bins; ++b) tot += sc->response[b];
+  double acc = 0.0;
+  cdf[0] = 0u;
+  for (int b = 0; b < sc->n_bins; ++b) {
+    acc += sc->response[b];
+    cdf[b + 1] = (uint32_t)floor(8388608.0 * acc / tot + 0.5);
+  }
+  cdf[sc->n_bins] = 8388608u;
+}
+
+static int response_bin(const or_scene* sc, const uint32_t* cdf, uint32_t m, double* weight) {
+  int b = 0;
+  for (int k = 0; k < sc->n_bins; ++k)
+    if (cdf[k] <= m) b = k;
+  /* a bin with pi_b = 0 cannot be reached: c_b <= m < c_{b+1} needs c_{b+1} > c_b */
+  double pi = (double)(cdf[b + 1] - cdf[b]) / 8388608.0;
+  *weight = sc->response[b] / pi;
+  return b;
+}
+
 /* One DARTS path; returns acc (sum of its contributions). */
 static double darts_path(const or_scene* sc, const derived* dv, const uint16_t* q, uint64_t seed,
                          uint64_t id, int px, int py, int b, double* order_acc, int n_orders,
@@ -897,6 +933,7 @@ static double darts_path(const or_scene* sc, const derived* dv, const uint16_t* 
   memcpy(ps.xe, sc->em_pos[e], sizeof ps.xe);
   ps.Pe = sc->em_energy[e];
   ps.Ne = sc->n_emitters;
+  ps.bin = b;
   if (st) st->paths++;
   if (nvert) *nvert = 0;
   /* camera ray must meet the medium */
@@ -1031,12 +1068,18 @@ static void vanilla_path(const or_scene* sc, const derived* dv, uint64_t seed, u
     }
     c *= exp(-dv->sigma_t * len) * vis * Pe / (4.0 * OR_PI) * Ne / (C * C);
     if (sc->parity_r_excl > 0.0 && C < sc->parity_r_excl) c = 0.0;
-    if (arrive >= sc->t0 && c != 0.0 && isfinite(c)) {
-      int bin = (int)floor((arrive - sc->t0) / dt);
-      if (bin >= 0 && bin < sc->n_bins) {
-        hrow[bin] += c * inv_spp;
-        if (path_bins) path_bins[bin] += c;
-        if (order_rows && k < n_orders) order_rows[(size_t)k * cells + cell0 + bin] += c * inv_spp;
+    if (c != 0.0 && isfinite(c)) {
+      int bin = arrive >= sc->t0 ? (int)floor((arrive - sc->t0) / dt) : -1;
+      double wgt = 1.0;
+      if (bin >= 0 && bin < sc->n_bins && sc->spp_mode == OR_SPP_RESPONSE) wgt = sc->response[bin];
+      if (st) {
+        st->samples++;
+        if (!(bin >= 0 && bin < sc->n_bins) || wgt == 0.0) st->rejected++; /* W = 0 at its time */
+      }
+      if (bin >= 0 && bin < sc->n_bins && wgt != 0.0) {
+        hrow[bin] += wgt * c * inv_spp;
+        if (path_bins) path_bins[bin] += wgt * c;
+        if (order_rows && k < n_orders) order_rows[(size_t)k * cells + cell0 + bin] += wgt * c * inv_spp;
       }
     }
   }
@@ -1098,21 +1141,39 @@ static void* render_worker(void* arg) {
     }
   } else {
     uint64_t total = npix_local * ns;
+    uint32_t* cdf = NULL;
+    if (sc->spp_mode == OR_SPP_RESPONSE) {
+      cdf = (uint32_t*)malloc(sizeof(uint32_t) * (B + 1));
+      response_cdf(sc, cdf);
+    }
     for (uint64_t i = (uint64_t)jb->tid; i < total; i += (uint64_t)jb->nthreads) {
       uint64_t pl = i % npix_local, s = jb->s_begin + i / npix_local;
       int px = sc->crop[0] + (int)(pl % cw), py = sc->crop[1] + (int)(pl / cw);
       uint64_t p = (uint64_t)py * sc->width + px;
-      int op = pixel_offset(sc, jb->seed, p);
-      int b = (int)((s + (uint64_t)op) % B);
       uint64_t id = s * Npix + p;
+      /* the cell's estimate is the mean over its n samples of X = scale * acc */
+      int op = 0, b;
+      double inv_n, scale = 1.0;
+      if (cdf) {
+        uint32_t a[4];
+        draw4(jb->seed, id, 0xFFFFFFFFu, 0, a); /* R24: a[3] of the path-start draw */
+        b = response_bin(sc, cdf, a[3] >> 9, &scale);
+        inv_n = 1.0 / (double)jb->spp; /* every path of the pixel is a sample of every cell (X = 0 off its bin) */
+      } else {
+        op = pixel_offset(sc, jb->seed, p);
+        b = (int)((s + (uint64_t)op) % B);
+        inv_n = 1.0 / (double)cell_count(sc, jb->spp, op, b);
+      }
       if (oacc) memset(oacc, 0, sizeof(double) * jb->n_orders);
-      double acc = darts_path(sc, &dv, jb->q, jb->seed, id, px, py, b, oacc, jb->n_orders, &jb->st, NULL);
-      double inv_n = 1.0 / (double)cell_count(sc, jb->spp, op, b);
+      double acc = scale * darts_path(sc, &dv, jb->q, jb->seed, id, px, py, b, oacc, jb->n_orders, &jb->st, NULL);
+      if (oacc)
+        for (int k = 0; k < jb->n_orders; ++k) oacc[k] *= scale;
       jb->hist[pl * B + b] += acc * inv_n;
       if (jb->hist_sq) jb->hist_sq[pl * B + b] += acc * acc * inv_n;
       if (oacc)
         for (int k = 0; k < jb->n_orders; ++k) jb->order_hist[(size_t)k * cells + pl * B + b] += oacc[k] * inv_n;
     }
+    free(cdf);
   }
   free(oacc);
   return NULL;
@@ -1123,6 +1184,7 @@ int or_render(const or_scene* sc, const uint16_t* q, uint64_t spp, uint64_t seed
               or_stats* stats, int nthreads) {
   if (!hist || s_end < s_begin) return -1;
   if ((sc->strategy == OR_STRATEGY_DARTS || sc->strategy == OR_STRATEGY_EDA_ONLY) && !q) return -2;
+  if (sc->spp_mode == OR_SPP_RESPONSE && !sc->response) return -3;
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   int cw = sc->crop[2] - sc->crop[0], ch = sc->crop[3] - sc->crop[1];
@@ -1150,6 +1212,7 @@ int or_render(const or_scene* sc, const uint16_t* q, uint64_t spp, uint64_t seed
       stats->ris_all_invalid += jb->st.ris_all_invalid; stats->early_exit += jb->st.early_exit;
       stats->escapes += jb->st.escapes; stats->cap_hits += jb->st.cap_hits;
       stats->nonfinite += jb->st.nonfinite; stats->wall_nee += jb->st.wall_nee;
+      stats->samples += jb->st.samples; stats->rejected += jb->st.rejected;
     }
     free(jb->hist); free(jb->hist_sq); free(jb->order_hist);
   }
@@ -1170,6 +1233,14 @@ int or_render_ids(const or_scene* sc, const uint16_t* q, uint64_t spp, uint64_t 
     if (sc->spp_mode == OR_SPP_PER_CELL) {
       b = (int)(id % B);
       p = (id / B) % Npix;
+    } else if (sc->spp_mode == OR_SPP_RESPONSE) {
+      p = id % Npix;
+      uint32_t cdf_local[4097], a[4];
+      if (B > 4096) return -1;
+      response_cdf(sc, cdf_local);
+      draw4(seed, id, 0xFFFFFFFFu, 0, a);
+      double wgt;
+      b = response_bin(sc, cdf_local, a[3] >> 9, &wgt);
     } else {
       p = id % Npix;
       uint64_t s = id / Npix;

@@ -28,7 +28,10 @@ enum { OR_STRATEGY_DARTS = 0, OR_STRATEGY_VANILLA = 1, OR_STRATEGY_DA_ONLY = 2, 
 /* distribution P of S in the elliptical sampling of E21 */
 enum { OR_CONN_TRUNC_EXP = 0, OR_CONN_UNIFORM_S = 1 };
 enum { OR_DIR_REUSE = 0, OR_DIR_SPLIT = 1 };
-enum { OR_SPP_PER_CELL = 0, OR_SPP_PER_PIXEL = 1 };
+/* PER_CELL: spp paths per (pixel, bin) cell; PER_PIXEL: spp paths per pixel,
+ * bin by a per-pixel offset (R21); RESPONSE: spp paths per pixel, bin drawn
+ * with probability ~ the sensor response W (R31). */
+enum { OR_SPP_PER_CELL = 0, OR_SPP_PER_PIXEL = 1, OR_SPP_RESPONSE = 2 };
 enum { OR_KIND_CAMERA = 0, OR_KIND_MEDIUM = 1, OR_KIND_WALL = 2 };
 enum { OR_HIT_NONE = 0, OR_HIT_OPEN = 1, OR_HIT_WALL = 2, OR_HIT_MISS = 3 };
 
@@ -54,6 +57,7 @@ typedef struct {
   int32_t table_nr, table_ns;
   double table_smin, table_smax;
   int32_t conn_sampling; /* OR_CONN_* */
+  const double* response; /* RESPONSE: W per bin (n_bins values >= 0), else NULL */
 } or_scene;
 
 /* 16-bit quantised per-cell CDF of the EDA direction table (R8-R10):
@@ -91,6 +95,9 @@ typedef struct {
 typedef struct {
   uint64_t paths, camera_miss, vertices, conn_nonempty, ris_all_invalid,
       early_exit, escapes, cap_hits, nonfinite, wall_nee;
+  /* path samples (non-zero connection contributions before W) and those
+   * rejected because W is zero at their recorded time (Fig. 6) */
+  uint64_t samples, rejected;
 } or_stats;
 
 void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

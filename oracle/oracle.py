@@ -71,13 +71,14 @@ class OrScene(ctypes.Structure):
         ("table_nr", ctypes.c_int32), ("table_ns", ctypes.c_int32),
         ("table_smin", ctypes.c_double), ("table_smax", ctypes.c_double),
         ("conn_sampling", ctypes.c_int32),
+        ("response", ctypes.c_void_p),
     ]
 
 
 class OrStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "paths", "camera_miss", "vertices", "conn_nonempty", "ris_all_invalid",
-        "early_exit", "escapes", "cap_hits", "nonfinite", "wall_nee")]
+        "early_exit", "escapes", "cap_hits", "nonfinite", "wall_nee", "samples", "rejected")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -112,7 +113,7 @@ _CAM = {"pinhole": 0, "detector": 1}
 _STRAT = {"darts": 0, "vanilla": 1, "da_only": 2, "eda_only": 3}
 _CONN = {"exp": 0, "uniform": 1}
 _DIR = {"reuse": 0, "split": 1}
-_SPP = {"cell": 0, "pixel": 1}
+_SPP = {"cell": 0, "pixel": 1, "response": 2}
 
 
 def scene(c: dict) -> OrScene:
@@ -150,6 +151,11 @@ def scene(c: dict) -> OrScene:
     s.table_nr, s.table_ns = c["table_nr"], c["table_ns"]
     s.table_smin, s.table_smax = c["table_smin"], c["table_smax"]
     s.conn_sampling = _CONN[c.get("conn_sampling", "exp")]
+    if c.get("response") is not None:
+        w = np.ascontiguousarray(np.asarray(c["response"], dtype=np.float64))
+        assert w.shape == (c["n_bins"],)
+        s._response_keepalive = w
+        s.response = w.ctypes.data
     return s
 
 

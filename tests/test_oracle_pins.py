@@ -618,6 +618,68 @@ def test_uniform_s_connection_pdf(oracle):
     np.testing.assert_allclose(o["p_t"] * dtdu, 1.0, rtol=2e-5)
 
 
+# ---------------------------------------------------------------- sensor response W(t)
+def _resp_cfg(**kw):
+    c = I.small(I.as_f32(I.response_config(**kw)), 2, 2)
+    c["response"] = I.two_peak_response(c["n_bins"], c["t0"], c["t1"])
+    return c
+
+
+def test_response_bins_follow_w(oracle):
+    """R31: a path's bin is drawn with probability pi_b ~ W_b (PAPER.md:258
+    "a time interval will be sampled"); bins where W = 0 are never drawn and
+    pi_b = W_b / sum W to 2^-23."""
+    c = _resp_cfg()
+    w = np.asarray(c["response"])
+    q, _ = oracle.build_table(c)
+    ids = np.arange(200_000, dtype=np.uint64) * np.uint64(c["width"] * c["height"])   # pixel 0, s = 0..
+    cdf = np.floor(2**23 * np.cumsum(w) / w.sum() + 0.5)
+    cdf[-1] = 2**23
+    cdf = np.concatenate([[0.0], cdf])
+    pi = np.diff(cdf) / 2**23
+    np.testing.assert_allclose(pi, w / w.sum(), atol=2**-23)
+    bins = []
+    for i in ids[:20000]:
+        a = oracle.philox([int(i) & 0xFFFFFFFF, int(i) >> 32, 0xFFFFFFFF, 0], [c["seed"], 0])
+        m = a[3] >> 9
+        bins.append(int(np.searchsorted(cdf, m, side="right") - 1))
+    bins = np.array(bins)
+    assert (w[bins] > 0).all()
+    cnt = np.bincount(bins, minlength=len(w))
+    nz = pi > 0
+    exp_ = pi[nz] * len(bins)
+    chi2 = ((cnt[nz] - exp_) ** 2 / exp_).sum()
+    from scipy.stats import chi2 as chi2d
+    assert chi2d.sf(chi2, nz.sum() - 1) > 0.001
+
+
+def test_response_darts_equals_vanilla_and_rejection(oracle):
+    """Importance-sampling the sensor response: DARTS, with
+    its bin drawn ~ W and weighted W_b / pi_b, and vanilla, weighting each
+    connection by W at its arrival time, estimate the same image sum_b W_b H;
+    vanilla rejects most path samples (W = 0 at their time; the paper's
+    85.31 %), DARTS none (the paper's < 3 %)."""
+    c = _resp_cfg(parity_r_excl=0.3, parity_s_excess=0.05)
+    q, _ = oracle.build_table(c)
+    td, tv = [], []
+    rej_d = smp_d = rej_v = smp_v = 0
+    for s in range(6):
+        d = oracle.render(c, q, 20000, 300 + s, sq=False)
+        td.append(d["hist"].sum(axis=-1).ravel())
+        rej_d += d["stats"]["rejected"]
+        smp_d += d["stats"]["samples"]
+    for s in range(3):
+        v = oracle.render(dict(c, strategy="vanilla"), None, 300000, 400 + s, sq=False)
+        tv.append(v["hist"].sum(axis=-1).ravel())
+        rej_v += v["stats"]["rejected"]
+        smp_v += v["stats"]["samples"]
+    td, tv = np.array(td), np.array(tv)
+    z = (td.mean(0) - tv.mean(0)) / np.sqrt(td.var(0, ddof=1) / len(td) + tv.var(0, ddof=1) / len(tv))
+    assert (np.abs(z) < 3).all(), z
+    assert smp_d > 1000 and rej_d == 0
+    assert rej_v / smp_v > 0.5, rej_v / smp_v
+
+
 # ---------------------------------------------------------------- causality and determinism
 def test_causality_zero_bins(oracle):
     """Bins before the minimal arrival are exactly zero: config 2
