@@ -67,7 +67,12 @@ enum { DTS_STRATEGY_DARTS = 0, DTS_STRATEGY_VANILLA = 1, DTS_STRATEGY_DA_ONLY = 
  * paper's truncated exponential, or uniform (the Jarabo et al. variant). */
 enum { DTS_CONN_TRUNC_EXP = 0, DTS_CONN_UNIFORM_S = 1 };
 enum { DTS_DIR_REUSE = 0, DTS_DIR_SPLIT = 1 };     /* R29 */
-enum { DTS_SPP_PER_CELL = 0, DTS_SPP_PER_PIXEL = 1 }; /* R21 */
+/* PER_CELL: spp paths per (pixel, bin) cell; PER_PIXEL: spp paths per pixel,
+ * bin by a per-pixel Philox offset (R21); RESPONSE: spp paths per pixel, bin
+ * drawn with probability ~ the sensor response W of dts_set_response and the
+ * contribution weighted by W_b / pi_b, so cell (p, b) estimates W_b H[p, b]
+ * and the sum over b the W-weighted image (R31). */
+enum { DTS_SPP_PER_CELL = 0, DTS_SPP_PER_PIXEL = 1, DTS_SPP_RESPONSE = 2 };
 
 /* Scene description.  Validation (dts_scene_create): sigma_s > 0, sigma_a >= 0,
  * -1 < g < 1; 1 <= n_emitters <= 8; width, height >= 1; crop
@@ -160,6 +165,8 @@ enum {
   DTS_CTR_CAP_HITS,        /* walks truncated at max_bounces */
   DTS_CTR_NONFINITE,       /* paths discarded for a non-finite contribution */
   DTS_CTR_WALL_NEE,        /* non-zero wall NEE contributions */
+  DTS_CTR_SAMPLES,         /* path samples: non-zero connection / NEE contributions before W */
+  DTS_CTR_REJECTED,        /* path samples whose recorded time has W = 0 (Fig. 6) */
   DTS_NUM_COUNTERS
 };
 
@@ -178,6 +185,14 @@ dts_status dts_table_build(dts_scene_t scene, const dts_table_desc* desc, void* 
 dts_status dts_table_export(dts_scene_t scene, uint16_t* host_q, size_t n);
 /* Number of table entries (0 before dts_table_build). */
 size_t dts_table_size(dts_scene_t scene);
+
+/* Sets the sensor response W(t) of DTS_SPP_RESPONSE scenes: h_w (host, n =
+ * n_bins floats, finite, >= 0, not all zero) is W on each bin (piecewise
+ * constant).  Copied; the bin CDF of R31 is built on the host in double
+ * (c_k = round(2^23 sum_{j<k} W_j / sum W)).  Synchronous.  A RESPONSE render
+ * without it fails with DTS_E_STATE.  VANILLA scenes weight each connection
+ * by W at its arrival time. */
+dts_status dts_set_response(dts_scene_t scene, const float* h_w, int32_t n);
 
 /* Number of histogram cells: crop_w * crop_h * n_bins, layout [y][x][bin]
  * (bin fastest) over the crop. */

@@ -585,6 +585,10 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
                    exp(-dv->sigma_t * len) / (C * C);
       if (sc->parity_r_excl > 0.0 && C < sc->parity_r_excl) nee = 0.0;
       *contrib += nee;
+      if (st && nee != 0.0) {
+        st->samples++;
+        if (sc->spp_mode == OR_SPP_RESPONSE && sc->response[ps->bin] == 0.0) st->rejected++;
+      }
       if (dbg) dbg->nee = nee;
       if (st && nee > 0.0) st->wall_nee++;
     }

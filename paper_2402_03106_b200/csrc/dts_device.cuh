@@ -479,7 +479,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason,
                                              const Defer* df = nullptr, bool* pushed = nullptr,
-                                             RisReq* rq = nullptr) {
+                                             RisReq* rq = nullptr, uint32_t* nsamp = nullptr) {
   contrib = 0.0f;
   conn_nonempty = false;
   wall_nee = false;
@@ -514,6 +514,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       if (S.r_excl > 0.0f && C < S.r_excl) nee = 0.0f;
       contrib += nee;
       wall_nee = nee > 0.0f;
+      if (nsamp && nee != 0.0f) ++*nsamp;
     }
     if (DBG) dbg->nee = nee;
     // Lambertian: cosine hemisphere about n (1 - cos^2 = u5), beta *= albedo
@@ -703,6 +704,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       float r2;
       const float c = conn_contrib<SH, WALLS>(S, ps.x, wc, xe, ek, t, pt, pSt, clo, ps.beta * wconn, &xell, &r2);
       contrib += c;
+      if (nsamp && c != 0.0f) ++*nsamp;
       if (DBG) {
         dbg->S = (S.warped == 0 && ps.kind == KIND_CAMERA) ? t + r2 : Ssamp;
         dbg->t = t;
@@ -734,7 +736,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
         qq[10 * st] = __uint_as_float(df->cell);
         *pushed = true;
       } else {
-        contrib += conn_job_run<SH, FL>(S, ps.x, wc, job_dlo, job_width, coef, m7e);
+        const float c = conn_job_run<SH, FL>(S, ps.x, wc, job_dlo, job_width, coef, m7e);
+        contrib += c;
+        if (nsamp && c != 0.0f) ++*nsamp;
       }
     }
   }

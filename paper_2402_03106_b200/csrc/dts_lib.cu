@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/dts.h"
 #include "dts_device.cuh"
@@ -43,6 +44,9 @@ struct dts_scene {
   float* d_hist_host = nullptr;          // dts_render_host scratch
   size_t d_hist_host_n = 0;
   uint64_t* d_ctr_host = nullptr;
+  uint32_t* d_resp_cdf = nullptr;  // R31 bin CDF (n_bins + 1)
+  float* d_resp_wgt = nullptr;     // W_b / pi_b
+  float* d_resp_w = nullptr;       // W_b
   int num_sms = 0;
   int device = 0;
 };
@@ -176,6 +180,9 @@ struct RenderParams {
   uint32_t cw;       // crop width
   uint32_t table_u4; // table size in 16-byte words
   uint32_t spp_div_b, spp_mod_b;  // SPP_PER_PIXEL cell counts (R21)
+  const uint32_t* resp_cdf;       // SPP_RESPONSE: bin CDF c_0..c_B (R31)
+  const float* resp_wgt;          // SPP_RESPONSE: W_b / pi_b
+  const float* resp_w;            // W_b (vanilla weighting; null = rectangle)
   uint32_t priv_cells;            // > 0: the CTA privatises the whole histogram in shared memory
   uint32_t defer;                 // 1: connections are queued per warp and evaluated in batches
   uint32_t flush_at;              // queue length that triggers a batch
@@ -243,8 +250,23 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   }
   const uint32_t px = (uint32_t)S.crop[0] + pl % P.cw, py = (uint32_t)S.crop[1] + pl / P.cw;
   const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
+  float scale = 1.0f;
   if (S.spp_mode == DTS_SPP_PER_CELL) {
     id = (s * Npix + p) * (uint64_t)B + b;
+  } else if (S.spp_mode == DTS_SPP_RESPONSE) {
+    // R31: bin b with c_b <= m < c_{b+1} (m = 23 bits of the path-start draw's
+    // 4th word), weight W_b / pi_b; every path of the pixel samples each cell
+    id = s * Npix + p;
+    const u4 a0 = philox_rk((uint32_t)id, (uint32_t)(id >> 32), 0xFFFFFFFFu, 0u, S.rk);
+    const uint32_t m = a0.d >> 9;
+    int lo = 0, hi = (int)B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(P.resp_cdf + mid) <= m) lo = mid; else hi = mid - 1;
+    }
+    b = (uint32_t)lo;
+    scale = __ldg(P.resp_wgt + b);
+    inv_n = 1.0f / (float)P.spp;
   } else {
     // R21: bin = (s + o_p) mod B with a per-pixel Philox offset
     const u4 o = philox_rk((uint32_t)p, (uint32_t)(p >> 32), 0xFFFFFFFEu, 0u, S.rk);
@@ -288,6 +310,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     ps.w = mk(s2 * cp, s2 * sp, z2);
     ps.beta = 4.0f * kPi;
   }
+  ps.beta *= scale;
   ps.kind = KIND_CAMERA;
   ps.face = -1;
   ps.resM = S.t0 + (double)(b + 1) * S.dt - (double)S.em_t[e];  // R_M - E with E = 0
@@ -422,6 +445,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
   PathCtx pc;
   // per-lane event counters, summed over the warp at the end
   uint32_t c_paths = 0, c_vert = 0, c_conn = 0, c_ris = 0, c_early = 0, c_esc = 0, c_cap = 0, c_nf = 0, c_nee = 0;
+  uint32_t c_samp = 0;  // non-zero contributions (path samples); DARTS never rejects one (its bin has W > 0)
   uint32_t l_miss = 0, l_early = 0;  // start-time retirements
   uint32_t waste = 0;                // idle lane-iterations since the last refill
   // evaluates the queued jobs, one per lane, and splats them (cells differ per job)
@@ -434,6 +458,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
         ++c_nf;
         c = 0.0f;
       }
+      c_samp += c != 0.0f ? 1u : 0u;
     }
     const bool has = c != 0.0f;
     const unsigned m = __ballot_sync(FULL, has);
@@ -505,7 +530,8 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       df.cell = pc.cell;
       df.inv_n = pc.inv_n;
       alive = darts_vertex<false, SMEM, SH, FL>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
-                                                s_queue ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr);
+                                                s_queue ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr,
+                                                &c_samp);
     }
     if (kRisWarp) {
       // RIS layout B: the warp draws every pending medium event's distance
@@ -566,9 +592,11 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
     c_cap += __shfl_xor_sync(FULL, c_cap, o);
     c_nf += __shfl_xor_sync(FULL, c_nf, o);
     c_nee += __shfl_xor_sync(FULL, c_nee, o);
+    c_samp += __shfl_xor_sync(FULL, c_samp, o);
   }
   if (lane == 0 && P.counters) {
     unsigned long long* C = P.counters;
+    atomicAdd(C + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
     atomicAdd(C + DTS_CTR_PATHS, (unsigned long long)c_paths);
     atomicAdd(C + DTS_CTR_CAMERA_MISS, (unsigned long long)l_miss);
     atomicAdd(C + DTS_CTR_VERTICES, (unsigned long long)c_vert);
@@ -583,19 +611,24 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
 }
 
 // ============================================================== vanilla
-__device__ __forceinline__ void vanilla_splat(const RenderParams& P, uint32_t pl, double arrive, float c) {
+// splats a vanilla connection into the bin of its arrival time, weighted by
+// the sensor response W there (RESPONSE scenes); returns 1 for a path sample
+// rejected by W = 0 (outside the bins, or a zero of W), 0 if splatted
+__device__ __forceinline__ int vanilla_splat(const RenderParams& P, uint32_t pl, double arrive, float c) {
   const DevScene& S = P.S;
-  if (!(c != 0.0f) || !isfinite(c) || arrive < S.t0) return;
-  const int bin = (int)floor((arrive - S.t0) / S.dt);
-  if (bin < 0 || bin >= S.n_bins) return;
-  atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, c / (float)P.spp);
+  const int bin = arrive >= S.t0 ? (int)floor((arrive - S.t0) / S.dt) : -1;
+  if (bin < 0 || bin >= S.n_bins) return 1;
+  const float w = P.resp_w ? __ldg(P.resp_w + bin) : 1.0f;
+  if (w == 0.0f) return 1;
+  atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, w * c / (float)P.spp);
+  return 0;
 }
 
 template <int SH, bool WALLS>
 __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderParams P) {
   const DevScene& S = P.S;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint32_t c_paths = 0, c_miss = 0, c_vert = 0, c_early = 0, c_esc = 0, c_cap = 0;
+  uint32_t c_paths = 0, c_miss = 0, c_vert = 0, c_early = 0, c_esc = 0, c_cap = 0, c_samp = 0, c_rej = 0;
   for (uint64_t widx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; widx < P.total; widx += stride) {
     const uint32_t pl = (uint32_t)(widx % P.npix);
     const uint64_t s = P.s_begin + widx / P.npix;
@@ -706,7 +739,10 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
       }
       c *= segment_tr<SH, WALLS>(S, x, xe, C, we) * ek / (C * C);
       if (S.r_excl > 0.0f && C < S.r_excl) c = 0.0f;
-      vanilla_splat(P, pl, arrive, c);
+      if (c != 0.0f && isfinite(c)) {
+        ++c_samp;
+        c_rej += vanilla_splat(P, pl, arrive, c);
+      }
     }
     if (alive && k >= S.max_bounces) ++c_cap;
   }
@@ -718,6 +754,8 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     c_early += __shfl_xor_sync(0xffffffffu, c_early, o);
     c_esc += __shfl_xor_sync(0xffffffffu, c_esc, o);
     c_cap += __shfl_xor_sync(0xffffffffu, c_cap, o);
+    c_samp += __shfl_xor_sync(0xffffffffu, c_samp, o);
+    c_rej += __shfl_xor_sync(0xffffffffu, c_rej, o);
   }
   if ((threadIdx.x & 31) == 0 && P.counters) {
     atomicAdd(P.counters + DTS_CTR_PATHS, (unsigned long long)c_paths);
@@ -726,6 +764,8 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     atomicAdd(P.counters + DTS_CTR_EARLY_EXIT, (unsigned long long)c_early);
     atomicAdd(P.counters + DTS_CTR_ESCAPES, (unsigned long long)c_esc);
     atomicAdd(P.counters + DTS_CTR_CAP_HITS, (unsigned long long)c_cap);
+    atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
+    atomicAdd(P.counters + DTS_CTR_REJECTED, (unsigned long long)c_rej);
   }
 }
 
@@ -847,7 +887,7 @@ static dts_status validate(const dts_scene_desc& d) {
   if (!(d.alpha >= 0.0f)) return bad("alpha must be >= 0");
   if (d.max_bounces < 1 || d.max_bounces > 65536) return bad("max_bounces must be 1..65536");
   if (d.direction_mode != DTS_DIR_REUSE && d.direction_mode != DTS_DIR_SPLIT) return bad("unknown direction_mode");
-  if (d.spp_mode != DTS_SPP_PER_CELL && d.spp_mode != DTS_SPP_PER_PIXEL) return bad("unknown spp_mode");
+  if (d.spp_mode < DTS_SPP_PER_CELL || d.spp_mode > DTS_SPP_RESPONSE) return bad("unknown spp_mode");
   if (!(d.parity_r_excl >= 0.0f) || !(d.parity_s_excess >= 0.0f)) return bad("parity restrictions must be >= 0");
   return DTS_OK;
 }
@@ -971,6 +1011,9 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaFree(s->d_work);
   cudaFree(s->d_hist_host);
   cudaFree(s->d_ctr_host);
+  cudaFree(s->d_resp_cdf);
+  cudaFree(s->d_resp_wgt);
+  cudaFree(s->d_resp_w);
   delete s;
   return DTS_OK;
 }
@@ -1021,6 +1064,41 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
   return DTS_OK;
 }
 
+dts_status dts_set_response(dts_scene_t s, const float* h_w, int32_t n) {
+  if (!s || !h_w) return fail(DTS_E_INVALID_ARG, "NULL argument");
+  if (n != s->desc.n_bins) return fail(DTS_E_INVALID_ARG, "n must equal n_bins");
+  double tot = 0.0;
+  for (int b = 0; b < n; ++b) {
+    if (!(h_w[b] >= 0.0f) || !std::isfinite(h_w[b])) return fail(DTS_E_INVALID_ARG, "W must be finite and >= 0");
+    tot += h_w[b];
+  }
+  if (!(tot > 0.0)) return fail(DTS_E_INVALID_ARG, "W must not be all zero");
+  // R31: c_k = round(2^23 sum_{j<k} W_j / sum W), sums in bin order, c_B = 2^23
+  std::vector<uint32_t> cdf(n + 1);
+  std::vector<float> wgt(n);
+  double acc = 0.0;
+  cdf[0] = 0u;
+  for (int b = 0; b < n; ++b) {
+    acc += h_w[b];
+    cdf[b + 1] = (uint32_t)std::floor(8388608.0 * acc / tot + 0.5);
+  }
+  cdf[n] = 8388608u;
+  for (int b = 0; b < n; ++b) {
+    const uint32_t dc = cdf[b + 1] - cdf[b];
+    wgt[b] = dc ? (float)((double)h_w[b] / ((double)dc / 8388608.0)) : 0.0f;
+  }
+  if (!s->d_resp_cdf) {
+    if (cudaMalloc(&s->d_resp_cdf, (n + 1) * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&s->d_resp_wgt, n * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&s->d_resp_w, n * sizeof(float)) != cudaSuccess)
+      return fail(DTS_E_OOM, "cudaMalloc(response) failed");
+  }
+  CUDA_TRY(cudaMemcpy(s->d_resp_cdf, cdf.data(), (n + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(s->d_resp_wgt, wgt.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(s->d_resp_w, h_w, n * sizeof(float), cudaMemcpyHostToDevice));
+  return DTS_OK;
+}
+
 size_t dts_table_size(dts_scene_t s) { return s ? s->table_n : 0; }
 
 dts_status dts_table_export(dts_scene_t s, uint16_t* host_q, size_t n) {
@@ -1054,8 +1132,15 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   // path ids must fit 64 bits: (s * Npix + p) * B + b
   const double idmax = ((double)spp * (double)Npix + (double)Npix) * (double)d.n_bins;
   if (idmax > 1.8e19) return fail(DTS_E_RANGE, "path id space exceeds 64 bits");
+  if (d.spp_mode == DTS_SPP_RESPONSE && !s->d_resp_cdf)
+    return fail(DTS_E_STATE, "dts_set_response must run before a RESPONSE render");
   RenderParams P;
   memset(&P, 0, sizeof P);
+  if (d.spp_mode == DTS_SPP_RESPONSE) {
+    P.resp_cdf = s->d_resp_cdf;
+    P.resp_wgt = s->d_resp_wgt;
+    P.resp_w = s->d_resp_w;
+  }
   P.S = s->S;
   set_round_keys(P.S, seed);
   P.tab = s->d_table;

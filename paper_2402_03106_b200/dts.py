@@ -23,9 +23,9 @@ _lib = ctypes.CDLL(LIB_PATH)
 # ----------------------------------------------------------------- ABI structs
 F3 = ctypes.c_float * 3
 MAX_EMITTERS = 8
-NUM_COUNTERS = 10
+NUM_COUNTERS = 12
 COUNTER_NAMES = ("paths", "camera_miss", "vertices", "conn_nonempty", "ris_invalid", "early_exit", "escapes",
-                 "cap_hits", "nonfinite", "wall_nee")
+                 "cap_hits", "nonfinite", "wall_nee", "samples", "rejected")
 
 
 class SceneDesc(ctypes.Structure):
@@ -88,12 +88,14 @@ _lib.dts_render.argtypes = [_VP, _U64, _U64, _U64, _U64, _VP, _VP, _VP, _VP]
 _lib.dts_render_host.argtypes = [_VP, _U64, _U64, _U64, _U64, _VP, _VP, _VP]
 _lib.dts_sample_debug.argtypes = [_VP, ctypes.c_int32, _VP, _VP, _VP]
 _lib.dts_last_launch.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 4
+_lib.dts_set_response.argtypes = [_VP, _VP, ctypes.c_int32]
 _lib.dts_status_string.restype = ctypes.c_char_p
 _lib.dts_status_string.argtypes = [ctypes.c_int]
 _lib.dts_last_error.restype = ctypes.c_char_p
 _lib.dts_abi_version.restype = ctypes.c_int32
 
-EXPORTED = ("dts_scene_create", "dts_scene_destroy", "dts_table_build", "dts_table_export", "dts_table_size",
+EXPORTED = ("dts_scene_create", "dts_scene_destroy", "dts_set_response", "dts_table_build", "dts_table_export",
+            "dts_table_size",
             "dts_hist_cells", "dts_render", "dts_render_host", "dts_sample_debug", "dts_last_launch",
             "dts_status_string", "dts_last_error", "dts_abi_version")
 
@@ -138,7 +140,7 @@ _CAM = {"pinhole": 0, "detector": 1}
 _STRAT = {"darts": 0, "vanilla": 1, "da_only": 2, "eda_only": 3}
 _CONN = {"exp": 0, "uniform": 1}
 _DIR = {"reuse": 0, "split": 1}
-_SPP = {"cell": 0, "pixel": 1}
+_SPP = {"cell": 0, "pixel": 1, "response": 2}
 
 
 def scene_desc(c: dict) -> SceneDesc:
@@ -187,6 +189,8 @@ class Scene:
         h = _VP()
         _check(_lib.dts_scene_create(ctypes.byref(self._desc), ctypes.byref(h)), "dts_scene_create")
         self.handle = h.value
+        if c.get("response") is not None:
+            self.set_response(c["response"])
 
     def close(self):
         if getattr(self, "handle", None):
@@ -213,6 +217,10 @@ class Scene:
                        s_min if s_min is not None else c.get("table_smin") or 0.0,
                        s_max if s_max is not None else c.get("table_smax") or 0.0)
         _check(_lib.dts_table_build(self.handle, ctypes.byref(td), _stream(stream)), "dts_table_build")
+
+    def set_response(self, w) -> None:
+        a = np.ascontiguousarray(np.asarray(w, dtype=np.float32))
+        _check(_lib.dts_set_response(self.handle, a.ctypes.data, a.size), "dts_set_response")
 
     def table_size(self) -> int:
         return int(_lib.dts_table_size(self.handle))

@@ -319,3 +319,52 @@ def test_single_pixel_single_bin_and_table_in_global_memory(dts, oracle):
     o = oracle.render(c, qo, 4096, 8, sq=False)["hist"]
     g = h.cpu().numpy()
     assert abs(g.sum() - o.sum()) <= 0.01 * o.sum()
+
+
+# ------------------------------------------------------------------ sensor response W(t)
+def _resp_small(**kw):
+    c = I.small(I.as_f32(I.response_config(**kw)), 12, 10)
+    c["response"] = I.two_peak_response(c["n_bins"], c["t0"], c["t1"])
+    return c
+
+
+@pytest.mark.parametrize("strategy,spp", [("darts", 256), ("vanilla", 4096)])
+def test_response_same_key_and_rejection(dts, oracle, strategy, spp):
+    """RESPONSE mode (R31) against the oracle on the same Philox keys, and the
+    path-sample rejection counters of PAPER.md:310 / Fig. 6: vanilla rejects
+    most samples (W = 0 at their time), DARTS none."""
+    c = dict(_resp_small(), strategy=strategy)
+    g, o, ctr = _same_key(dts, oracle, c, spp, 5)
+    ho = o["hist"]
+    rel = np.linalg.norm(g - ho) / np.linalg.norm(ho)
+    st = o["stats"]
+    print(f"response/{strategy}: same-key rel L2 {rel:.3e}; samples gpu {ctr['samples']} oracle {st['samples']}; "
+          f"rejected gpu {ctr['rejected']} ({ctr['rejected'] / max(1, ctr['samples']):.4f}) oracle {st['rejected']}")
+    assert rel <= 0.01
+    assert abs(ctr["samples"] - st["samples"]) <= 0.01 * st["samples"]
+    assert abs(ctr["rejected"] - st["rejected"]) <= 0.01 * max(st["rejected"], 1)
+    if strategy == "darts":
+        assert ctr["rejected"] == 0 and ctr["samples"] > 1000
+    else:
+        assert ctr["rejected"] / ctr["samples"] > 0.5
+
+
+def test_response_boundary_errors(dts):
+    c = _resp_small()
+    sc = dts.Scene(dict(c, response=None))
+    sc.table_build()
+    h = torch.zeros(sc.hist_shape(), device="cuda")
+    with pytest.raises(dts.DtsError, match="DTS_E_STATE"):
+        sc.render(4, 1, 0, 4, h)                       # RESPONSE without dts_set_response
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        sc.set_response(np.zeros(c["n_bins"]))          # all zero
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        sc.set_response(np.ones(c["n_bins"] - 1))       # wrong length
+    bad = np.ones(c["n_bins"])
+    bad[3] = -1.0
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        sc.set_response(bad)
+    sc.set_response(c["response"])
+    sc.render(4, 1, 0, 4, h)
+    torch.cuda.synchronize()
+    assert float(h.sum()) > 0.0
