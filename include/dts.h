@@ -224,6 +224,12 @@ dts_status dts_render_host(dts_scene_t scene, uint64_t spp, uint64_t seed, uint6
 dts_status dts_sample_debug(dts_scene_t scene, int32_t n, const dts_debug_in* d_in, dts_debug_out* d_out,
                             void* stream);
 
+/* Number of failed device-side bounds checks (table, histogram, queue and
+ * response-CDF indices) since the last call, then reset; always 0 unless the
+ * library was built with -DDTS_CHECKS=1 (scripts/build_variants.sh).
+ * Synchronizes the device. */
+dts_status dts_check_failures(uint64_t* out);
+
 /* Kernel launches issued by the last dts_render on this thread (for the
  * bench's gpu_launches count) and the launch geometry. */
 dts_status dts_last_launch(int32_t* n_launches, int32_t* grid, int32_t* block, int32_t* smem_bytes);

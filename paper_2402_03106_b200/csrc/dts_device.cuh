@@ -14,6 +14,18 @@
 
 namespace dts {
 
+// Device-side bounds checks of the check build (-DDTS_CHECKS=1, see
+// dts_check_failures in dts.h): a failed check is counted, never trapped
+// (compute-sanitizer is not available on the GPU pool).
+#ifndef DTS_CHECKS
+#define DTS_CHECKS 0
+#endif
+__device__ unsigned long long g_dts_check_fail;
+#define DTS_CHECK(cond)                                              \
+  do {                                                               \
+    if (DTS_CHECKS && !(cond)) atomicAdd(&dts::g_dts_check_fail, 1ull); \
+  } while (0)
+
 constexpr float kPi = 3.14159265358979323846f;
 constexpr float kInv4Pi = 0.0795774715459476679f;
 constexpr float kLog2e = 1.44269504088896341f;
@@ -539,6 +551,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const int ir = min((int)(ratio * S.nr_f), S.nr - 1);
     const int is = min(max((int)ls, 0), S.ns - 1);
     const uint16_t* qc = tab + (valid ? (size_t)(ir * S.ns + is) * DTS_TABLE_COS_BINS : 0);
+    DTS_CHECK((size_t)(qc - tab) + DTS_TABLE_COS_BINS <= S.table_n);
     const f3 axis = cv * __fdividef(1.0f, C);
     const float u4 = unif(r[4]), u5 = unif(r[5]);
     const float phi = kPi * (2.0f * unif(r[6]) - 1.0f);
@@ -553,8 +566,10 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const uint32_t gi = Ti >> 8;
     int j = (int)gload<SMEM>(gc, gi);
     int jh = gi == 255u ? 255 : (int)gload<SMEM>(gc, gi + 1);
+    DTS_CHECK(gi < 256u && j >= 0 && j < 256 && jh >= 0 && jh < 256);
     while (j < jh) {
       const int mid = (j + jh + 1) >> 1;
+      DTS_CHECK(mid > 0 && mid < 256);
       if (qload<SMEM>(qc, mid) <= Ti) j = mid; else jh = mid - 1;
     }
     const float T = (float)(r[5] >> 9) * (1.0f / 128.0f);
@@ -571,6 +586,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const f3 om = from_frame(eda ? axis : ps.w, opc, omc, phi);
     if (!eda) {  // EDA pdf of the HG direction: bin of its cos to the emitter axis
       const int jb = min(max((int)floorf((dot(om, axis) + 1.0f) * 128.0f), 0), 255);
+      DTS_CHECK(jb >= 0 && jb < 256);
       qa = (float)qload<SMEM>(qc, jb);
       qb = jb == 255 ? 65536.0f : (float)qload<SMEM>(qc, jb + 1);
     }
@@ -725,6 +741,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const float coef = ps.beta * wconn;
       const uint32_t m7e = (r[7] >> 9) | ((uint32_t)ps.e << 23);
       if (slot < (uint32_t)kQueue) {
+        DTS_CHECK(df->q != nullptr);
         float* qq = df->q + slot;
         const uint32_t st = df->qstride;
         qq[0 * st] = ps.x.x; qq[1 * st] = ps.x.y; qq[2 * st] = ps.x.z;

@@ -9,6 +9,7 @@
 // its own cell).  No tensor cores: nothing on this path is a dense contraction.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -262,6 +263,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     int lo = 0, hi = (int)B - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
+      DTS_CHECK(mid > 0 && mid <= (int)B);
       if (__ldg(P.resp_cdf + mid) <= m) lo = mid; else hi = mid - 1;
     }
     b = (uint32_t)lo;
@@ -361,6 +363,7 @@ __device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t 
 }
 
 // ---------------------------------------------------------------- histogram splat (step 4)
+__constant__ uint32_t g_check_cells;  // histogram cells of the current launch (check build)
 // Per-bin dedicated paths: a retiring path adds its whole
 // contribution to its own cell.  Lanes that retire in the same iteration on the
 // same cell (consecutive sample ids of one cell) are combined first
@@ -386,6 +389,7 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
     }
   }
   if (lane != leader || v == 0.0f) return;
+  DTS_CHECK(cell < g_check_cells);
   if (s_hist) {
     atomicAdd(s_hist + cell, v);
     if (s_sq) atomicAdd(s_sq + cell, v2);
@@ -618,6 +622,7 @@ __device__ __forceinline__ int vanilla_splat(const RenderParams& P, uint32_t pl,
   const DevScene& S = P.S;
   const int bin = arrive >= S.t0 ? (int)floor((arrive - S.t0) / S.dt) : -1;
   if (bin < 0 || bin >= S.n_bins) return 1;
+  DTS_CHECK((size_t)pl * S.n_bins + bin < g_check_cells);
   const float w = P.resp_w ? __ldg(P.resp_w + bin) : 1.0f;
   if (w == 0.0f) return 1;
   atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, w * c / (float)P.spp);
@@ -1156,6 +1161,10 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   P.spp_div_b = (uint32_t)(spp / (uint64_t)d.n_bins);
   P.spp_mod_b = (uint32_t)(spp % (uint64_t)d.n_bins);
   cudaStream_t st = (cudaStream_t)stream;
+  if (DTS_CHECKS) {
+    const uint32_t cells32 = (uint32_t)std::min<size_t>(dts_hist_cells(s), 0xFFFFFFFFu);
+    CUDA_TRY(cudaMemcpyToSymbolAsync(g_check_cells, &cells32, sizeof cells32, 0, cudaMemcpyHostToDevice, st));
+  }
   if (darts) {
     P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix * (uint64_t)d.n_bins * ns : npix * ns;
     const size_t tbytes = s->table_n * 3;  // 16-bit CDF + 8-bit guide
@@ -1259,6 +1268,16 @@ dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, 
   void* args[] = {&S, &tab, &n, &d_in, &d_out};
   CUDA_TRY(cudaLaunchKernel(kfn, dim3((n + 127) / 128), dim3(128), args, 0, (cudaStream_t)stream));
   CUDA_TRY(cudaGetLastError());
+  return DTS_OK;
+}
+
+dts_status dts_check_failures(uint64_t* out) {
+  if (!out) return fail(DTS_E_INVALID_ARG, "NULL argument");
+  unsigned long long v = 0, z = 0;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpyFromSymbol(&v, dts::g_dts_check_fail, sizeof v));
+  CUDA_TRY(cudaMemcpyToSymbol(dts::g_dts_check_fail, &z, sizeof z));
+  *out = (uint64_t)v;
   return DTS_OK;
 }
 

@@ -89,13 +89,14 @@ _lib.dts_render_host.argtypes = [_VP, _U64, _U64, _U64, _U64, _VP, _VP, _VP]
 _lib.dts_sample_debug.argtypes = [_VP, ctypes.c_int32, _VP, _VP, _VP]
 _lib.dts_last_launch.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 4
 _lib.dts_set_response.argtypes = [_VP, _VP, ctypes.c_int32]
+_lib.dts_check_failures.argtypes = [ctypes.POINTER(ctypes.c_uint64)]
 _lib.dts_status_string.restype = ctypes.c_char_p
 _lib.dts_status_string.argtypes = [ctypes.c_int]
 _lib.dts_last_error.restype = ctypes.c_char_p
 _lib.dts_abi_version.restype = ctypes.c_int32
 
 EXPORTED = ("dts_scene_create", "dts_scene_destroy", "dts_set_response", "dts_table_build", "dts_table_export",
-            "dts_table_size",
+            "dts_table_size", "dts_check_failures",
             "dts_hist_cells", "dts_render", "dts_render_host", "dts_sample_debug", "dts_last_launch",
             "dts_status_string", "dts_last_error", "dts_abi_version")
 
@@ -258,6 +259,13 @@ def last_launch() -> dict:
     v = [ctypes.c_int32() for _ in range(4)]
     _lib.dts_last_launch(*[ctypes.byref(x) for x in v])
     return dict(n_launches=v[0].value, grid=v[1].value, block=v[2].value, smem=v[3].value)
+
+
+def check_failures() -> int:
+    """Failed device-side bounds checks since the last call (check builds only)."""
+    v = ctypes.c_uint64()
+    _check(_lib.dts_check_failures(ctypes.byref(v)), "dts_check_failures")
+    return int(v.value)
 
 
 def abi_version() -> int:
