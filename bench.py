@@ -144,19 +144,25 @@ def run_gpu(args):
 
     kern_ms = []
 
+    from paper_2402_03106_b200.shard import render_sharded
+
     def step(i, timed):
         hist.zero_()
         sc.table_build(stream=stream)
-        if timed:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        sc.render(spp, c["seed"] + 1000 * i, sb, se, hist, None, ctr if timed else None, stream)
-        if timed:
-            e1.record(stream)
-            kern_ms.append((e0, e1))
-        if world > 1:
-            dist.reduce(hist, dst=0)
+
+        def render_range(b, e):  # this rank's disjoint Philox key range
+            assert (b, e) == (sb, se)
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            sc.render(spp, c["seed"] + 1000 * i, b, e, hist, None, ctr if timed else None, stream)
+            if timed:
+                e1.record(stream)
+                kern_ms.append((e0, e1))
+
+        # render the shard, then ONE reduce of the histograms to rank 0 (NCCL over NVLink)
+        render_sharded(render_range, spp, hist)
 
     for i in range(args.warmup):
         step(i, False)

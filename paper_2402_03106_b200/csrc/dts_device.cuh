@@ -579,9 +579,11 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     // HG about w_{k-1}
     float opc, omc;
     hg_sample(S, u5, opc, omc);
-    if (eda) {  // cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts
-      opc = ((float)j + (T - qa) * iq) * (1.0f / 128.0f);
-      omc = ((float)(255 - j) + (qb - T) * iq) * (1.0f / 128.0f);
+    {  // EDA: cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts (selected, not branched)
+      const float eo = ((float)j + (T - qa) * iq) * (1.0f / 128.0f);
+      const float em = ((float)(255 - j) + (qb - T) * iq) * (1.0f / 128.0f);
+      opc = eda ? eo : opc;
+      omc = eda ? em : omc;
     }
     const f3 om = from_frame(eda ? axis : ps.w, opc, omc, phi);
     if (!eda) {  // EDA pdf of the HG direction: bin of its cos to the emitter axis

@@ -201,6 +201,10 @@ constexpr uint32_t kChunk = 128;
 // RIS layout: A = lane per path, 8 candidates in registers
 // (default); B = warp-collective 8-lane groups with shuffle scan/selection.
 constexpr bool kRisWarp = DTS_RIS_WARP != 0;
+#ifndef DTS_INNER
+#define DTS_INNER 1
+#endif
+constexpr int kInner = DTS_INNER;  // vertices per lane between refill checks
 constexpr size_t kPrivMaxCells = 4096;  // histograms up to 16 KiB are privatised per CTA
 
 struct PathCtx {
@@ -518,57 +522,64 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
     }
     if (s_queue && df.qn >= P.flush_at) flush();
     bool done = false;
-    bool pushed = false;
-    bool cn = false, wnee = false, alive = false;
-    int reason = 0;
-    uint32_t r[8];
-    float contrib = 0.0f;
-    RisReq rq;
-    rq.need = false;
-    if (active) {
-      const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
-      const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
-      r[0] = a.a; r[1] = a.b; r[2] = a.c; r[3] = a.d;
-      r[4] = b.a; r[5] = b.b; r[6] = b.c; r[7] = b.d;
-      df.act = act;
-      df.cell = pc.cell;
-      df.inv_n = pc.inv_n;
-      alive = darts_vertex<false, SMEM, SH, FL>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
-                                                s_queue ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr,
-                                                &c_samp);
-    }
-    if (kRisWarp) {
-      // RIS layout B: the warp draws every pending medium event's distance
-      const f3 xe = ld3(S.em_pos[(FL & FL_MULTI_E) ? pc.ps.e : 0]);
-      float dsel, Wr, wsel;
-      ris_warp(S, pc.ps, rq, xe, r[1], r[2], r[3], lane, dsel, Wr, wsel);
-      if (rq.need) {
-        if (Wr > 0.0f) {
-          ris_apply(S, pc.ps, dsel, Wr, wsel, rq.counts);
-          alive = vertex_tail(pc.ps, xe, reason);
-        } else {
-          alive = false;
-          reason = DTS_CTR_RIS_INVALID;  // R5
+    // kInner vertices per lane between refills (the refill / flush bookkeeping
+    // is paid once per kInner vertices; a lane that retires in the first waits)
+    for (int rep = 0; rep < kInner; ++rep) {
+      const unsigned act_r = rep == 0 ? act : __ballot_sync(FULL, active && !done);
+      if (act_r == 0u) break;
+      const bool run = active && !done;
+      bool pushed = false;
+      bool cn = false, wnee = false, alive = false;
+      int reason = 0;
+      uint32_t r[8];
+      float contrib = 0.0f;
+      RisReq rq;
+      rq.need = false;
+      if (run) {
+        const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
+        const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
+        r[0] = a.a; r[1] = a.b; r[2] = a.c; r[3] = a.d;
+        r[4] = b.a; r[5] = b.b; r[6] = b.c; r[7] = b.d;
+        df.act = act_r;
+        df.cell = pc.cell;
+        df.inv_n = pc.inv_n;
+        alive = darts_vertex<false, SMEM, SH, FL>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
+                                                  s_queue ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr,
+                                                  &c_samp);
+      }
+      if (kRisWarp) {
+        // RIS layout B: the warp draws every pending medium event's distance
+        const f3 xe = ld3(S.em_pos[(FL & FL_MULTI_E) ? pc.ps.e : 0]);
+        float dsel, Wr, wsel;
+        ris_warp(S, pc.ps, rq, xe, r[1], r[2], r[3], lane, dsel, Wr, wsel);
+        if (rq.need) {
+          if (Wr > 0.0f) {
+            ris_apply(S, pc.ps, dsel, Wr, wsel, rq.counts);
+            alive = vertex_tail(pc.ps, xe, reason);
+          } else {
+            alive = false;
+            reason = DTS_CTR_RIS_INVALID;  // R5
+          }
         }
       }
-    }
-    if (active) {
-      pc.acc += contrib;
-      ++pc.k;
-      const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
-      done = !alive || cap;
-      ++c_vert;
-      c_conn += cn ? 1u : 0u;
-      if (WALLS) c_nee += wnee ? 1u : 0u;
-      if (done) {
-        c_ris += reason == DTS_CTR_RIS_INVALID ? 1u : 0u;
-        c_early += reason == DTS_CTR_EARLY_EXIT ? 1u : 0u;
-        c_esc += reason == DTS_CTR_ESCAPES ? 1u : 0u;
-        c_nf += reason == DTS_CTR_NONFINITE ? 1u : 0u;
-        c_cap += cap ? 1u : 0u;
+      if (run) {
+        pc.acc += contrib;
+        ++pc.k;
+        const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
+        done = !alive || cap;
+        ++c_vert;
+        c_conn += cn ? 1u : 0u;
+        if (WALLS) c_nee += wnee ? 1u : 0u;
+        if (done) {
+          c_ris += reason == DTS_CTR_RIS_INVALID ? 1u : 0u;
+          c_early += reason == DTS_CTR_EARLY_EXIT ? 1u : 0u;
+          c_esc += reason == DTS_CTR_ESCAPES ? 1u : 0u;
+          c_nf += reason == DTS_CTR_NONFINITE ? 1u : 0u;
+          c_cap += cap ? 1u : 0u;
+        }
       }
+      if (s_queue) df.qn += __popc(__ballot_sync(FULL, pushed));
     }
-    if (s_queue) df.qn += __popc(__ballot_sync(FULL, pushed));
     const unsigned dmask = __ballot_sync(FULL, done);
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
