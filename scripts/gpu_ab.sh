@@ -1,13 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "same_key or crop" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
-DTS_LIB=libdts_inner2.so timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "same_key or crop" > gpurun_out/pytest_gpu2.log 2>&1; echo "pytest inner2 rc=$?"; tail -1 gpurun_out/pytest_gpu2.log
-B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
-run() { tag=$1; shift; env "$@" timeout 600 $B $BARGS > gpurun_out/ab_$tag.json 2> gpurun_out/ab_$tag.err; echo "$tag rc=$? $(python -c "import json;d=json.load(open('gpurun_out/ab_$tag.json'));print('%.4e v/s  kernel %.1f ms frac %.3f' % (d['value'], d['roofline']['kernel_ms'], d['roofline']['frac']))" 2>&1 | tail -1)"; }
-for cfg in "5 256" "3 16" "4 256"; do
-  set -- $cfg
-  BARGS="--config $1 --spp $2"
-  run c$1_i1
-  run c$1_i2 DTS_LIB=libdts_inner2.so
-  run c$1_i2_f24 DTS_LIB=libdts_inner2.so DTS_FLUSH_AT=24
-  run c$1_i3_f20 DTS_LIB=libdts_inner3.so DTS_FLUSH_AT=20
-done
+timeout 1800 python -m pytest tests -m gpu -q -x -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
+timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 1 --warmup 3 --spp 256 --no-cpu-baseline > gpurun_out/bench_torchrun1.json 2> gpurun_out/bench_torchrun1.err; echo "torchrun rc=$?"; tail -c 300 gpurun_out/bench_torchrun1.json
+timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json | tail -c 400
+bash scripts/gpu_prof.sh v4
