@@ -507,6 +507,66 @@ def test_single_scatter_closed_form(cfg1_runs):
     assert m[1:].sum() == pytest.approx(ref[1:].sum(), rel=5e-3)
 
 
+def _hg(g, mu):
+    return (1 - g * g) / (4 * math.pi * (1 + g * g - 2 * g * mu) ** 1.5)
+
+
+@pytest.mark.parametrize("case", ["cfg3_backscatter_warped", "cfg2_forward_unwarped"])
+def test_pinhole_single_scatter_quadrature(oracle, case):
+    """Order-1 (camera-vertex connection, R13) of a pinhole pixel against a
+    deterministic 1-D quadrature along its ray: a one-pixel
+    camera with a 0.2 degree fov so the pixel is one ray to O(1e-5).
+    cfg3: camera = emitter at (0,0,-2) over the slab -- backscatter, recorded
+    time 2t (warped, camera outside the medium).  cfg2: camera at (0,0,4), the
+    sphere, emitter at (0,0,-3) straight ahead -- forward scattering, recorded
+    time |x(t) - xe| (unwarped, R16/R17).  H_1[b] = int sigma_s
+    e^{-sigma_t (l1 + l2)} rho_HG P/(4 pi) / r2^2 [T(t) in bin b] dt."""
+    if case.startswith("cfg3"):
+        c = I.as_f32(I.small(I.config(3, fov_y_deg=0.2), 1, 1, n_bins=36, t1=6.5))
+        dt = (c["t1"] - c["t0"]) / c["n_bins"]
+        tl, th = 2.0, 3.0                                   # the ray inside z in [0, 1]
+        r2 = lambda t: t
+        l12 = lambda t: 2.0 * (t - 2.0)
+        mu = -1.0
+        Tof = lambda t: 2.0 * t
+        tinv = lambda T: T / 2.0
+    else:
+        c = I.as_f32(I.small(I.config(2, fov_y_deg=0.2), 1, 1, n_bins=64, t1=5.0))
+        dt = (c["t1"] - c["t0"]) / c["n_bins"]
+        tl, th = 3.0, 5.0                                   # the ray inside the unit sphere
+        r2 = lambda t: 7.0 - t
+        l12 = lambda t: 2.0
+        mu = 1.0
+        Tof = lambda t: 7.0 - t                             # unwarped: camera leg excluded
+        tinv = lambda T: 7.0 - T
+    ss, st, g = c["sigma_s"], c["sigma_s"] + c["sigma_a"], c["g"]
+    f = lambda t: ss * math.exp(-st * l12(t)) * _hg(g, mu) / (4 * math.pi) / r2(t) ** 2
+    ref = np.zeros(c["n_bins"])
+    inner = np.zeros(c["n_bins"], bool)      # bins whose whole time range lies on the ray's medium part
+    for b in range(c["n_bins"]):
+        a, z = sorted((tinv(c["t0"] + b * dt), tinv(c["t0"] + (b + 1) * dt)))
+        inner[b] = a >= tl and z <= th
+        a, z = max(a, tl), min(z, th)
+        if z > a:
+            ref[b] = integrate.quad(f, a, z)[0]
+    q, _ = oracle.build_table(c)
+    runs = [oracle.render(c, q, 2000, 500 + s, n_orders=1, sq=False)["order_hist"][0, 0, 0] for s in range(16)]
+    o1 = np.array(runs)
+    m, se = o1.mean(0), o1.std(0, ddof=1) / math.sqrt(len(o1))
+    nz = ref > 0
+    assert nz.sum() >= 10
+    assert (m[~nz] == 0).all()                              # causality: nothing outside the ray's times
+    # the estimator's SE is tiny here (the truncated-exponential S matches the
+    # transmittance), so the pixel's finite footprint (~(fov)^2 ~ 1e-5 relative)
+    # enters the bound next to 3 SE
+    # (bins cut by the medium boundary also see the footprint's chord-length spread)
+    sel = nz & inner
+    err = np.abs(m[sel] - ref[sel])
+    ok = err <= 3 * se[sel] + 2e-4 * ref[sel]
+    assert ok.mean() >= 0.95, (err / np.maximum(se[sel], 1e-300))[~ok]
+    assert m[nz].sum() == pytest.approx(ref[nz].sum(), rel=2e-3)
+
+
 def test_multiple_scattering_tail_vs_diffusion(oracle, cfg1_runs):
     """Total response at t in [6, 12) vs the E9 Green's function at R = 2:
     the diffusion approximation is accurate there to ~7 %."""
