@@ -48,6 +48,7 @@ struct dts_scene {
   uint32_t* d_resp_cdf = nullptr;  // R31 bin CDF (n_bins + 1)
   float* d_resp_wgt = nullptr;     // W_b / pi_b
   float* d_resp_w = nullptr;       // W_b
+  uint16_t* d_zero_cell = nullptr; // debug kernel table for vanilla scenes
   int num_sms = 0;
   int device = 0;
 };
@@ -1030,6 +1031,7 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaFree(s->d_resp_cdf);
   cudaFree(s->d_resp_wgt);
   cudaFree(s->d_resp_w);
+  cudaFree(s->d_zero_cell);
   delete s;
   return DTS_OK;
 }
@@ -1265,12 +1267,14 @@ dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, 
   if (!s || (n > 0 && (!d_in || !d_out)) || n < 0) return fail(DTS_E_INVALID_ARG, "bad arguments");
   if (n == 0) return DTS_OK;
   if (s->desc.strategy != DTS_STRATEGY_VANILLA && !s->d_table) return fail(DTS_E_STATE, "table not built");
-  static uint16_t* d_dummy = nullptr;
   const uint16_t* tab = s->d_table;
   if (!tab) {
-    if (!d_dummy) CUDA_TRY(cudaMalloc(&d_dummy, 256 * sizeof(uint16_t)));
-    CUDA_TRY(cudaMemsetAsync(d_dummy, 0, 256 * sizeof(uint16_t), (cudaStream_t)stream));
-    tab = d_dummy;
+    // vanilla scenes have no table: the debug kernel reads a zero cell (gamma = 0)
+    if (!s->d_zero_cell) {
+      if (cudaMalloc(&s->d_zero_cell, 3 * 256) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(zero cell) failed");
+      CUDA_TRY(cudaMemset(s->d_zero_cell, 0, 3 * 256));
+    }
+    tab = s->d_zero_cell;
   }
   const void* kfn = debug_kernel_ptr(s->desc);
   if (!kfn) return fail(DTS_E_INVALID_ARG, "no debug kernel for this scene shape");
