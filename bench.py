@@ -132,6 +132,8 @@ def run_gpu(args):
     c = I.as_f32(I.config(args.config))
     if args.direction_mode:
         c["direction_mode"] = args.direction_mode
+    if args.strategy:
+        c["strategy"] = args.strategy
     if args.spp:
         c["spp"] = args.spp
     spp = c["spp"]
@@ -378,6 +380,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--direction-mode", choices=["reuse", "split"], default=None)
+    ap.add_argument("--strategy", choices=["darts", "vanilla", "da_only", "eda_only"], default=None,
+                    help="estimator (default: the config's, DARTS); other values are comparison runs, not bench lines")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
