@@ -206,7 +206,13 @@ size_t dts_hist_cells(dts_scene_t scene);
  * d_hist (device, dts_hist_cells floats) is ACCUMULATED (+=) with each path's
  * contribution / (paths of its cell); d_hist_sq (device, nullable) accumulates
  * contribution^2 / (paths of its cell); d_counters (device, nullable,
- * DTS_NUM_COUNTERS uint64) accumulates the counters.  Asynchronous. */
+ * DTS_NUM_COUNTERS uint64) accumulates the counters.  Asynchronous.
+ * Tuning knobs, read from the environment on every call (defaults are the
+ * measured optima of profiles/README.md): DTS_NO_DEFER=1 turns the per-warp
+ * connection queue off; DTS_FLUSH_AT (1..32, default 28) is the queue length
+ * that triggers a batch; DTS_REFILL_K (default 16) is the idle
+ * lane-iterations that trigger a lane refill.  None changes any result
+ * beyond fp32 summation order. */
 dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
                       uint64_t sample_end, float* d_hist, float* d_hist_sq, uint64_t* d_counters,
                       void* stream);
