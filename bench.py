@@ -33,6 +33,16 @@ import numpy as np  # noqa: E402
 
 import dts_inputs as I  # noqa: E402
 
+# BASELINE.json's metric (the value is its first part: path vertices/s of the
+# whole job; the roofline fraction is the JSON line's roofline.frac; the
+# equal-time MSE is measured by scripts/mse_vs_oracle.py and mse_equal_time.py)
+METRIC = "path vertices/s at 1/2/4/8 B200 (% FP32/SFU roofline); MSE vs oracle at equal time"
+try:
+    with open(os.path.join(ROOT, "BASELINE.json")) as _f:
+        METRIC = json.load(_f).get("metric", METRIC)
+except (OSError, ValueError):
+    pass
+
 # algorithmic thread-instructions per DARTS vertex
 # (REUSE 610; SPLIT adds an HG sample and a second intersection, +40).
 ALG_INSTR_PER_VERTEX = {"reuse": 610, "split": 650}
@@ -213,7 +223,7 @@ def run_gpu(args):
         traffic = _profile_traffic(args.config)
         clocks = clk.summary()
         line = {
-            "metric": "path vertices/s (DARTS transient volumetric PT)",
+            "metric": METRIC,
             "value": value,
             "unit": "vertices/s",
             "n_gpus": world,
@@ -361,7 +371,7 @@ def run_reference(args):
     value = tot_v / tot_t
     st, el, c = last
     line = {
-        "impl": "reference", "metric": "path vertices/s (DARTS transient volumetric PT)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "vertices/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
