@@ -258,6 +258,13 @@ def run_gpu(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
+        mse = _profile_json("mse_vs_oracle_r01.json")
+        if mse and args.config == 5:
+            # the metric's second half, measured by scripts/mse_vs_oracle.py (not in this run)
+            line["mse_vs_oracle_equal_time"] = {
+                "ratio_cpu_over_gpu": mse.get("mse_ratio_cpu_over_gpu_equal_time"),
+                "mse_vs_spp_slope": mse.get("mse_vs_spp_slope"), "crop": mse.get("crop"),
+                "source": "profiles/mse_vs_oracle_r01.json (scripts/mse_vs_oracle.py)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -313,6 +320,14 @@ def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts):
             "h2d_bytes_per_step": ctypes.sizeof(dts.SceneDesc),
             "d2h_bytes_per_step": cells * 4 + (8 * dts.NUM_COUNTERS if world == 1 else 0),
             "timing": "host wall clock (perf_counter) around scene_create..histogram in pinned host memory, max over ranks"}
+
+
+def _profile_json(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
 
 
 def _profile_traffic(cfg):
