@@ -220,7 +220,7 @@ def run_gpu(args):
         # the dominant kernel is the render kernel: per-rank vertices / its launch time
         achieved = (verts_per_step / world) * alg / (kern_avg * 1e-3) / 1e12
         value = verts_per_step / (ms / args.steps * 1e-3)
-        traffic = _profile_traffic(args.config)
+        traffic = None if (args.spp or args.strategy or args.direction_mode) else _profile_traffic(args.config)
         clocks = clk.summary()
         line = {
             "metric": METRIC,
