@@ -70,6 +70,7 @@ struct DevScene {
   int32_t conn_uniform;  // 1: P of S uniform (ablation of PAPER.md:295)
   float alpha;
   float r_excl, s_excess;
+  float far_e;  // largest distance from an emitter to a point of the medium (+ margin; inf for INFINITE)
   // EDA table (R8-R10)
   int32_t nr, ns;
   float nr_f, ns_f;
@@ -438,15 +439,42 @@ __device__ __forceinline__ float conn_job_run(const DevScene& S, f3 x, f3 wc, fl
 // S sample and contribution at a few active lanes.
 constexpr int kJobWords = 11;  // x[3] w[3] dlo width coef m7e cell
 constexpr int kQueue = 32;     // slots per warp
+constexpr int kJob1Words = 14;  // stage-1 job: x[3] w_prev[3] resM(hi, lo) coef r4 r5 r6 m7e cell
+// Stage-1 deferral (SPLIT: the whole connection stage queued) is a build
+// option (-DDTS_STAGE1=1): it executes 8 % fewer instructions on config 5 but
+// the alternation of two large code regions thrashes the instruction cache
+// (ncu no_instruction stalls 0.25 -> 2.1 per issue) and it runs 12 % slower.
+#ifndef DTS_STAGE1
+#define DTS_STAGE1 0
+#endif
+constexpr bool kStage1Build = DTS_STAGE1 != 0;
 struct Defer {
   float* q;           // this warp's queue: word f of slot j at q[f * qstride + j]
+  float* q1;          // this warp's stage-1 queue (SPLIT: whole connection stages), same stride
+  float* g;           // global overflow slots kQueue..2 kQueue-1 of q: word f of slot j at g[f * kQueue + j - kQueue]
+  float* g1;          // the same for q1
   uint32_t qstride;   // words between fields (= kQueue * warps per CTA)
   uint32_t qn;        // jobs queued (warp-uniform)
+  uint32_t qn1;       // stage-1 jobs queued (warp-uniform)
   unsigned act;       // lanes executing darts_vertex
   uint32_t lane_lt;   // lanes below this one
   uint32_t cell;      // the path's histogram cell
   float inv_n;        // 1 / paths of the cell
 };
+
+// Address of queue slot `slot` (< 2 kQueue): the first kQueue slots are in
+// shared memory (stride qstride between fields), the next kQueue in the warp's
+// global overflow area (stride kQueue), so a push never has to fall back to an
+// inline connection.  *st receives the field stride.
+__device__ __forceinline__ float* queue_slot(float* qs, uint32_t qstride, float* qg, uint32_t slot, uint32_t* st) {
+  DTS_CHECK(slot < 2u * (uint32_t)kQueue);
+  if (slot < (uint32_t)kQueue) {
+    *st = qstride;
+    return qs + slot;
+  }
+  *st = (uint32_t)kQueue;
+  return qg + (slot - (uint32_t)kQueue);
+}
 
 // A medium event whose RIS distance is drawn later by the warp-collective
 // sampler (RIS layout B); the vertex state is kept in PathState
@@ -483,15 +511,116 @@ __device__ __forceinline__ bool vertex_tail(const PathState& ps, f3 xe, int& end
   return true;
 }
 
+// Could a connection from x (inside the medium) reach the bin's lower residual
+// resm = R_m - E at all?  S(t) = t + |x + w t - xe| over any chord from x is at
+// most (farthest medium point from x) + (farthest medium point from any
+// emitter, S.far_e): a larger resm means an empty S range for every direction.
+template <int SH>
+__device__ __forceinline__ bool may_connect_bound(const DevScene& S, f3 x, float resm) {
+  if (SH == DTS_MEDIUM_BOX) {
+    const float fx = fmaxf(x.x - S.bmin[0], S.bmax[0] - x.x);
+    const float fy = fmaxf(x.y - S.bmin[1], S.bmax[1] - x.y);
+    const float fz = fmaxf(x.z - S.bmin[2], S.bmax[2] - x.z);
+    return resm <= sqrtf(fmaf(fx, fx, fmaf(fy, fy, fz * fz))) + S.far_e;
+  }
+  if (SH == DTS_MEDIUM_SPHERE) {
+    const f3 d = x - ld3(S.center);
+    return resm <= sqrtf(dot(d, d)) + sqrtf(S.radius2) + S.far_e;
+  }
+  return true;
+}
+
+// ----------------------------------------------------------------- direction mixture (E16-E19)
+// One-sample MIS of the EDA table and HG at a medium vertex x with incoming
+// direction w: gamma of E19 with the table cell of R10 at S = R_M - E (R11),
+// technique by u4, cos(theta) by u5 (EDA: inverse transform of the cell's
+// 16-bit CDF; HG about w), phi = pi (2 u6 - 1) (R12).  GUIDE: the CDF rows are
+// followed by 8-bit guide rows (REUSE kernels stage both); without it the bin
+// is found by an 8-step branchless binary search -- the same bin.
+struct MixDir {
+  f3 om;
+  float gamma, p_eda, p_hg, p_mix;
+  bool eda;
+};
+template <bool SMEM, bool GUIDE>
+__device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_t* __restrict__ tab, f3 x, f3 w,
+                                                float resM, f3 xe, uint32_t r4, uint32_t r5, uint32_t r6) {
+  const f3 cv = xe - x;
+  const float C = sqrtf(dot(cv, cv));
+  const float ratio = __fdividef(C, resM);
+  const float ls = (__logf(resM) - S.ln_smin) * S.inv_dls;
+  // DA_ONLY ablation: phase-function directions only (gamma = 0)
+  const bool valid = (resM > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < S.ns_f) &&
+                     S.strategy != DTS_STRATEGY_DA_ONLY;
+  MixDir m;
+  m.gamma = valid ? __fdividef(ratio, ratio + S.alpha) : 0.0f;
+  const int ir = min((int)(ratio * S.nr_f), S.nr - 1);
+  const int is = min(max((int)ls, 0), S.ns - 1);
+  const uint16_t* qc = tab + (valid ? (size_t)(ir * S.ns + is) * DTS_TABLE_COS_BINS : 0);
+  DTS_CHECK((size_t)(qc - tab) + DTS_TABLE_COS_BINS <= S.table_n);
+  const f3 axis = cv * __fdividef(1.0f, C);
+  const float u4 = unif(r4), u5 = unif(r5);
+  const float phi = kPi * (2.0f * unif(r6) - 1.0f);
+  m.eda = u4 < m.gamma;
+  // Both techniques are evaluated by every lane and one is selected, so the
+  // warp never splits into an EDA and an HG branch.
+  // EDA: T = u5 * 65536 exactly; the bin is the largest j with q_j <= T, i.e.
+  // q_j <= Ti = floor(T).
+  const uint32_t Ti = r5 >> 16;
+  int j;
+  if (GUIDE) {  // guide entry of Ti's 1/256 slice, then bisect within the slice
+    const uint8_t* gc = reinterpret_cast<const uint8_t*>(tab + S.table_n) + (qc - tab);
+    const uint32_t gi = Ti >> 8;
+    j = (int)gload<SMEM>(gc, gi);
+    int jh = gi == 255u ? 255 : (int)gload<SMEM>(gc, gi + 1);
+    DTS_CHECK(gi < 256u && j >= 0 && j < 256 && jh >= 0 && jh < 256);
+    while (j < jh) {
+      const int mid = (j + jh + 1) >> 1;
+      DTS_CHECK(mid > 0 && mid < 256);
+      if (qload<SMEM>(qc, mid) <= Ti) j = mid; else jh = mid - 1;
+    }
+  } else {  // q_0 = 0 <= Ti: binary search with steps 128 .. 1
+    j = 0;
+#pragma unroll
+    for (int st = 128; st > 0; st >>= 1)
+      if (qload<SMEM>(qc, j + st) <= Ti) j += st;
+  }
+  const float T = (float)(r5 >> 9) * (1.0f / 128.0f);
+  float qa = (float)qload<SMEM>(qc, j);
+  float qb = j == 255 ? 65536.0f : (float)qload<SMEM>(qc, j + 1);
+  const float iq = __fdividef(1.0f, qb - qa);
+  // HG about w_{k-1}
+  float opc, omc;
+  hg_sample(S, u5, opc, omc);
+  {  // EDA: cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts (selected, not branched)
+    const float eo = ((float)j + (T - qa) * iq) * (1.0f / 128.0f);
+    const float em = ((float)(255 - j) + (qb - T) * iq) * (1.0f / 128.0f);
+    opc = m.eda ? eo : opc;
+    omc = m.eda ? em : omc;
+  }
+  m.om = from_frame(m.eda ? axis : w, opc, omc, phi);
+  if (!m.eda) {  // EDA pdf of the HG direction: bin of its cos to the emitter axis
+    const int jb = min(max((int)floorf((dot(m.om, axis) + 1.0f) * 128.0f), 0), 255);
+    DTS_CHECK(jb >= 0 && jb < 256);
+    qa = (float)qload<SMEM>(qc, jb);
+    qb = jb == 255 ? 65536.0f : (float)qload<SMEM>(qc, jb + 1);
+  }
+  m.p_eda = valid ? (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi)) : 0.0f;
+  m.p_hg = hg_eval(S, dot(m.om, w));
+  m.p_mix = m.gamma * m.p_eda + (1.0f - m.gamma) * m.p_hg;
+  return m;
+}
+
 // ----------------------------------------------------------------- one DARTS vertex
 // Returns true if the walk continues.  contrib receives the vertex's
 // connection (+ wall NEE) contribution; end_reason the DTS_CTR_* of a stop.
-template <bool DBG, bool SMEM, int SH, int FL>
+template <bool DBG, bool SMEM, int SH, int FL, bool DEFER = false>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason,
                                              const Defer* df = nullptr, bool* pushed = nullptr,
-                                             RisReq* rq = nullptr, uint32_t* nsamp = nullptr) {
+                                             RisReq* rq = nullptr, uint32_t* nsamp = nullptr,
+                                             bool* pushed1 = nullptr) {
   contrib = 0.0f;
   conn_nonempty = false;
   wall_nee = false;
@@ -503,6 +632,35 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   f3 wc, ww;
   float wconn = 1.0f;
   const float resM = d2f(ps.resM);
+
+  // ---- SPLIT render kernel: queue this vertex's whole connection stage (stage 1) ----
+  // A medium vertex whose connection can reach its bin at all (may_connect_bound)
+  // writes x, w_{k-1}, R_M - E, beta / n_cell, u4..u7 and its cell into the
+  // warp's stage-1 queue; the warp later runs up to 32 of them at once (mixture
+  // direction, intersection, S range) and forwards the non-empty ones to the
+  // sampling queue.  A lane that finds the queue full connects inline.
+  bool skip_conn = false;
+  if (SPLIT && DEFER && kStage1Build && !DBG) {
+    const bool cand = ps.kind == KIND_MEDIUM && may_connect_bound<SH>(S, ps.x, d2f(ps.resM - S.dt));
+    const unsigned m1 = __ballot_sync(df->act, cand);
+    const uint32_t slot1 = df->qn1 + __popc(m1 & df->lane_lt);
+    *pushed1 = cand;
+    skip_conn = ps.kind == KIND_MEDIUM;  // queued, or unable to land in the bin
+    if (cand) {
+      uint32_t st;
+      float* qq = queue_slot(df->q1, df->qstride, df->g1, slot1, &st);
+      qq[0 * st] = ps.x.x; qq[1 * st] = ps.x.y; qq[2 * st] = ps.x.z;
+      qq[3 * st] = ps.w.x; qq[4 * st] = ps.w.y; qq[5 * st] = ps.w.z;
+      qq[6 * st] = __int_as_float(__double2hiint(ps.resM));
+      qq[7 * st] = __int_as_float(__double2loint(ps.resM));
+      qq[8 * st] = ps.beta * df->inv_n;
+      qq[9 * st] = __uint_as_float(r[4]);
+      qq[10 * st] = __uint_as_float(r[5]);
+      qq[11 * st] = __uint_as_float(r[6]);
+      qq[12 * st] = __uint_as_float((r[7] >> 9) | ((uint32_t)ps.e << 23));
+      qq[13 * st] = __uint_as_float(df->cell);
+    }
+  }
 
   // ---- step 2: direction ----
   if (ps.kind == KIND_CAMERA) {
@@ -539,62 +697,18 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       dbg->beta_dir = alb;
     }
   } else {
-    // medium vertex: gamma of E19 with the table cell of R10 at S = R_M - E (R11)
-    const f3 cv = xe - ps.x;
-    const float C = sqrtf(dot(cv, cv));
-    const float ratio = __fdividef(C, resM);
-    const float ls = (__logf(resM) - S.ln_smin) * S.inv_dls;
-    // DA_ONLY ablation: phase-function directions only (gamma = 0)
-    const bool valid = (resM > 0.0f) && (ratio < 1.0f) && (ls >= 0.0f) && (ls < S.ns_f) &&
-                       S.strategy != DTS_STRATEGY_DA_ONLY;
-    const float gamma = valid ? __fdividef(ratio, ratio + S.alpha) : 0.0f;
-    const int ir = min((int)(ratio * S.nr_f), S.nr - 1);
-    const int is = min(max((int)ls, 0), S.ns - 1);
-    const uint16_t* qc = tab + (valid ? (size_t)(ir * S.ns + is) * DTS_TABLE_COS_BINS : 0);
-    DTS_CHECK((size_t)(qc - tab) + DTS_TABLE_COS_BINS <= S.table_n);
-    const f3 axis = cv * __fdividef(1.0f, C);
-    const float u4 = unif(r[4]), u5 = unif(r[5]);
-    const float phi = kPi * (2.0f * unif(r[6]) - 1.0f);
-    const bool eda = u4 < gamma;
-    // Both techniques are evaluated by every lane and one is selected, so the
-    // warp never splits into an EDA and an HG branch.
-    // EDA: inverse transform of the cell's 16-bit CDF.  T = u5 * 65536 exactly;
-    // the bin is the largest j with q_j <= T, i.e. q_j <= Ti = floor(T): start
-    // from the guide entry of Ti's 1/256 slice and bisect within the slice.
-    const uint32_t Ti = r[5] >> 16;
-    const uint8_t* gc = reinterpret_cast<const uint8_t*>(tab + S.table_n) + (qc - tab);
-    const uint32_t gi = Ti >> 8;
-    int j = (int)gload<SMEM>(gc, gi);
-    int jh = gi == 255u ? 255 : (int)gload<SMEM>(gc, gi + 1);
-    DTS_CHECK(gi < 256u && j >= 0 && j < 256 && jh >= 0 && jh < 256);
-    while (j < jh) {
-      const int mid = (j + jh + 1) >> 1;
-      DTS_CHECK(mid > 0 && mid < 256);
-      if (qload<SMEM>(qc, mid) <= Ti) j = mid; else jh = mid - 1;
-    }
-    const float T = (float)(r[5] >> 9) * (1.0f / 128.0f);
-    float qa = (float)qload<SMEM>(qc, j);
-    float qb = j == 255 ? 65536.0f : (float)qload<SMEM>(qc, j + 1);
-    const float iq = __fdividef(1.0f, qb - qa);
-    // HG about w_{k-1}
-    float opc, omc;
-    hg_sample(S, u5, opc, omc);
-    {  // EDA: cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts (selected, not branched)
-      const float eo = ((float)j + (T - qa) * iq) * (1.0f / 128.0f);
-      const float em = ((float)(255 - j) + (qb - T) * iq) * (1.0f / 128.0f);
-      opc = eda ? eo : opc;
-      omc = eda ? em : omc;
-    }
-    const f3 om = from_frame(eda ? axis : ps.w, opc, omc, phi);
-    if (!eda) {  // EDA pdf of the HG direction: bin of its cos to the emitter axis
-      const int jb = min(max((int)floorf((dot(om, axis) + 1.0f) * 128.0f), 0), 255);
-      DTS_CHECK(jb >= 0 && jb < 256);
-      qa = (float)qload<SMEM>(qc, jb);
-      qb = jb == 255 ? 65536.0f : (float)qload<SMEM>(qc, jb + 1);
-    }
-    const float p_eda = valid ? (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi)) : 0.0f;
-    const float p_hg = hg_eval(S, dot(om, ps.w));
-    const float p_mix = gamma * p_eda + (1.0f - gamma) * p_hg;
+    // medium vertex: one-sample MIS of EDA and HG
+    if (SPLIT && skip_conn) {
+      // R29 SPLIT, connection queued (or unreachable): only the walk's
+      // independent HG direction is drawn here
+      float o2, m2;
+      hg_sample(S, u_split(r[0], r[1], r[2]), o2, m2);
+      wc = ww = from_frame(ps.w, o2, m2, kPi * (2.0f * u_split(r[3], r[4], r[5]) - 1.0f));
+    } else {
+    const MixDir md = mix_direction<SMEM, !(SPLIT && kStage1Build)>(S, tab, ps.x, ps.w, resM, xe, r[4], r[5], r[6]);
+    const f3 om = md.om;
+    const bool eda = md.eda;
+    const float gamma = md.gamma, p_eda = md.p_eda, p_hg = md.p_hg, p_mix = md.p_mix;
     const float ratio_w = __fdividef(p_hg, p_mix);
     wc = om;
     if (SPLIT) {
@@ -616,6 +730,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       dbg->p_hg = p_hg;
       dbg->p_mix = p_mix;
     }
+    }
   }
   if (DBG) {
     dbg->wc[0] = wc.x; dbg->wc[1] = wc.y; dbg->wc[2] = wc.z;
@@ -629,14 +744,32 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   const int hit = ps.kind == KIND_CAMERA ? intersect<SH, WALLS>(S, ps.x, ww, lo, hi, face)
                                          : intersect_inside<SH, WALLS>(S, ps.x, ww, lo, hi, face);
   // render kernel: non-empty connections of medium/wall vertices are queued (df)
-  const bool defer = !DBG && df && ps.kind != KIND_CAMERA;
+  const bool defer = DEFER && !DBG && ps.kind != KIND_CAMERA;
+#ifdef DTS_MEASURE_MAYCONNECT
+  if (!DBG && SH == DTS_MEDIUM_BOX && ps.kind == KIND_MEDIUM) {
+    // experiment: fraction of medium vertices whose connection could be non-empty
+    // by the bound  R_m - E <= |farthest box corner from x| + |farthest box corner from xe|
+    const float fx = fmaxf(ps.x.x - S.bmin[0], S.bmax[0] - ps.x.x);
+    const float fy = fmaxf(ps.x.y - S.bmin[1], S.bmax[1] - ps.x.y);
+    const float fz = fmaxf(ps.x.z - S.bmin[2], S.bmax[2] - ps.x.z);
+    const float ex_ = fmaxf(fabsf(xe.x - S.bmin[0]), fabsf(S.bmax[0] - xe.x));
+    const float ey_ = fmaxf(fabsf(xe.y - S.bmin[1]), fabsf(S.bmax[1] - xe.y));
+    const float ez_ = fmaxf(fabsf(xe.z - S.bmin[2]), fabsf(S.bmax[2] - xe.z));
+    const float bound = sqrtf(fx * fx + fy * fy + fz * fz) + sqrtf(ex_ * ex_ + ey_ * ey_ + ez_ * ez_);
+    if (d2f(ps.resM - S.dt) <= bound) atomicAdd(&dts::g_dts_check_fail, 1ull);
+  }
+#endif
   bool want_job = false;
   float job_dlo = 0.0f, job_width = 0.0f;
   float clo = lo, chi = hi;
   int hitc = hit;
   if (SPLIT && ps.kind == KIND_MEDIUM) {
-    int fc;
-    hitc = intersect_inside<SH, WALLS>(S, ps.x, wc, clo, chi, fc);
+    if (skip_conn) {
+      hitc = HIT_MISS;  // the connection stage runs from the stage-1 queue (or cannot land)
+    } else {
+      int fc;
+      hitc = intersect_inside<SH, WALLS>(S, ps.x, wc, clo, chi, fc);
+    }
   }
   if (DBG) {
     dbg->t_lo = lo; dbg->t_hi = hi; dbg->hit = hit; dbg->face_hit = face;
@@ -733,31 +866,28 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       }
     }
   }
-  if (!DBG && df) {
-    // queue the job in a free slot; a lane that finds the queue full runs its
-    // connection now (the same arithmetic)
+  if (DEFER && !DBG) {
+    // queue the job (slots beyond the shared-memory queue are global overflow)
     const unsigned jm = __ballot_sync(df->act, want_job);
     const uint32_t slot = df->qn + __popc(jm & df->lane_lt);
-    *pushed = false;
+    *pushed = want_job;
     if (want_job) {
-      const float coef = ps.beta * wconn;
-      const uint32_t m7e = (r[7] >> 9) | ((uint32_t)ps.e << 23);
-      if (slot < (uint32_t)kQueue) {
-        DTS_CHECK(df->q != nullptr);
+      const float w8 = ps.beta * wconn * df->inv_n;
+      const float w9 = __uint_as_float((r[7] >> 9) | ((uint32_t)ps.e << 23));
+      const float w10 = __uint_as_float(df->cell);
+      DTS_CHECK(slot < 2u * (uint32_t)kQueue);
+      if (slot < (uint32_t)kQueue) {  // shared-memory slot (STS)
         float* qq = df->q + slot;
         const uint32_t st = df->qstride;
         qq[0 * st] = ps.x.x; qq[1 * st] = ps.x.y; qq[2 * st] = ps.x.z;
         qq[3 * st] = wc.x; qq[4 * st] = wc.y; qq[5 * st] = wc.z;
-        qq[6 * st] = job_dlo;
-        qq[7 * st] = job_width;
-        qq[8 * st] = coef * df->inv_n;
-        qq[9 * st] = __uint_as_float(m7e);
-        qq[10 * st] = __uint_as_float(df->cell);
-        *pushed = true;
-      } else {
-        const float c = conn_job_run<SH, FL>(S, ps.x, wc, job_dlo, job_width, coef, m7e);
-        contrib += c;
-        if (nsamp && c != 0.0f) ++*nsamp;
+        qq[6 * st] = job_dlo; qq[7 * st] = job_width; qq[8 * st] = w8; qq[9 * st] = w9; qq[10 * st] = w10;
+      } else {  // global overflow slot (STG)
+        float* qq = df->g + (slot - (uint32_t)kQueue);
+        constexpr uint32_t st = kQueue;
+        qq[0 * st] = ps.x.x; qq[1 * st] = ps.x.y; qq[2 * st] = ps.x.z;
+        qq[3 * st] = wc.x; qq[4 * st] = wc.y; qq[5 * st] = wc.z;
+        qq[6 * st] = job_dlo; qq[7 * st] = job_width; qq[8 * st] = w8; qq[9 * st] = w9; qq[10 * st] = w10;
       }
     }
   }

@@ -49,6 +49,8 @@ struct dts_scene {
   float* d_resp_wgt = nullptr;     // W_b / pi_b
   float* d_resp_w = nullptr;       // W_b
   uint16_t* d_zero_cell = nullptr; // debug kernel table for vanilla scenes
+  float* d_qover = nullptr;        // deferred-connection queue overflow slots
+  size_t qover_n = 0;
   int num_sms = 0;
   int device = 0;
 };
@@ -188,6 +190,8 @@ struct RenderParams {
   uint32_t priv_cells;            // > 0: the CTA privatises the whole histogram in shared memory
   uint32_t defer;                 // 1: connections are queued per warp and evaluated in batches
   uint32_t flush_at;              // queue length that triggers a batch
+  uint32_t flush1_at;             // stage-1 queue length that triggers a batch (SPLIT)
+  float* qover;                   // DEFER: global overflow queue slots, kQueue x (kJobWords + kJob1Words) per warp
   uint32_t refill_k;              // idle lane-iterations that trigger a refill
 };
 
@@ -410,7 +414,7 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
 #ifndef DTS_TABLE_SMEM
 #define DTS_TABLE_SMEM 1
 #endif
-template <bool SMEM, int SH, int FL>
+template <bool SMEM, int SH, int FL, bool DEFER>
 __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const RenderParams P) {
   constexpr bool WALLS = (FL & FL_WALLS) != 0;
   extern __shared__ __align__(16) uint16_t s_dyn[];
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s_hist[i] = 0.0f;
       base += (size_t)n * sizeof(float);
     }
-    if (P.defer) s_queue = reinterpret_cast<float*>(base);
+    if (DEFER) s_queue = reinterpret_cast<float*>(base);
   }
   if (SMEM) {
     bulk_stage(s_dyn, P.tab, P.table_u4 * 16u, &s_bar);
@@ -443,9 +447,20 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
   // this warp's connection-job queue: field f of slot j at q[f * qstride + j]
   const uint32_t qstride = (uint32_t)kQueue * (kBlock / 32);
   Defer df;
-  df.q = s_queue ? s_queue + (threadIdx.x >> 5) * kQueue : nullptr;
+  df.q = DEFER ? s_queue + (threadIdx.x >> 5) * kQueue : nullptr;
+  // SPLIT kernels: the stage-1 queues follow the sampling queues
+  constexpr bool kStage1 = kStage1Build && DEFER && (FL & FL_SPLIT) != 0;
+  df.q1 = kStage1 ? s_queue + (size_t)kJobWords * qstride + (threadIdx.x >> 5) * kQueue : nullptr;
+  {  // this warp's global overflow slots (kQueue per queue)
+    float* gw = DEFER ? P.qover + ((size_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5)) *
+                                      (size_t)(kQueue * (kJobWords + kJob1Words))
+                      : nullptr;
+    df.g = gw;
+    df.g1 = DEFER ? gw + kQueue * kJobWords : nullptr;
+  }
   df.qstride = qstride;
   df.qn = 0;
+  df.qn1 = 0;
   df.lane_lt = lt_mask;
   // warp-uniform work queue [wn, we)
   uint64_t wn = 0, we = 0;
@@ -457,7 +472,8 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
   uint32_t c_samp = 0;  // non-zero contributions (path samples); DARTS never rejects one (its bin has W > 0)
   uint32_t l_miss = 0, l_early = 0;  // start-time retirements
   uint32_t waste = 0;                // idle lane-iterations since the last refill
-  // evaluates the queued jobs, one per lane, and splats them (cells differ per job)
+  // runs up to kQueue queued sampling jobs, one per lane, and splats them;
+  // jobs left in the global overflow slots move down into the shared slots
   auto flush = [&]() {
     float c = 0.0f;
     uint32_t cell = 0;
@@ -472,7 +488,67 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
     const bool has = c != 0.0f;
     const unsigned m = __ballot_sync(FULL, has);
     if (m) splat(m, has, cell, c, 0.0f, P.hist, nullptr, s_hist, nullptr, lane);
-    df.qn = 0;
+    __syncwarp();
+    const uint32_t rest = df.qn > (uint32_t)kQueue ? df.qn - kQueue : 0u;
+    if ((uint32_t)lane < rest)
+      for (int f = 0; f < kJobWords; ++f) df.q[f * qstride + lane] = df.g[f * kQueue + lane];
+    df.qn = rest;
+    __syncwarp();
+  };
+  // runs up to kQueue stage-1 jobs (SPLIT: mixture direction, its intersection,
+  // S range), one per lane, and forwards the non-empty ones to the sampling queue
+  auto flush1 = [&]() {
+    bool want2 = false;
+    f3 x = mk(0.0f, 0.0f, 0.0f), wc = x;
+    float dlo = 0.0f, width = 0.0f, coef2 = 0.0f;
+    uint32_t m7e = 0, cell = 0;
+    if ((uint32_t)lane < df.qn1) {
+      const float* q = df.q1 + lane;
+      const uint32_t st = qstride;
+      x = mk(q[0 * st], q[1 * st], q[2 * st]);
+      const f3 wprev = mk(q[3 * st], q[4 * st], q[5 * st]);
+      const double resM_d = __hiloint2double(__float_as_int(q[6 * st]), __float_as_int(q[7 * st]));
+      const float coef = q[8 * st];
+      const uint32_t r4 = __float_as_uint(q[9 * st]), r5 = __float_as_uint(q[10 * st]), r6 = __float_as_uint(q[11 * st]);
+      m7e = __float_as_uint(q[12 * st]);
+      cell = __float_as_uint(q[13 * st]);
+      const int e = (FL & FL_MULTI_E) ? (int)(m7e >> 23) : 0;
+      const f3 xe = ld3(S.em_pos[e]);
+      const MixDir md = mix_direction<SMEM, false>(S, tab, x, wprev, d2f(resM_d), xe, r4, r5, r6);
+      wc = md.om;
+      float lo_, chi;
+      int face_;
+      if (intersect_inside<SH, WALLS>(S, x, wc, lo_, chi, face_) != HIT_MISS) {
+        const f3 cv = xe - x;
+        const float C = sqrtf(dot(cv, cv));
+        const SRange rg = conn_range(S, x, wc, xe, C, dot(wc, cv), 0.0f, chi, resM_d);
+        if (rg.width > 0.0f) {
+          want2 = true;
+          ++c_conn;
+          dlo = rg.dlo;
+          width = rg.width;
+          coef2 = coef * __fdividef(md.p_hg, md.p_mix);  // R29 SPLIT: the MIS weight stays on the connection
+        }
+      }
+    }
+    __syncwarp();
+    const uint32_t rest = df.qn1 > (uint32_t)kQueue ? df.qn1 - kQueue : 0u;
+    if ((uint32_t)lane < rest)
+      for (int f = 0; f < kJob1Words; ++f) df.q1[f * qstride + lane] = df.g1[f * kQueue + lane];
+    df.qn1 = rest;
+    const unsigned m2 = __ballot_sync(FULL, want2);
+    if (want2) {
+      uint32_t st;
+      float* qq = queue_slot(df.q, qstride, df.g, df.qn + __popc(m2 & lt_mask), &st);
+      qq[0 * st] = x.x; qq[1 * st] = x.y; qq[2 * st] = x.z;
+      qq[3 * st] = wc.x; qq[4 * st] = wc.y; qq[5 * st] = wc.z;
+      qq[6 * st] = dlo;
+      qq[7 * st] = width;
+      qq[8 * st] = coef2;
+      qq[9 * st] = __uint_as_float(m7e);
+      qq[10 * st] = __uint_as_float(cell);
+    }
+    df.qn += __popc(m2);
     __syncwarp();
   };
   while (true) {
@@ -517,11 +593,27 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       }
     }
     const unsigned act = __ballot_sync(FULL, active);
+    // queue batches; once the work is exhausted and every lane idle, drain them
+    // (one call site each: the queue code is inlined once)
+    const bool drain = act == 0u && exhausted;
+    // Capacity: each queue has kQueue shared + kQueue global slots.  After this
+    // loop qn < flush_at and qn1 < flush1_at (<= kQueue), so the <= 32 pushes of
+    // the next vertex always fit; flush1 (which feeds <= 32 jobs to the sampling
+    // queue) only runs while that queue has <= kQueue jobs.
+    while (DEFER) {
+      const bool need1 = kStage1 && df.qn1 && (df.qn1 >= P.flush1_at || drain);
+      if (df.qn && (df.qn >= P.flush_at || drain || (need1 && df.qn > (uint32_t)kQueue))) {
+        flush();
+      } else if (need1) {
+        flush1();
+      } else {
+        break;
+      }
+    }
     if (act == 0u) {
-      if (exhausted) break;
+      if (drain && df.qn1 == 0u && df.qn == 0u) break;
       continue;
     }
-    if (s_queue && df.qn >= P.flush_at) flush();
     bool done = false;
     // kInner vertices per lane between refills (the refill / flush bookkeeping
     // is paid once per kInner vertices; a lane that retires in the first waits)
@@ -529,7 +621,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       const unsigned act_r = rep == 0 ? act : __ballot_sync(FULL, active && !done);
       if (act_r == 0u) break;
       const bool run = active && !done;
-      bool pushed = false;
+      bool pushed = false, pushed1 = false;
       bool cn = false, wnee = false, alive = false;
       int reason = 0;
       uint32_t r[8];
@@ -544,9 +636,9 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
         df.act = act_r;
         df.cell = pc.cell;
         df.inv_n = pc.inv_n;
-        alive = darts_vertex<false, SMEM, SH, FL>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
-                                                  s_queue ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr,
-                                                  &c_samp);
+        alive = darts_vertex<false, SMEM, SH, FL, DEFER>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
+                                                         DEFER ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr,
+                                                         &c_samp, &pushed1);
       }
       if (kRisWarp) {
         // RIS layout B: the warp draws every pending medium event's distance
@@ -579,7 +671,8 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
           c_cap += cap ? 1u : 0u;
         }
       }
-      if (s_queue) df.qn += __popc(__ballot_sync(FULL, pushed));
+      if (DEFER) df.qn += __popc(__ballot_sync(FULL, pushed));
+      if (kStage1) df.qn1 += __popc(__ballot_sync(FULL, pushed1));
     }
     const unsigned dmask = __ballot_sync(FULL, done);
     if (dmask) {
@@ -588,7 +681,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
       if (done) active = false;
     }
   }
-  if (s_queue && df.qn) flush();
+
   if (P.priv_cells) {  // flush the CTA's private histogram (coalesced REDs of its non-zero cells)
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < P.priv_cells; i += blockDim.x) {
@@ -792,8 +885,6 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
 // FL_MULTI_E (more than one emitter), so no launch carries the branches,
 // registers or constant-bank indexing of the other scene kinds.  Walls exist
 // only in BOX media (validated), so the other shapes instantiate the even FLs.
-template <bool SMEM, int SH, int FL>
-static const void* rk_ptr() { return (const void*)render_darts_kernel<SMEM, SH, FL>; }
 template <int SH, int FL>
 static const void* dk_ptr() { return (const void*)debug_kernel<SH, FL>; }
 
@@ -819,15 +910,14 @@ static const void* pick_fl(int shape, int fl) {
   }
   return nullptr;
 }
-template <int FL> struct PickRenderSmem {
-  static const void* box() { return rk_ptr<true, DTS_MEDIUM_BOX, FL>(); }
-  static const void* inf() { return rk_ptr<true, DTS_MEDIUM_INFINITE, FL>(); }
-  static const void* sph() { return rk_ptr<true, DTS_MEDIUM_SPHERE, FL>(); }
-};
-template <int FL> struct PickRenderGlobal {
-  static const void* box() { return rk_ptr<false, DTS_MEDIUM_BOX, FL>(); }
-  static const void* inf() { return rk_ptr<false, DTS_MEDIUM_INFINITE, FL>(); }
-  static const void* sph() { return rk_ptr<false, DTS_MEDIUM_SPHERE, FL>(); }
+template <bool SMEM, bool DEFER>
+struct PickRender {
+  template <int FL>
+  struct F {
+    static const void* box() { return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, FL, DEFER>; }
+    static const void* inf() { return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_INFINITE, FL, DEFER>; }
+    static const void* sph() { return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, FL, DEFER>; }
+  };
 };
 template <int FL> struct PickDebug {
   static const void* box() { return dk_ptr<DTS_MEDIUM_BOX, FL>(); }
@@ -838,9 +928,10 @@ static int scene_flags(const dts_scene_desc& d) {
   return (d.wall_mask ? FL_WALLS : 0) | (d.direction_mode == DTS_DIR_SPLIT ? FL_SPLIT : 0) |
          (d.n_emitters > 1 ? FL_MULTI_E : 0);
 }
-static const void* darts_kernel_ptr(bool smem, const dts_scene_desc& d) {
-  return smem ? pick_fl<PickRenderSmem>(d.medium_shape, scene_flags(d))
-              : pick_fl<PickRenderGlobal>(d.medium_shape, scene_flags(d));
+static const void* darts_kernel_ptr(bool smem, bool defer, const dts_scene_desc& d) {
+  const int sh = d.medium_shape, fl = scene_flags(d);
+  if (smem) return defer ? pick_fl<PickRender<true, true>::F>(sh, fl) : pick_fl<PickRender<true, false>::F>(sh, fl);
+  return defer ? pick_fl<PickRender<false, true>::F>(sh, fl) : pick_fl<PickRender<false, false>::F>(sh, fl);
 }
 static const void* debug_kernel_ptr(const dts_scene_desc& d) { return pick_fl<PickDebug>(d.medium_shape, scene_flags(d)); }
 static const void* vanilla_kernel_ptr(int shape, bool walls) {
@@ -976,6 +1067,23 @@ static void derive(const dts_scene_desc& d, DevScene& S) {
   S.alpha = d.alpha;
   S.r_excl = d.parity_r_excl;
   S.s_excess = d.parity_s_excess;
+  // far_e: largest distance from an emitter to a point of the medium (box: its
+  // farthest corner; sphere: centre distance + radius), with a rounding margin
+  double far = 0.0;
+  for (int e = 0; e < d.n_emitters; ++e) {
+    double f2 = 0.0;
+    if (d.medium_shape == DTS_MEDIUM_BOX) {
+      for (int a = 0; a < 3; ++a) {
+        const double u = std::fmax(std::fabs((double)d.bmin[a] - d.em_pos[e][a]), std::fabs((double)d.bmax[a] - d.em_pos[e][a]));
+        f2 += u * u;
+      }
+      far = std::fmax(far, std::sqrt(f2));
+    } else if (d.medium_shape == DTS_MEDIUM_SPHERE) {
+      for (int a = 0; a < 3; ++a) f2 += ((double)d.em_pos[e][a] - d.center[a]) * ((double)d.em_pos[e][a] - d.center[a]);
+      far = std::fmax(far, std::sqrt(f2) + d.radius);
+    }
+  }
+  S.far_e = d.medium_shape == DTS_MEDIUM_INFINITE ? INFINITY : (float)(far * (1.0 + 1e-4) + 1e-4);
 }
 
 // ============================================================== C ABI
@@ -1032,6 +1140,7 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaFree(s->d_resp_wgt);
   cudaFree(s->d_resp_w);
   cudaFree(s->d_zero_cell);
+  cudaFree(s->d_qover);
   delete s;
   return DTS_OK;
 }
@@ -1180,7 +1289,10 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   }
   if (darts) {
     P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix * (uint64_t)d.n_bins * ns : npix * ns;
-    const size_t tbytes = s->table_n * 3;  // 16-bit CDF + 8-bit guide
+    // kernels stage the 16-bit CDF rows and the 8-bit guide rows; stage-1 SPLIT
+    // builds stage the CDF only (binary search) to leave room for the stage-1 queues
+    const bool split = kStage1Build && d.direction_mode == DTS_DIR_SPLIT;
+    const size_t tbytes = s->table_n * (split ? 2 : 3);
     P.table_u4 = (uint32_t)(tbytes / 16);
     const bool smem = DTS_TABLE_SMEM && tbytes <= 220 * 1024;
     // privatise small histograms (config 1: 128 cells) in shared memory
@@ -1189,19 +1301,29 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     const size_t kSmemCap = 227 * 1024 - 64;  // opt-in per-block maximum less the static mbarrier
     if (cells <= kPrivMaxCells && (smem ? tbytes : 0) + pbytes <= kSmemCap) P.priv_cells = (uint32_t)cells;
     // per-warp connection-job queues (not with hist_sq: its per-path squares need whole-path sums)
-    const size_t qbytes = (size_t)kJobWords * kQueue * (kBlock / 32) * sizeof(float);
-    const char* nd = getenv("DTS_NO_DEFER");
-    const bool defer = !d_hist_sq && !(nd && nd[0] == '1') &&
+    const size_t qbytes = (size_t)(kJobWords + (split ? kJob1Words : 0)) * kQueue * (kBlock / 32) * sizeof(float);
+    // Deferral pays only for long walks (A/B, profiles/README.md: +1.6 % on config 5,
+    // sigma_t T = 2000; -6 % / -10 % / -30 % on configs 3, 2, 4): on by default when
+    // sigma_t (t1 - min tau_e) >= 1000; DTS_DEFER=0/1 overrides
+    float tmin = d.em_t[0];
+    for (int e = 1; e < d.n_emitters; ++e) tmin = std::fmin(tmin, d.em_t[e]);
+    bool want_defer = (double)s->S.sigma_t * ((double)d.t1 - tmin) >= 1000.0;
+    const char* dv = getenv("DTS_DEFER");
+    if (dv && (dv[0] == '0' || dv[0] == '1')) want_defer = dv[0] == '1';
+    const bool defer = want_defer && !d_hist_sq &&
                        (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + qbytes <= kSmemCap;
     P.defer = defer ? 1u : 0u;
     const char* rk = getenv("DTS_REFILL_K");
     P.refill_k = rk ? (uint32_t)atoi(rk) : 16u;
     if (P.refill_k < 1 || P.refill_k > 4096) P.refill_k = 16u;
+    const char* f1 = getenv("DTS_FLUSH1_AT");
+    P.flush1_at = f1 ? (uint32_t)atoi(f1) : 16u;
+    if (P.flush1_at < 1 || P.flush1_at > (uint32_t)kQueue) P.flush1_at = 16u;
     const char* fa = getenv("DTS_FLUSH_AT");
     P.flush_at = fa ? (uint32_t)atoi(fa) : 28u;
     if (P.flush_at < 1 || P.flush_at > (uint32_t)kQueue) P.flush_at = 28u;
     const size_t dyn = (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + (defer ? qbytes : 0);
-    const void* kfn = darts_kernel_ptr(smem, d);
+    const void* kfn = darts_kernel_ptr(smem, defer, d);
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
     int blocks_per_sm = 1;
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
@@ -1210,6 +1332,17 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     uint64_t grid = (uint64_t)s->num_sms * blocks_per_sm;
     const uint64_t need = (P.total + 31) / 32 / (kBlock / 32) + 1;
     if (grid > need) grid = need;
+    if (defer) {  // global overflow queue slots: kQueue x (kJobWords + kJob1Words) floats per warp
+      const size_t ov = (size_t)grid * (kBlock / 32) * kQueue * (kJobWords + kJob1Words);
+      if (ov > s->qover_n) {
+        cudaFree(s->d_qover);
+        s->d_qover = nullptr;
+        s->qover_n = 0;
+        if (cudaMalloc(&s->d_qover, ov * sizeof(float)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(queue overflow) failed");
+        s->qover_n = ov;
+      }
+      P.qover = s->d_qover;
+    }
     CUDA_TRY(cudaMemsetAsync(s->d_work, 0, sizeof(unsigned long long), st));
     void* args[] = {&P};
     CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(kBlock), args, dyn, st));
