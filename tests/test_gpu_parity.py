@@ -368,3 +368,29 @@ def test_response_boundary_errors(dts):
     sc.render(4, 1, 0, 4, h)
     torch.cuda.synchronize()
     assert float(h.sum()) > 0.0
+
+
+# ------------------------------------------------------------------ both kernel variants (DEFER on / off)
+DEFER_CASES = [
+    ("cfg2_small", lambda: I.small(I.config(2), 16, 16, n_bins=64, t1=10.0), 8),
+    ("cfg3_small", lambda: I.small(I.config(3), 6, 5, n_bins=64, t1=8.5), 8),
+    ("cfg4_walls", lambda: I.small(I.config(4), 24, 24), 64),
+    ("cfg5_small", lambda: I.small(I.config(5), 7, 9, n_bins=120, t1=12.0), 150),
+]
+
+
+@pytest.mark.parametrize("defer", ["0", "1"])
+@pytest.mark.parametrize("name,mk,spp", DEFER_CASES, ids=[d[0] for d in DEFER_CASES])
+def test_render_same_key_both_variants(dts, oracle, monkeypatch, name, mk, spp, defer):
+    """The deferred-connection kernels (per-warp queues, global overflow
+    slots) and the immediate ones give the oracle's histogram on the same
+    keys (DTS_DEFER forces the variant; the default picks by walk length)."""
+    monkeypatch.setenv("DTS_DEFER", defer)
+    c = I.as_f32(mk())
+    g, o, ctr = _same_key(dts, oracle, c, spp, c["seed"])
+    ho = o["hist"]
+    rel = np.linalg.norm(g - ho) / np.linalg.norm(ho)
+    assert ctr["paths"] == o["stats"]["paths"]
+    assert abs(ctr["conn_nonempty"] - o["stats"]["conn_nonempty"]) <= 0.01 * o["stats"]["conn_nonempty"] + 2
+    print(f"{name}/DTS_DEFER={defer}: same-key relative L2 {rel:.3e}")
+    assert rel <= 0.01
