@@ -198,7 +198,13 @@ struct RenderParams {
 #ifndef DTS_BLOCK
 #define DTS_BLOCK 768
 #endif
-constexpr int kBlock = DTS_BLOCK;
+constexpr int kBlock = DTS_BLOCK;  // deferred-connection kernels: the queues take the shared memory
+#ifndef DTS_BLOCK_IMM
+#define DTS_BLOCK_IMM 896
+#endif
+// immediate-connection kernels: 28 warps at <= 72 registers (A/B in profiles/README.md)
+constexpr int kBlockImm = DTS_BLOCK_IMM;
+__host__ __device__ constexpr int render_block(bool defer) { return defer ? kBlock : kBlockImm; }
 constexpr uint32_t kChunk = 128;
 #ifndef DTS_RIS_WARP
 #define DTS_RIS_WARP 0
@@ -415,7 +421,7 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
 #define DTS_TABLE_SMEM 1
 #endif
 template <bool SMEM, int SH, int FL, bool DEFER>
-__global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const RenderParams P) {
+__global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_kernel(const RenderParams P) {
   constexpr bool WALLS = (FL & FL_WALLS) != 0;
   extern __shared__ __align__(16) uint16_t s_dyn[];
   __shared__ uint64_t s_bar;
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(kBlock, DTS_MINB) render_darts_kernel(const Re
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   // this warp's connection-job queue: field f of slot j at q[f * qstride + j]
-  const uint32_t qstride = (uint32_t)kQueue * (kBlock / 32);
+  const uint32_t qstride = (uint32_t)kQueue * (kBlock / 32);  // (DEFER kernels only)
   Defer df;
   df.q = DEFER ? s_queue + (threadIdx.x >> 5) * kQueue : nullptr;
   // SPLIT kernels: the stage-1 queues follow the sampling queues
@@ -1327,10 +1333,11 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
     int blocks_per_sm = 1;
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, kBlock, dyn));
+    const int blk = render_block(defer);
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, blk, dyn));
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     uint64_t grid = (uint64_t)s->num_sms * blocks_per_sm;
-    const uint64_t need = (P.total + 31) / 32 / (kBlock / 32) + 1;
+    const uint64_t need = (P.total + 31) / 32 / (blk / 32) + 1;
     if (grid > need) grid = need;
     if (defer) {  // global overflow queue slots: kQueue x (kJobWords + kJob1Words) floats per warp
       const size_t ov = (size_t)grid * (kBlock / 32) * kQueue * (kJobWords + kJob1Words);
@@ -1345,11 +1352,11 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     }
     CUDA_TRY(cudaMemsetAsync(s->d_work, 0, sizeof(unsigned long long), st));
     void* args[] = {&P};
-    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(kBlock), args, dyn, st));
+    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(blk), args, dyn, st));
     CUDA_TRY(cudaGetLastError());
     g_last_launches = 1;
     g_last_grid = (int)grid;
-    g_last_block = kBlock;
+    g_last_block = blk;
     g_last_smem = (int)dyn;
   } else {
     P.total = npix * ns;

@@ -1,7 +1,9 @@
-for spec in "5 16" "3 4"; do
-  set -- $spec
-  PCMD="python bench.py --config $1 --spp $2 --steps 1 --warmup 3 --no-cpu-baseline"
-  $PCMD > gpurun_out/plain_prof_c$1.log 2>&1 && \
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_darts -s 3 -c 1 \
-      -o gpurun_out/prof_v5_c$1 $PCMD > gpurun_out/ncu_full_c$1.log 2>&1; echo "ncu c$1 rc=$?"
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -q -x -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
+B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
+run() { tag=$1; shift; env "$@" timeout 600 $B $BARGS > gpurun_out/ab_$tag.json 2> gpurun_out/ab_$tag.err; echo "$tag rc=$? $(python -c "import json;d=json.load(open('gpurun_out/ab_$tag.json'));c=d['counters'];print('%.4e v/s  kernel %.1f ms frac %.3f block %d' % (d['value'], d['roofline']['kernel_ms'], d['roofline']['frac'], d['launch']['block']))" 2>&1 | tail -1)"; }
+for cfg in "5 256" "3 16" "4 256" "2 16" "1 2048"; do
+  set -- $cfg
+  BARGS="--config $1 --spp $2"
+  run c$1_v52
 done
