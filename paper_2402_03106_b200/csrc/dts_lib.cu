@@ -229,8 +229,8 @@ struct PathCtx {
 
 // decode a work index into a path (returns false if the path retires at start)
 template <int SH, int FL>
-__device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx, PathCtx& pc, uint32_t& ctr_miss,
-                                           uint32_t& ctr_early) {
+__device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx, PathCtx& pc,
+                                           uint32_t* s_ctr) {
   const DevScene& S = P.S;
   const uint32_t B = (uint32_t)S.n_bins;
   uint64_t s;
@@ -334,13 +334,13 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   float lo, hi;
   int f;
   if (intersect<SH, (FL & FL_WALLS) != 0>(S, ps.x, ps.w, lo, hi, f) == HIT_MISS) {
-    ++ctr_miss;
+    atomicAdd(s_ctr + DTS_CTR_CAMERA_MISS, 1u);
     return false;
   }
   if (S.warped || S.camera_kind == DTS_CAMERA_SPHERE_DETECTOR) {
     const f3 dv = ps.x - ld3(S.em_pos[e]);
     if (sqrtf(dot(dv, dv)) >= d2f(ps.resM)) {
-      ++ctr_early;
+      atomicAdd(s_ctr + DTS_CTR_EARLY_EXIT, 1u);
       return false;
     }
   }
@@ -425,6 +425,10 @@ __global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_ke
   constexpr bool WALLS = (FL & FL_WALLS) != 0;
   extern __shared__ __align__(16) uint16_t s_dyn[];
   __shared__ uint64_t s_bar;
+  // rare events (path starts and ends) are counted per CTA in shared memory;
+  // the per-vertex ones in registers
+  __shared__ uint32_t s_ctr[DTS_NUM_COUNTERS];  // 32-bit: native shared atomics; <= paths per CTA
+  if (threadIdx.x < DTS_NUM_COUNTERS) s_ctr[threadIdx.x] = 0u;
   const DevScene& S = P.S;
   const uint16_t* tab = P.tab;
   // dynamic shared memory: [EDA table (SMEM)] [private histogram] [private hist_sq] [job queues]
@@ -474,9 +478,8 @@ __global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_ke
   bool active = false;
   PathCtx pc;
   // per-lane event counters, summed over the warp at the end
-  uint32_t c_paths = 0, c_vert = 0, c_conn = 0, c_ris = 0, c_early = 0, c_esc = 0, c_cap = 0, c_nf = 0, c_nee = 0;
+  uint32_t c_vert = 0, c_conn = 0, c_nee = 0;
   uint32_t c_samp = 0;  // non-zero contributions (path samples); DARTS never rejects one (its bin has W > 0)
-  uint32_t l_miss = 0, l_early = 0;  // start-time retirements
   uint32_t waste = 0;                // idle lane-iterations since the last refill
   // runs up to kQueue queued sampling jobs, one per lane, and splats them;
   // jobs left in the global overflow slots move down into the shared slots
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_ke
     if ((uint32_t)lane < df.qn) {
       c = conn_job_eval<SH, FL>(S, df.q + lane, qstride, cell);
       if (!isfinite(c)) {
-        ++c_nf;
+        atomicAdd(s_ctr + DTS_CTR_NONFINITE, 1u);
         c = 0.0f;
       }
       c_samp += c != 0.0f ? 1u : 0u;
@@ -593,10 +596,10 @@ __global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_ke
         wn = nq < ne ? nq : ne;
         we = ne;
       }
-      if (!active && my != ~0ull && my < P.total) {
-        active = start_path<SH, FL>(P, my, pc, l_miss, l_early);
-        ++c_paths;
-      }
+      const bool starts = !active && my != ~0ull && my < P.total;
+      const unsigned sm = __ballot_sync(FULL, starts);
+      if (lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
+      if (starts) active = start_path<SH, FL>(P, my, pc, s_ctr);
     }
     const unsigned act = __ballot_sync(FULL, active);
     // queue batches; once the work is exhausted and every lane idle, drain them
@@ -669,13 +672,7 @@ __global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_ke
         ++c_vert;
         c_conn += cn ? 1u : 0u;
         if (WALLS) c_nee += wnee ? 1u : 0u;
-        if (done) {
-          c_ris += reason == DTS_CTR_RIS_INVALID ? 1u : 0u;
-          c_early += reason == DTS_CTR_EARLY_EXIT ? 1u : 0u;
-          c_esc += reason == DTS_CTR_ESCAPES ? 1u : 0u;
-          c_nf += reason == DTS_CTR_NONFINITE ? 1u : 0u;
-          c_cap += cap ? 1u : 0u;
-        }
+        if (done) atomicAdd(s_ctr + (cap ? (int)DTS_CTR_CAP_HITS : reason), 1u);  // reason: a DTS_CTR_* index
       }
       if (DEFER) df.qn += __popc(__ballot_sync(FULL, pushed));
       if (kStage1) df.qn1 += __popc(__ballot_sync(FULL, pushed1));
@@ -688,41 +685,27 @@ __global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_ke
     }
   }
 
+  for (int o = 16; o > 0; o >>= 1) {
+    c_vert += __shfl_xor_sync(FULL, c_vert, o);
+    c_conn += __shfl_xor_sync(FULL, c_conn, o);
+    c_nee += __shfl_xor_sync(FULL, c_nee, o);
+    c_samp += __shfl_xor_sync(FULL, c_samp, o);
+  }
+  if (lane == 0 && P.counters) {  // per-vertex counters: 64-bit, straight to global
+    atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
+    atomicAdd(P.counters + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
+    atomicAdd(P.counters + DTS_CTR_WALL_NEE, (unsigned long long)c_nee);
+    atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
+  }
+  __syncthreads();
   if (P.priv_cells) {  // flush the CTA's private histogram (coalesced REDs of its non-zero cells)
-    __syncthreads();
     for (uint32_t i = threadIdx.x; i < P.priv_cells; i += blockDim.x) {
       if (s_hist[i] != 0.0f) atomicAdd(P.hist + i, s_hist[i]);
       if (s_sq && s_sq[i] != 0.0f) atomicAdd(P.hist_sq + i, s_sq[i]);
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    c_paths += __shfl_xor_sync(FULL, c_paths, o);
-    l_miss += __shfl_xor_sync(FULL, l_miss, o);
-    l_early += __shfl_xor_sync(FULL, l_early, o);
-    c_vert += __shfl_xor_sync(FULL, c_vert, o);
-    c_conn += __shfl_xor_sync(FULL, c_conn, o);
-    c_ris += __shfl_xor_sync(FULL, c_ris, o);
-    c_early += __shfl_xor_sync(FULL, c_early, o);
-    c_esc += __shfl_xor_sync(FULL, c_esc, o);
-    c_cap += __shfl_xor_sync(FULL, c_cap, o);
-    c_nf += __shfl_xor_sync(FULL, c_nf, o);
-    c_nee += __shfl_xor_sync(FULL, c_nee, o);
-    c_samp += __shfl_xor_sync(FULL, c_samp, o);
-  }
-  if (lane == 0 && P.counters) {
-    unsigned long long* C = P.counters;
-    atomicAdd(C + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
-    atomicAdd(C + DTS_CTR_PATHS, (unsigned long long)c_paths);
-    atomicAdd(C + DTS_CTR_CAMERA_MISS, (unsigned long long)l_miss);
-    atomicAdd(C + DTS_CTR_VERTICES, (unsigned long long)c_vert);
-    atomicAdd(C + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
-    atomicAdd(C + DTS_CTR_RIS_INVALID, (unsigned long long)c_ris);
-    atomicAdd(C + DTS_CTR_EARLY_EXIT, (unsigned long long)(c_early + l_early));
-    atomicAdd(C + DTS_CTR_ESCAPES, (unsigned long long)c_esc);
-    atomicAdd(C + DTS_CTR_CAP_HITS, (unsigned long long)c_cap);
-    atomicAdd(C + DTS_CTR_NONFINITE, (unsigned long long)c_nf);
-    atomicAdd(C + DTS_CTR_WALL_NEE, (unsigned long long)c_nee);
-  }
+  if (P.counters && threadIdx.x < DTS_NUM_COUNTERS && s_ctr[threadIdx.x])
+    atomicAdd(P.counters + threadIdx.x, (unsigned long long)s_ctr[threadIdx.x]);
 }
 
 // ============================================================== vanilla
@@ -1304,7 +1287,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     // privatise small histograms (config 1: 128 cells) in shared memory
     const size_t cells = dts_hist_cells(s);
     const size_t pbytes = cells * sizeof(float) * (d_hist_sq ? 2 : 1);
-    const size_t kSmemCap = 227 * 1024 - 64;  // opt-in per-block maximum less the static mbarrier
+    const size_t kSmemCap = 227 * 1024 - 256;  // opt-in per-block maximum less the static shared memory (mbarrier, counters)
     if (cells <= kPrivMaxCells && (smem ? tbytes : 0) + pbytes <= kSmemCap) P.priv_cells = (uint32_t)cells;
     // per-warp connection-job queues (not with hist_sq: its per-path squares need whole-path sums)
     const size_t qbytes = (size_t)(kJobWords + (split ? kJob1Words : 0)) * kQueue * (kBlock / 32) * sizeof(float);
