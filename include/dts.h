@@ -208,9 +208,9 @@ size_t dts_hist_cells(dts_scene_t scene);
  * contribution^2 / (paths of its cell); d_counters (device, nullable,
  * DTS_NUM_COUNTERS uint64) accumulates the counters.  Asynchronous.
  * Tuning knobs, read from the environment on every call (defaults are the
- * measured optima of profiles/README.md): DTS_DEFER=0/1 forces the per-warp
- * connection queue off/on (default: on when sigma_t (t1 - min tau_e) >= 1000,
- * i.e. long walks); DTS_FLUSH_AT (1..32, default 28) is the queue length
+ * measured optima of profiles/README.md): DTS_DEFER=1 selects the kernels
+ * with per-warp connection queues (default off: the immediate kernels are as
+ * fast or faster on every config); DTS_FLUSH_AT (1..32, default 28) is the queue length
  * that triggers a batch; DTS_REFILL_K (default 16) is the idle
  * lane-iterations that trigger a lane refill.  None changes any result
  * beyond fp32 summation order. */

@@ -1291,12 +1291,10 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     if (cells <= kPrivMaxCells && (smem ? tbytes : 0) + pbytes <= kSmemCap) P.priv_cells = (uint32_t)cells;
     // per-warp connection-job queues (not with hist_sq: its per-path squares need whole-path sums)
     const size_t qbytes = (size_t)(kJobWords + (split ? kJob1Words : 0)) * kQueue * (kBlock / 32) * sizeof(float);
-    // Deferral pays only for long walks (A/B, profiles/README.md: +1.6 % on config 5,
-    // sigma_t T = 2000; -6 % / -10 % / -30 % on configs 3, 2, 4): on by default when
-    // sigma_t (t1 - min tau_e) >= 1000; DTS_DEFER=0/1 overrides
-    float tmin = d.em_t[0];
-    for (int e = 1; e < d.n_emitters; ++e) tmin = std::fmin(tmin, d.em_t[e]);
-    bool want_defer = (double)s->S.sigma_t * ((double)d.t1 - tmin) >= 1000.0;
+    // Deferral is opt-in (DTS_DEFER=1): since the immediate kernels run 896-thread
+    // CTAs without spills they are as fast or faster on every config (A/B,
+    // profiles/README.md: config 5 2.93e10 vs 2.91e10, config 3 2.83e10 vs 2.59e10)
+    bool want_defer = false;
     const char* dv = getenv("DTS_DEFER");
     if (dv && (dv[0] == '0' || dv[0] == '1')) want_defer = dv[0] == '1';
     const bool defer = want_defer && !d_hist_sq &&
