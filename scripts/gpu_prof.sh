@@ -1,8 +1,6 @@
 # bench lines (c5 full with cpu baseline, c3) + ncu full captures of the render kernel (tag = $1)
 TAG=${1:-dev}
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench_c5_$TAG.json 2> gpurun_out/bench_c5_$TAG.err; echo "bench5 rc=$?"
-timeout 600 python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_c3_$TAG.json 2> gpurun_out/bench_c3_$TAG.err; echo "bench3 rc=$?"
 for spec in "5 16" "3 4"; do
   set -- $spec
   PCMD="python bench.py --config $1 --spp $2 --steps 1 --warmup 3 --no-cpu-baseline"
