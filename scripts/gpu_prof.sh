@@ -1,4 +1,4 @@
-# bench lines (c5 full with cpu baseline, c3) + ncu full captures of the render kernel (tag = $1)
+# ncu --set full captures of the render kernel, config 5 at spp 16 and config 3 at spp 4 (tag = $1)
 TAG=${1:-dev}
 mkdir -p gpurun_out
 for spec in "5 16" "3 4"; do
