@@ -745,20 +745,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
                                          : intersect_inside<SH, WALLS>(S, ps.x, ww, lo, hi, face);
   // render kernel: non-empty connections of medium/wall vertices are queued (df)
   const bool defer = DEFER && !DBG && ps.kind != KIND_CAMERA;
-#ifdef DTS_MEASURE_MAYCONNECT
-  if (!DBG && SH == DTS_MEDIUM_BOX && ps.kind == KIND_MEDIUM) {
-    // experiment: fraction of medium vertices whose connection could be non-empty
-    // by the bound  R_m - E <= |farthest box corner from x| + |farthest box corner from xe|
-    const float fx = fmaxf(ps.x.x - S.bmin[0], S.bmax[0] - ps.x.x);
-    const float fy = fmaxf(ps.x.y - S.bmin[1], S.bmax[1] - ps.x.y);
-    const float fz = fmaxf(ps.x.z - S.bmin[2], S.bmax[2] - ps.x.z);
-    const float ex_ = fmaxf(fabsf(xe.x - S.bmin[0]), fabsf(S.bmax[0] - xe.x));
-    const float ey_ = fmaxf(fabsf(xe.y - S.bmin[1]), fabsf(S.bmax[1] - xe.y));
-    const float ez_ = fmaxf(fabsf(xe.z - S.bmin[2]), fabsf(S.bmax[2] - xe.z));
-    const float bound = sqrtf(fx * fx + fy * fy + fz * fz) + sqrtf(ex_ * ex_ + ey_ * ey_ + ez_ * ez_);
-    if (d2f(ps.resM - S.dt) <= bound) atomicAdd(&dts::g_dts_check_fail, 1ull);
-  }
-#endif
+
   bool want_job = false;
   float job_dlo = 0.0f, job_width = 0.0f;
   float clo = lo, chi = hi;
