@@ -156,25 +156,30 @@ def run_gpu(args):
 
     kern_ms = []
 
-    from paper_2402_03106_b200.shard import render_sharded
+    from paper_2402_03106_b200.shard import render_sharded, render_sharded_p2p
 
     def step(i, timed):
-        hist.zero_()
         sc.table_build(stream=stream)
 
-        def render_range(b, e):  # this rank's disjoint Philox key range
+        def render_range(b, e, target=None):  # this rank's disjoint Philox key range
             assert (b, e) == (sb, se)
             if timed:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            sc.render(spp, c["seed"] + 1000 * i, b, e, hist, None, ctr if timed else None, stream)
+            sc.render(spp, c["seed"] + 1000 * i, b, e, hist if target is None else target, None,
+                      ctr if timed else None, stream)
             if timed:
                 e1.record(stream)
                 kern_ms.append((e0, e1))
 
-        # render the shard, then ONE reduce of the histograms to rank 0 (NCCL over NVLink)
-        render_sharded(render_range, spp, hist)
+        if args.reduce == "p2p":
+            # fused: every rank's kernel adds straight into rank 0's histogram (peer memory)
+            render_sharded_p2p(render_range, spp, hist)
+        else:
+            # render the shard, then ONE reduce of the histograms to rank 0 (NCCL over NVLink)
+            hist.zero_()
+            render_sharded(render_range, spp, hist)
 
     for i in range(args.warmup):
         step(i, False)
@@ -239,7 +244,8 @@ def run_gpu(args):
                 "workload": c["name"], "config_index": args.config, "pixels": c["width"] * c["height"],
                 "bins": c["n_bins"], "spp": spp, "spp_mode": c["spp_mode"], "direction_mode": mode,
                 "paths_per_step": paths_per_step, "vertices_per_step": verts_per_step,
-                "parallelism": f"sample-range shards x{world}" + (" + NCCL reduce" if world > 1 else ""),
+                "parallelism": f"sample-range shards x{world}" + (
+                    (" + fused peer-memory REDs" if args.reduce == "p2p" else " + NCCL reduce") if world > 1 else ""),
                 "l2": "histogram (%.2f GB) > L2 is re-zeroed every step" % (hist.numel() * 4 / 1e9),
             },
             "paths_per_s": paths_per_step / (ms / args.steps * 1e-3),
@@ -267,6 +273,9 @@ def run_gpu(args):
                 "source": "profiles/mse_vs_oracle_r01.json (scripts/mse_vs_oracle.py)"}
         print(json.dumps(line), flush=True)
     if world > 1:
+        from paper_2402_03106_b200.shard import release_peer_histograms
+        release_peer_histograms()
+        torch.cuda.synchronize()
         dist.barrier()
         dist.destroy_process_group()
 
@@ -408,6 +417,9 @@ def main():
     ap.add_argument("--strategy", choices=["darts", "vanilla", "da_only", "eda_only"], default=None,
                     help="estimator (default: the config's, DARTS); other values are comparison runs, not bench lines")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--reduce", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1: one NCCL reduce after the renders (default), or p2p: every rank's render "
+                         "kernel adds into rank 0's histogram through CUDA IPC peer memory (no reduce)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--spp", type=int, default=None, help="override spp (profiling runs only; not a bench line)")

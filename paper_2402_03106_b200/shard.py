@@ -38,3 +38,62 @@ def render_sharded(render_range: Callable[[int, int], None], spp: int, hist, cou
         if counters is not None:
             dist.all_reduce(counters)
     return b, e
+
+
+_PEER_CACHE: dict = {}
+
+
+def peer_histogram(hist, dst: int = 0):
+    """The histogram every rank renders into for the fused reduce: rank dst's
+    own tensor there, elsewhere the same device memory mapped through CUDA IPC
+    (peer memory over NVLink / NVSwitch on a multi-GPU box).  Collective; the
+    mapping is made once per tensor."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    key = (hist.data_ptr(), hist.numel(), dst)
+    if key in _PEER_CACHE:
+        return _PEER_CACHE[key]
+    obj = [reduce_tensor(hist) if dist.get_rank() == dst else None]
+    dist.broadcast_object_list(obj, src=dst)
+    if dist.get_rank() == dst:
+        target = hist
+    else:
+        fn, args = obj[0]
+        target = fn(*args)
+    _PEER_CACHE[key] = target
+    return target
+
+
+def release_peer_histograms() -> None:
+    """Drops this process's peer mappings (before the producer rank exits)."""
+    _PEER_CACHE.clear()
+
+
+def render_sharded_p2p(render_range: Callable, spp: int, hist, counters=None, dst: int = 0, zero: bool = True):
+    """Fused render + reduce: each rank's render kernel adds its contributions
+    (fp32 REDs) directly into rank dst's histogram through peer memory, so no
+    reduce collective follows -- the transfer overlaps the render path by path.
+    ``render_range(begin, end, target)`` must render into ``target``.  With
+    ``zero`` rank dst clears its histogram first (every rank waits for it).
+    rank dst's ``hist`` holds the sum when this returns (every rank synchronises
+    and meets at a barrier); the other ranks' ``hist`` are untouched."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    b, e = shard_range(spp, rank, world)
+    target = hist if world == 1 else peer_histogram(hist, dst)
+    if zero and rank == dst:
+        hist.zero_()
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+    render_range(b, e, target)
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        if counters is not None:
+            dist.all_reduce(counters)
+    return b, e
