@@ -21,7 +21,9 @@
  *
  * Conventions (all calls):
  *  - lengths are times: c = eta = 1 (E3).
- *  - "device" pointers are CUDA global-memory pointers of the current device;
+ *  - "device" pointers are CUDA global-memory pointers of the current device
+ *    (d_hist may also be peer memory mapped into it, e.g. another GPU's
+ *    histogram through CUDA IPC for a fused render + reduce);
  *    "host" pointers are ordinary (pageable or pinned) CPU memory.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Device-side calls are asynchronous on that stream unless stated.
