@@ -130,6 +130,21 @@ __device__ __forceinline__ u4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, u
 __device__ __forceinline__ float mant01(uint32_t m23) { return __uint_as_float(0x3f800000u | m23) - 1.0f; }
 __device__ __forceinline__ float unif(uint32_t r) { return mant01(r >> 9); }
 
+// Small integer <-> float conversions on the FMA/ALU pipes instead of the XU
+// pipe (I2F/F2I share it with MUFU, ~60 % busy in the DARTS vertex):
+// u23f(x) = x exactly for x <= 2^23; f2u23(x) = floor(x) for 0 <= x < 2^23.
+#ifndef DTS_MAGIC_CVT
+#define DTS_MAGIC_CVT 0
+#endif
+__device__ __forceinline__ float u23f(uint32_t x) {
+  if (DTS_MAGIC_CVT) return __uint_as_float(0x4B000000u + x) - 8388608.0f;
+  return (float)x;
+}
+__device__ __forceinline__ uint32_t f2u23(float x) {
+  if (DTS_MAGIC_CVT) return __float_as_uint(__fadd_rd(x, 8388608.0f)) - 0x4B000000u;
+  return (uint32_t)x;
+}
+
 // ----------------------------------------------------------------- accurate small-argument helpers
 // -ln(1 - x) for x in [0, 1): series x + x^2/2 + x^3/3 below 1/64 (relative
 // truncation error < x^3/4 < 1e-6), MUFU lg2 above (relative error < 1e-5).
@@ -160,7 +175,7 @@ __device__ __forceinline__ float fexp(float x) { return exp2f(x * kLog2e); }
 // the caller, so directions near the pole (HG with g = 0.9) keep fp32 accuracy.
 __device__ __forceinline__ f3 from_frame(f3 n, float opc, float omc, float phi) {
   const float sign = copysignf(1.0f, n.z);
-  const float a = -1.0f / (sign + n.z);
+  const float a = __fdividef(-1.0f, sign + n.z);  // sign + n.z in [1, 2]
   const float b = n.x * n.y * a;
   const f3 b1 = mk(1.0f + sign * n.x * n.x * a, sign * b, -sign * n.x);
   const f3 b2 = mk(b, sign + n.y * n.y * a, -n.y);
@@ -554,8 +569,9 @@ __device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_
                      S.strategy != DTS_STRATEGY_DA_ONLY;
   MixDir m;
   m.gamma = valid ? __fdividef(ratio, ratio + S.alpha) : 0.0f;
-  const int ir = min((int)(ratio * S.nr_f), S.nr - 1);
-  const int is = min(max((int)ls, 0), S.ns - 1);
+  // (ir, is only address the table when valid: ratio in [0, 1), ls in [0, ns))
+  const int ir = min((int)f2u23(ratio * S.nr_f), S.nr - 1);
+  const int is = min((int)f2u23(ls), S.ns - 1);
   const uint16_t* qc = tab + (valid ? (size_t)(ir * S.ns + is) * DTS_TABLE_COS_BINS : 0);
   DTS_CHECK((size_t)(qc - tab) + DTS_TABLE_COS_BINS <= S.table_n);
   const f3 axis = cv * __fdividef(1.0f, C);
@@ -585,27 +601,29 @@ __device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_
     for (int st = 128; st > 0; st >>= 1)
       if (qload<SMEM>(qc, j + st) <= Ti) j += st;
   }
-  const float T = (float)(r5 >> 9) * (1.0f / 128.0f);
-  float qa = (float)qload<SMEM>(qc, j);
-  float qb = j == 255 ? 65536.0f : (float)qload<SMEM>(qc, j + 1);
-  const float iq = __fdividef(1.0f, qb - qa);
+  // T - q_j and q_{j+1} - T in units of 2^-7 are exact 23-bit integers
+  const uint32_t T7 = r5 >> 9;  // 128 T
+  uint32_t qa = qload<SMEM>(qc, j);
+  uint32_t qb = j == 255 ? 65536u : qload<SMEM>(qc, j + 1);
+  const float iq = __fdividef(1.0f / 128.0f, u23f(qb - qa));
   // HG about w_{k-1}
   float opc, omc;
   hg_sample(S, u5, opc, omc);
   {  // EDA: cos = -1 + (j + frac)/128: 1 + cos and 1 - cos from the integer parts (selected, not branched)
-    const float eo = ((float)j + (T - qa) * iq) * (1.0f / 128.0f);
-    const float em = ((float)(255 - j) + (qb - T) * iq) * (1.0f / 128.0f);
+    const float fj = u23f((uint32_t)j);
+    const float eo = (fj + u23f(T7 - (qa << 7)) * iq) * (1.0f / 128.0f);
+    const float em = ((255.0f - fj) + u23f((qb << 7) - T7) * iq) * (1.0f / 128.0f);
     opc = m.eda ? eo : opc;
     omc = m.eda ? em : omc;
   }
   m.om = from_frame(m.eda ? axis : w, opc, omc, phi);
   if (!m.eda) {  // EDA pdf of the HG direction: bin of its cos to the emitter axis
-    const int jb = min(max((int)floorf((dot(m.om, axis) + 1.0f) * 128.0f), 0), 255);
+    const int jb = (int)f2u23(fminf(fmaxf((dot(m.om, axis) + 1.0f) * 128.0f, 0.0f), 255.0f));
     DTS_CHECK(jb >= 0 && jb < 256);
-    qa = (float)qload<SMEM>(qc, jb);
-    qb = jb == 255 ? 65536.0f : (float)qload<SMEM>(qc, jb + 1);
+    qa = qload<SMEM>(qc, jb);
+    qb = jb == 255 ? 65536u : qload<SMEM>(qc, jb + 1);
   }
-  m.p_eda = valid ? (qb - qa) * (128.0f / 65536.0f / (2.0f * kPi)) : 0.0f;
+  m.p_eda = valid ? u23f(qb - qa) * (128.0f / 65536.0f / (2.0f * kPi)) : 0.0f;
   m.p_hg = hg_eval(S, dot(m.om, w));
   m.p_mix = m.gamma * m.p_eda + (1.0f - m.gamma) * m.p_hg;
   return m;
@@ -795,7 +813,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       float a_lo = clo;
       if (S.s_excess > 0.0f) {
         const float Se = C + S.s_excess;
-        a_lo = fmaxf(a_lo, (Se - C) * (Se + C) / (2.0f * (Se - q)));
+        a_lo = fmaxf(a_lo, __fdividef((Se - C) * (Se + C), 2.0f * (Se - q)));
       }
       float ia0 = 0.f, ib0 = 0.f, ia1 = 0.f, ib1 = 0.f;
       int ni = 0;
@@ -829,11 +847,11 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
         const float v = u7 * Z;
         const bool second = (m0 <= 0.0f) || (ni == 2 && !(v < m0));
         const float ia = second ? ia1 : ia0, ib = second ? ib1 : ib0;
-        float up = second ? (v - m0) / m1 : v / m0;
+        float up = second ? __fdividef(v - m0, m1) : __fdividef(v, m0);
         up = fminf(up, 0.99999994f);
         const float span = one_m_exp(S.sigma_t * (ib - ia));
         t = ia + neg_log1m2(up * span, fmaf(up, fexp(-S.sigma_t * (ib - ia)), 1.0f - up)) * S.inv_sigma_t;
-        pt = S.sigma_t * fexp(-S.sigma_t * (t - clo)) / Z;
+        pt = __fdividef(S.sigma_t * fexp(-S.sigma_t * (t - clo)), Z);
       }
     }
     if (ok) {

@@ -19,6 +19,7 @@
 
 #include "../../include/dts.h"
 #include "dts_device.cuh"
+#include "fastdiv.h"
 
 using namespace dts;
 
@@ -193,6 +194,8 @@ struct RenderParams {
   uint32_t flush1_at;             // stage-1 queue length that triggers a batch (SPLIT)
   float* qover;                   // DEFER: global overflow queue slots, kQueue x (kJobWords + kJob1Words) per warp
   uint32_t refill_k;              // idle lane-iterations that trigger a refill
+  uint32_t div32;                 // 1: work indices, sample indices + B fit 32 bits (fast divisions)
+  FastDiv fd_ns, fd_npix, fd_cw, fd_b;  // division by n_s, npix, cw, n_bins (fastdiv.h)
 };
 
 #ifndef DTS_BLOCK
@@ -238,15 +241,16 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   uint64_t id;
   const uint64_t Npix = (uint64_t)S.width * (uint64_t)S.height;
   float inv_n;
+  uint32_t cx, cy;
   if (S.spp_mode == DTS_SPP_PER_CELL) {
     // issue order (b descending, pixel, s): long late-bin walks first
     uint64_t sl, rest;
-    if (P.total <= 0xFFFFFFFFull) {  // 32-bit divisions when the launch allows
-      const uint32_t w32 = (uint32_t)widx, ns32 = (uint32_t)P.n_s;
-      sl = w32 % ns32;
-      rest = w32 / ns32;
-      pl = (uint32_t)rest % P.npix;
-      b = B - 1u - (uint32_t)rest / P.npix;
+    if (P.div32) {  // 32-bit divisions by launch invariants when the launch allows
+      uint32_t sl32, pl32;
+      const uint32_t rest32 = fastdiv_divmod((uint32_t)widx, P.fd_ns, sl32);
+      b = B - 1u - fastdiv_divmod(rest32, P.fd_npix, pl32);
+      sl = sl32;
+      pl = pl32;
     } else {
       sl = widx % P.n_s;
       rest = widx / P.n_s;
@@ -256,15 +260,15 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     s = P.s_begin + sl;
     inv_n = 1.0f / (float)P.spp;
   } else {
-    if (P.total <= 0xFFFFFFFFull) {
-      pl = (uint32_t)widx % P.npix;
-      s = P.s_begin + (uint32_t)widx / P.npix;
+    if (P.div32) {
+      s = P.s_begin + fastdiv_divmod((uint32_t)widx, P.fd_npix, pl);
     } else {
       pl = (uint32_t)(widx % P.npix);
       s = P.s_begin + widx / P.npix;
     }
   }
-  const uint32_t px = (uint32_t)S.crop[0] + pl % P.cw, py = (uint32_t)S.crop[1] + pl / P.cw;
+  cy = fastdiv_divmod(pl, P.fd_cw, cx);
+  const uint32_t px = (uint32_t)S.crop[0] + cx, py = (uint32_t)S.crop[1] + cy;
   const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
   float scale = 1.0f;
   if (S.spp_mode == DTS_SPP_PER_CELL) {
@@ -288,8 +292,11 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
     // R21: bin = (s + o_p) mod B with a per-pixel Philox offset
     const u4 o = philox_rk((uint32_t)p, (uint32_t)(p >> 32), 0xFFFFFFFEu, 0u, S.rk);
     const uint32_t op = min((uint32_t)((float)B * unif(o.a)), B - 1u);
-    b = (uint32_t)((s + op) % B);
-    const uint32_t rel = (b + B - op) % B;
+    // b = (s + op) mod B; the cell's rank rel = (b - op) mod B = s mod B
+    uint32_t rel;
+    if (P.div32) fastdiv_divmod((uint32_t)s, P.fd_b, rel);
+    else rel = (uint32_t)(s % B);
+    b = rel + op >= B ? rel + op - B : rel + op;
     const uint32_t n_pb = P.spp_div_b + (rel < P.spp_mod_b ? 1u : 0u);
     inv_n = 1.0f / (float)n_pb;
     id = s * Npix + p;
@@ -305,8 +312,8 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   PathState& ps = pc.ps;
   ps.e = e;
   if (S.camera_kind == DTS_CAMERA_PINHOLE) {
-    const float sx = (2.0f * ((float)px + unif(a.a)) / (float)S.width - 1.0f) * S.tan_half * S.aspect;
-    const float sy = (1.0f - 2.0f * ((float)py + unif(a.b)) / (float)S.height) * S.tan_half;
+    const float sx = (__fdividef(2.0f * ((float)px + unif(a.a)), (float)S.width) - 1.0f) * S.tan_half * S.aspect;
+    const float sy = (1.0f - __fdividef(2.0f * ((float)py + unif(a.b)), (float)S.height)) * S.tan_half;
     f3 w = mk(S.fwd[0] + sx * S.right[0] + sy * S.upc[0], S.fwd[1] + sx * S.right[1] + sy * S.upc[1],
               S.fwd[2] + sx * S.right[2] + sy * S.upc[2]);
     ps.w = w * rsqrtf(dot(w, w));
@@ -719,7 +726,7 @@ __device__ __forceinline__ int vanilla_splat(const RenderParams& P, uint32_t pl,
   DTS_CHECK((size_t)pl * S.n_bins + bin < g_check_cells);
   const float w = P.resp_w ? __ldg(P.resp_w + bin) : 1.0f;
   if (w == 0.0f) return 1;
-  atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, w * c / (float)P.spp);
+  atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, __fdividef(w * c, (float)P.spp));
   return 0;
 }
 
@@ -729,9 +736,16 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint32_t c_paths = 0, c_miss = 0, c_vert = 0, c_early = 0, c_esc = 0, c_cap = 0, c_samp = 0, c_rej = 0;
   for (uint64_t widx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; widx < P.total; widx += stride) {
-    const uint32_t pl = (uint32_t)(widx % P.npix);
-    const uint64_t s = P.s_begin + widx / P.npix;
-    const uint32_t px = (uint32_t)S.crop[0] + pl % P.cw, py = (uint32_t)S.crop[1] + pl / P.cw;
+    uint32_t pl, cx;
+    uint64_t s;
+    if (P.div32) {
+      s = P.s_begin + fastdiv_divmod((uint32_t)widx, P.fd_npix, pl);
+    } else {
+      pl = (uint32_t)(widx % P.npix);
+      s = P.s_begin + widx / P.npix;
+    }
+    const uint32_t cy = fastdiv_divmod(pl, P.fd_cw, cx);
+    const uint32_t px = (uint32_t)S.crop[0] + cx, py = (uint32_t)S.crop[1] + cy;
     const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
     const uint64_t id = s * ((uint64_t)S.width * (uint64_t)S.height) + p;
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
@@ -744,8 +758,8 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     f3 x, w;
     float beta;
     if (S.camera_kind == DTS_CAMERA_PINHOLE) {
-      const float sx = (2.0f * ((float)px + unif(a.a)) / (float)S.width - 1.0f) * S.tan_half * S.aspect;
-      const float sy = (1.0f - 2.0f * ((float)py + unif(a.b)) / (float)S.height) * S.tan_half;
+      const float sx = (__fdividef(2.0f * ((float)px + unif(a.a)), (float)S.width) - 1.0f) * S.tan_half * S.aspect;
+      const float sy = (1.0f - __fdividef(2.0f * ((float)py + unif(a.b)), (float)S.height)) * S.tan_half;
       w = mk(S.fwd[0] + sx * S.right[0] + sy * S.upc[0], S.fwd[1] + sx * S.right[1] + sy * S.upc[1],
              S.fwd[2] + sx * S.right[2] + sy * S.upc[2]);
       w = w * rsqrtf(dot(w, w));
@@ -792,7 +806,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
         float sp, cp;
         __sincosf(2.0f * kPi * u6, &sp, &cp);
         const float sign = copysignf(1.0f, n.z);
-        const float aa = -1.0f / (sign + n.z);
+        const float aa = __fdividef(-1.0f, sign + n.z);
         const float bq = n.x * n.y * aa;
         const f3 b1 = mk(1.0f + sign * n.x * n.x * aa, sign * bq, -sign * n.x);
         const f3 b2 = mk(bq, sign + n.y * n.y * aa, -n.y);
@@ -836,7 +850,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
       } else {
         c = beta * (S.wall_albedo[face] * (1.0f / kPi)) * fmaxf(0.0f, dot(inward_normal(face), we));
       }
-      c *= segment_tr<SH, WALLS>(S, x, xe, C, we) * ek / (C * C);
+      c *= segment_tr<SH, WALLS>(S, x, xe, C, we) * __fdividef(ek, C * C);
       if (S.r_excl > 0.0f && C < S.r_excl) c = 0.0f;
       if (c != 0.0f && isfinite(c)) {
         ++c_samp;
@@ -1269,6 +1283,13 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   P.spp = spp;
   P.npix = (uint32_t)npix;
   P.cw = (uint32_t)(d.crop[2] - d.crop[0]);
+  P.div32 = (sb + ns + (uint64_t)d.n_bins <= 0xFFFFFFFFull &&
+             npix * ns * ((darts && d.spp_mode == DTS_SPP_PER_CELL) ? (uint64_t)d.n_bins : 1u) <= 0xFFFFFFFFull)
+                ? 1u : 0u;
+  P.fd_ns = fastdiv_make((uint32_t)std::min<uint64_t>(ns, 0xFFFFFFFFull));
+  P.fd_npix = fastdiv_make((uint32_t)npix);
+  P.fd_cw = fastdiv_make(P.cw);
+  P.fd_b = fastdiv_make((uint32_t)d.n_bins);
   P.spp_div_b = (uint32_t)(spp / (uint64_t)d.n_bins);
   P.spp_mod_b = (uint32_t)(spp % (uint64_t)d.n_bins);
   cudaStream_t st = (cudaStream_t)stream;
