@@ -491,7 +491,7 @@ def _ball_single_scatter(c, edges):
 def cfg1_runs(oracle):
     c = I.as_f32(I.config(1))
     q, _ = oracle.build_table(c)
-    runs = [oracle.render(c, q, 2048, seed, n_orders=1, sq=False) for seed in range(100, 108)]
+    runs = [oracle.render(c, q, 2048, seed, n_orders=2, sq=False) for seed in range(100, 108)]
     return c, q, runs
 
 
@@ -505,6 +505,70 @@ def test_single_scatter_closed_form(cfg1_runs):
     assert np.mean(np.abs(z[1:]) < 3) >= 0.97, z
     # aggregate over bins 1..127 to 0.5 %
     assert m[1:].sum() == pytest.approx(ref[1:].sum(), rel=5e-3)
+
+
+def _double_scatter(ss, st, R, t):
+    """Order-2 fluence phi_2(R, t) of a unit isotropic pulse in an infinite
+    isotropically scattering medium (c = 1), from the order recursion
+    phi_{n+1} = sigma_s phi_n (*) K, K(y, tau) = e^{-sigma_t tau} delta(tau - |y|) / (4 pi |y|^2),
+    written for radial functions ((f (*) g)(R) = 2 pi / R int rho f(rho) int_{|R-rho|}^{R+rho} s g(s) ds drho):
+      phi_2(R, t) = sigma_s^2 e^{-sigma_t t} / (8 pi R) int_0^t ds [F(b) - F(a)] / (s tau),
+    tau = t - s, a = |R - s|, b = min(R + s, tau), F(rho) = (tau + rho) ln(tau + rho) + (tau - rho) ln(tau - rho)
+    (F is the antiderivative in rho of ln((tau + rho) / (tau - rho)), the order-1 factor).  The same
+    recursion applied to phi_0 gives the order-1 closed form of _ball_single_scatter (checked below)."""
+    def xlogx(x):
+        return x * math.log(x) if x > 0 else 0.0
+
+    def f(s):
+        tau = t - s
+        a, b = abs(R - s), min(R + s, tau)
+        if not a < b:
+            return 0.0
+        F = lambda r: xlogx(tau + r) + xlogx(tau - r)
+        return (F(b) - F(a)) / (s * tau)
+
+    lo, hi = 0.0, t
+    val = integrate.quad(f, lo, hi, points=[abs(t - R) / 2, (t + R) / 2, R], limit=200)[0]
+    return ss * ss * math.exp(-st * t) * val / (8 * math.pi * R)
+
+
+def test_double_scatter_recursion_reproduces_order_one():
+    """The radial-convolution recursion of _double_scatter, applied to phi_0,
+    reproduces the order-1 closed form (guards the recursion's factors)."""
+    ss, st, R = 0.9, 1.0, 2.0
+    for t in (2.5, 4.0, 9.0):
+        # phi_1 = sigma_s e^{-st t} / (8 pi R) int ds / (s (t - s)) over s in [(t - R)/2, (t + R)/2]
+        val = integrate.quad(lambda s: 1.0 / (s * (t - s)), (t - R) / 2, (t + R) / 2)[0]
+        rec = ss * math.exp(-st * t) * val / (8 * math.pi * R)
+        ref = ss * math.exp(-st * t) * math.log((t + R) / (t - R)) / (4 * math.pi * R * t)
+        assert rec == pytest.approx(ref, rel=1e-10)
+
+
+def test_double_scatter_quadrature(cfg1_runs):
+    """Order 2 of the whole oracle estimator (tally of connections from the
+    second vertex) on config 1 against the bin-integrated, ball-averaged order-2
+    fluence of _double_scatter: pins the absolute value of a multiple-scattering
+    order, not only its agreement with the vanilla estimator."""
+    c, q, runs = cfg1_runs
+    ss, st = c["sigma_s"], c["sigma_s"] + c["sigma_a"]
+    L, a = 2.0, c["det_radius"]
+    xr, wr = np.polynomial.legendre.leggauss(6)
+    Rs = L + a * xr
+    ws = a * wr * np.pi * Rs * (a * a - (Rs - L) ** 2) / L / (4 / 3 * np.pi * a ** 3)
+    edges = np.linspace(c["t0"], c["t1"], c["n_bins"] + 1)
+    xt, wt = np.polynomial.legendre.leggauss(6)
+    ref = np.zeros(c["n_bins"])
+    for j, (lo, hi) in enumerate(zip(edges[:-1], edges[1:])):
+        h = 0.5 * (hi - lo)
+        for tn, tw in zip(0.5 * (lo + hi) + h * xt, h * wt):
+            ref[j] += tw * sum(wR * _double_scatter(ss, st, R, tn) for R, wR in zip(Rs, ws))
+    # order-2 tallies are heavier-tailed than order 1: compare 4-bin windows (bins 4..127)
+    o2 = np.array([r["order_hist"][1, 0, 0] for r in runs])[:, 4:].reshape(len(runs), -1, 4).sum(-1)
+    ref = ref[4:].reshape(-1, 4).sum(-1)
+    m, se = o2.mean(0), o2.std(0, ddof=1) / math.sqrt(len(o2))
+    z = (m - ref) / se
+    assert np.mean(np.abs(z) < 3) >= 0.9, z
+    assert m.sum() == pytest.approx(ref.sum(), rel=1e-2)
 
 
 def _hg(g, mu):
