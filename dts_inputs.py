@@ -82,7 +82,7 @@ _DEFAULTS = dict(
     wall_mask=0, wall_albedo=(0.0,) * 6, look_at=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0),
     fov_y_deg=45.0, det_radius=0.0, strategy="darts", n_ris=8, alpha=0.5,
     parity_r_excl=0.0, parity_s_excess=0.0, table_nr=16, table_ns=16,
-    crop=None, table_smin=None, table_smax=None, response=None,
+    crop=None, table_smin=None, table_smax=None, response=None, mesh=None,
     conn_sampling="exp",   # "exp": truncated exponential P of S; "uniform": ablation
 )
 
@@ -150,6 +150,56 @@ def response_config(**overrides) -> dict:
     c = config(4, t0=3.0, t1=9.0, n_bins=120, spp=64, spp_mode="response", name="cfg4_two_peak_response")
     c.update(overrides)
     c["response"] = two_peak_response(c["n_bins"], c["t0"], c["t1"])
+    return c
+
+
+# ----------------------------------------------------------------------------
+# triangle meshes (R32, R33): synthetic stand-ins for the
+# paper's GLOSSY DRAGON and STAIRCASE scenes (Table 1),
+# whose geometry is not available: a glossy icosphere and a plastic staircase.
+def icosphere(center, radius, subdiv: int) -> np.ndarray:
+    """Triangles (n, 3, 3) of a subdivided icosahedron, vertices projected on the sphere."""
+    t = (1.0 + 5 ** 0.5) / 2.0
+    v = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+         (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    f = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2),
+         (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11),
+         (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    tris = [[np.asarray(v[i], float) / np.linalg.norm(v[i]) for i in tri] for tri in f]
+    for _ in range(subdiv):
+        nxt = []
+        for a, b, c in tris:
+            ab, bc, ca = [(p + q) / np.linalg.norm(p + q) for p, q in ((a, b), (b, c), (c, a))]
+            nxt += [[a, ab, ca], [b, bc, ab], [c, ca, bc], [ab, bc, ca]]
+        tris = nxt
+    return np.asarray(center, float) + radius * np.asarray(tris)
+
+
+def staircase(x0, x1, y0, z0, n_steps: int, rise: float, run: float) -> np.ndarray:
+    """Triangles of n steps rising along +y and receding along +z (two per tread, two per riser)."""
+    out = []
+    for k in range(n_steps):
+        ylo, yhi = y0 + k * rise, y0 + (k + 1) * rise
+        za, zb = z0 + k * run, z0 + (k + 1) * run
+        riser = [(x0, ylo, za), (x1, ylo, za), (x1, yhi, za), (x0, yhi, za)]
+        tread = [(x0, yhi, za), (x1, yhi, za), (x1, yhi, zb), (x0, yhi, zb)]
+        for q in (riser, tread):
+            out += [[q[0], q[1], q[2]], [q[0], q[2], q[3]]]
+    return np.asarray(out, float)
+
+
+def mesh_config(**overrides) -> dict:
+    """Config 6: config 4's fog cube with walls and two
+    emitters, plus a glossy icosphere (rho 0.8, ks 0.9, Phong n 40; 320
+    triangles) and a plastic staircase (rho 0.6, ks 0.25, n 15; 16 triangles),
+    time-gated in two bins of width 0.1."""
+    ico = icosphere((0.35, -0.45, 0.2), 0.35, 2)
+    st = staircase(-0.9, -0.1, -0.98, -0.2, 4, 0.2, 0.25)
+    tris = np.concatenate([ico, st]).astype(np.float32).astype(np.float64)
+    mat = np.concatenate([np.zeros(len(ico), np.int32), np.ones(len(st), np.int32)])
+    c = config(4, t0=5.0, t1=5.2, n_bins=2, spp=64, width=256, height=256, name="cfg6_mesh_glossy_stairs", seed=6)
+    c["mesh"] = dict(tris=tris.reshape(-1, 9), tri_mat=mat, mats=[(0.8, 0.9, 40.0), (0.6, 0.25, 15.0)])
+    c.update(overrides)
     return c
 
 

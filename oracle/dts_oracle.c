@@ -199,6 +199,14 @@ static void segment_medium(const or_scene* sc, const double p[3], const double x
   sub3(xe, p, dvec);
   double r = norm3(dvec);
   *vis = 1.0;
+  if (sc->n_tris > 0) { /* R32: a triangle on the segment occludes it */
+    double dir[3] = {dvec[0] / r, dvec[1] / r, dvec[2] / r}, tm;
+    if (or_mesh_hit(sc, p, dir, r, &tm) >= 0) {
+      *vis = 0.0;
+      *len = r;
+      return;
+    }
+  }
   if (sc->medium_shape == OR_MEDIUM_INFINITE) {
     *len = r;
     return;
@@ -218,6 +226,109 @@ static void segment_medium(const or_scene* sc, const double p[3], const double x
 static void inward_normal(int face, double n[3]) {
   n[0] = n[1] = n[2] = 0.0;
   n[face / 2] = (face & 1) ? -1.0 : 1.0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* triangle meshes (R32, R33; opaque surfaces of PAPER.md:105, 221, 301)       */
+/* Moller-Trumbore ray/triangle distance (edges inclusive), -1 for no hit */
+static double tri_hit(const double* v, const double o[3], const double d[3]) {
+  double e1[3], e2[3], s[3], p[3], qv[3];
+  sub3(v + 3, v, e1);
+  sub3(v + 6, v, e2);
+  cross3(d, e2, p);
+  double det = dot3(e1, p);
+  if (det == 0.0) return -1.0;
+  double inv = 1.0 / det;
+  sub3(o, v, s);
+  double u = dot3(s, p) * inv;
+  if (u < 0.0 || u > 1.0) return -1.0;
+  cross3(s, e1, qv);
+  double vv = dot3(d, qv) * inv;
+  if (vv < 0.0 || u + vv > 1.0) return -1.0;
+  return dot3(e2, qv) * inv;
+}
+
+/* nearest hit over every triangle (no acceleration structure) */
+int or_mesh_hit(const or_scene* sc, const double o[3], const double d[3], double t_max, double* t) {
+  int best = -1;
+  double tb = t_max;
+  for (int i = 0; i < sc->n_tris; ++i) {
+    double th = tri_hit(sc->tris + 9 * i, o, d);
+    if (th > 0.0 && th < tb) {
+      tb = th;
+      best = i;
+    }
+  }
+  if (best >= 0) *t = tb;
+  return best;
+}
+
+/* geometric normal turned to the side the incident direction w comes from */
+static void side_normal(const or_scene* sc, int tri, const double w[3], double n[3]) {
+  const double* v = sc->tris + 9 * tri;
+  double e1[3], e2[3];
+  sub3(v + 3, v, e1);
+  sub3(v + 6, v, e2);
+  cross3(e1, e2, n);
+  normalize3(n);
+  if (dot3(n, w) > 0.0) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; }
+}
+
+/* R32: f = rho [(1 - ks) / pi + ks (n + 2) / (2 pi) max(0, wo . r)^n] on the
+ * incident side, r = w - 2 (w . n_s) n_s the mirror direction (Lambertian for
+ * ks = 0, normalised Phong lobe for ks = 1, "plastic" in between). */
+double or_bsdf_eval(const or_scene* sc, int tri, const double w[3], const double wo[3]) {
+  double n[3], r[3];
+  side_normal(sc, tri, w, n);
+  if (!(dot3(wo, n) > 0.0)) return 0.0;
+  const double* m = sc->mats[sc->tri_mat[tri]];
+  double wn = dot3(w, n);
+  for (int i = 0; i < 3; ++i) r[i] = w[i] - 2.0 * wn * n[i];
+  double ca = fmax(0.0, dot3(wo, r));
+  return m[0] * ((1.0 - m[1]) / OR_PI + m[1] * (m[2] + 2.0) / (2.0 * OR_PI) * pow(ca, m[2]));
+}
+
+/* R32 sampling: u4 < ks picks the lobe (cos alpha = u5^{1/(n+1)} about r),
+ * else the cosine hemisphere (cos theta = sqrt(1 - u5) about n_s); phi = 2 pi u6.
+ * One-sample MIS over both: weight f cos / ((1 - ks) cos / pi + ks p_lobe). */
+double or_bsdf_sample(const or_scene* sc, int tri, const double w[3], double u4, double u5, double u6,
+                      double wo[3]) {
+  double n[3], r[3];
+  side_normal(sc, tri, w, n);
+  const double* m = sc->mats[sc->tri_mat[tri]];
+  double wn = dot3(w, n);
+  for (int i = 0; i < 3; ++i) r[i] = w[i] - 2.0 * wn * n[i];
+  if (u4 < m[1])
+    from_frame(r, pow(u5, 1.0 / (m[2] + 1.0)), 2.0 * OR_PI * u6, wo);
+  else
+    from_frame(n, sqrt(fmax(0.0, 1.0 - u5)), 2.0 * OR_PI * u6, wo);
+  double co = dot3(wo, n);
+  if (!(co > 0.0)) return 0.0;
+  double ca = fmax(0.0, dot3(wo, r));
+  double p = (1.0 - m[1]) * co / OR_PI + m[1] * (m[2] + 1.0) / (2.0 * OR_PI) * pow(ca, m[2]);
+  return or_bsdf_eval(sc, tri, w, wo) * co / p;
+}
+
+/* medium interval of a ray, cut at the nearest triangle (R32: case II of
+ * PAPER.md:301, "the closest surface distance t_s") */
+static int scene_intersect(const or_scene* sc, const double o[3], const double d[3], double* lo, double* hi,
+                           int* face) {
+  int hit = or_intersect(sc, o, d, lo, hi, face);
+  if (hit == OR_HIT_MISS || sc->n_tris == 0) return hit;
+  double tm;
+  int tri = or_mesh_hit(sc, o, d, *hi, &tm);
+  if (tri < 0) return hit;
+  *hi = tm;
+  *face = tri;
+  return OR_HIT_SURF;
+}
+
+/* R33: surface vertex at x + d t, moved OR_SURF_EPS off the triangle on the side d arrives from */
+static void surface_point(const or_scene* sc, int tri, const double x[3], const double d[3], double t,
+                          double out[3]) {
+  double n[3];
+  side_normal(sc, tri, d, n);
+  for (int i = 0; i < 3; ++i) out[i] = x[i] + d[i] * t + OR_SURF_EPS * n[i];
 }
 
 /* ------------------------------------------------------------------------- */
@@ -601,6 +712,43 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
     for (int i = 0; i < 3; ++i) wc[i] = ww[i] = b1[i] * lx + b2[i] * ly + n[i] * lz;
     ps->beta *= alb;
     if (dbg) { dbg->tech = 3; dbg->beta_dir = alb; }
+  } else if (ps->kind == OR_KIND_SURF) {
+    /* R32: surface vertex on triangle ps->face; time-checked NEE as at walls
+     * (R14) with the BSDF, then a BSDF-sampled direction for the connection
+     * and the walk */
+    double n[3];
+    side_normal(sc, ps->face, ps->w, n);
+    double Cvec[3];
+    sub3(ps->xe, ps->x, Cvec);
+    double C = norm3(Cvec);
+    double we[3] = {Cvec[0] / C, Cvec[1] / C, Cvec[2] / C};
+    double cw = dot3(n, we);
+    double arrive = ps->E + C;
+    if (cw > 0.0 && arrive >= ps->Rm && arrive < ps->RM) {
+      double len, vis;
+      segment_medium(sc, ps->x, ps->xe, &len, &vis);
+      double nee = ps->beta * or_bsdf_eval(sc, ps->face, ps->w, we) * cw * ps->Pe / (4.0 * OR_PI) * ps->Ne *
+                   vis * exp(-dv->sigma_t * len) / (C * C);
+      if (sc->parity_r_excl > 0.0 && C < sc->parity_r_excl) nee = 0.0;
+      *contrib += nee;
+      if (st && nee != 0.0) {
+        st->samples++;
+        if (sc->spp_mode == OR_SPP_RESPONSE && sc->response[ps->bin] == 0.0) st->rejected++;
+      }
+      if (dbg) dbg->nee = nee;
+      if (st && nee > 0.0) st->wall_nee++;
+    }
+    double wo[3];
+    double wgt = or_bsdf_sample(sc, ps->face, ps->w, uu(r, 4), uu(r, 5), uu(r, 6), wo);
+    if (dbg) { dbg->tech = 4; dbg->beta_dir = wgt; }
+    if (!(wgt > 0.0)) { /* sampled below the surface: the path ends */
+      if (dbg) { dbg->event = 3; dbg->terminate = 1; dbg->beta_out = ps->beta; }
+      if (st) st->escapes++;
+      return 0;
+    }
+    memcpy(wc, wo, sizeof wc);
+    memcpy(ww, wo, sizeof ww);
+    ps->beta *= wgt;
   } else {
     /* medium vertex: one-sample MIS of EDA and HG */
     double Cvec[3];
@@ -676,11 +824,11 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
   /* ---- intersection, reused by connection and walk ---- */
   double lo = 0, hi = 0;
   int face = -1;
-  int hit = or_intersect(sc, ps->x, ww, &lo, &hi, &face);
+  int hit = scene_intersect(sc, ps->x, ww, &lo, &hi, &face);
   double clo = lo, chi = hi;
   int hitc = hit, facec = face;
   if (sc->direction_mode == OR_DIR_SPLIT && ps->kind == OR_KIND_MEDIUM)
-    hitc = or_intersect(sc, ps->x, wc, &clo, &chi, &facec);
+    hitc = scene_intersect(sc, ps->x, wc, &clo, &chi, &facec);
   if (dbg) { dbg->t_lo = lo; dbg->t_hi = hi; dbg->hit = hit; dbg->face_hit = face; dbg->tc_lo = clo; dbg->tc_hi = chi; }
 
   /* ---- step 3: elliptical connection ---- */
@@ -779,6 +927,16 @@ static int darts_vertex(const or_scene* sc, const derived* dv, const uint16_t* q
       ps->face = face;
       memcpy(ps->w, ww, sizeof ps->w);
       if (dbg) { dbg->event = 2; dbg->d = hi; dbg->beta_ris = 1.0; }
+    } else if (hit == OR_HIT_SURF) {
+      /* R32/R33: the walk reaches the triangle (probability 1 - p_m) */
+      double xn[3];
+      surface_point(sc, face, ps->x, ww, hi, xn);
+      memcpy(ps->x, xn, sizeof xn);
+      ps->E += counts * hi;
+      ps->kind = OR_KIND_SURF;
+      ps->face = face;
+      memcpy(ps->w, ww, sizeof ps->w);
+      if (dbg) { dbg->event = 5; dbg->d = hi; dbg->beta_ris = 1.0; }
     } else {
       if (dbg) { dbg->event = 3; dbg->terminate = 1; dbg->beta_out = ps->beta; }
       if (st) st->escapes++;
@@ -1024,10 +1182,17 @@ static void vanilla_path(const or_scene* sc, const derived* dv, uint64_t seed, u
       double lx = rr * cos(ph), ly = rr * sin(ph), lz = sqrt(fmax(0.0, 1.0 - u5));
       for (int i = 0; i < 3; ++i) ps.w[i] = b1[i] * lx + b2[i] * ly + n[i] * lz;
       ps.beta *= sc->wall_albedo[ps.face];
+    } else if (ps.kind == OR_KIND_SURF) {
+      /* R32: lobe u3, direction u1, u2 */
+      double wo[3];
+      double wgt = or_bsdf_sample(sc, ps.face, ps.w, or_uniform(r[3]), or_uniform(r[1]), or_uniform(r[2]), wo);
+      if (!(wgt > 0.0)) { if (st) st->escapes++; break; }
+      memcpy(ps.w, wo, sizeof wo);
+      ps.beta *= wgt;
     }
     double lo, hi;
     int face;
-    int hit = or_intersect(sc, ps.x, ps.w, &lo, &hi, &face);
+    int hit = scene_intersect(sc, ps.x, ps.w, &lo, &hi, &face);
     if (hit == OR_HIT_MISS) { if (st) st->escapes++; break; }
     double counts = (sc->warped || ps.kind != OR_KIND_CAMERA) ? 1.0 : 0.0;
     double dd0[3];
@@ -1049,6 +1214,14 @@ static void vanilla_path(const or_scene* sc, const derived* dv, uint64_t seed, u
       ps.E += counts * hi;
       ps.kind = OR_KIND_WALL;
       ps.face = face;
+    } else if (hit == OR_HIT_SURF) {
+      d = hi;
+      double xn[3];
+      surface_point(sc, face, ps.x, ps.w, hi, xn);
+      memcpy(ps.x, xn, sizeof xn);
+      ps.E += counts * hi;
+      ps.kind = OR_KIND_SURF;
+      ps.face = face;
     } else {
       if (st) st->escapes++;
       break;
@@ -1065,6 +1238,10 @@ static void vanilla_path(const or_scene* sc, const derived* dv, uint64_t seed, u
     if (ps.kind == OR_KIND_MEDIUM) {
       c = ps.beta * or_hg_eval(sc->g, dot3(ps.w, we));
       if (sc->parity_s_excess > 0.0 && d + C - Cprev < sc->parity_s_excess) c = 0.0;
+    } else if (ps.kind == OR_KIND_SURF) {
+      double n[3];
+      side_normal(sc, ps.face, ps.w, n);
+      c = ps.beta * or_bsdf_eval(sc, ps.face, ps.w, we) * fmax(0.0, dot3(n, we));
     } else {
       double n[3];
       inward_normal(ps.face, n);

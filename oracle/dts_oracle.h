@@ -32,8 +32,11 @@ enum { OR_DIR_REUSE = 0, OR_DIR_SPLIT = 1 };
  * bin by a per-pixel offset (R21); RESPONSE: spp paths per pixel, bin drawn
  * with probability ~ the sensor response W (R31). */
 enum { OR_SPP_PER_CELL = 0, OR_SPP_PER_PIXEL = 1, OR_SPP_RESPONSE = 2 };
-enum { OR_KIND_CAMERA = 0, OR_KIND_MEDIUM = 1, OR_KIND_WALL = 2 };
-enum { OR_HIT_NONE = 0, OR_HIT_OPEN = 1, OR_HIT_WALL = 2, OR_HIT_MISS = 3 };
+enum { OR_KIND_CAMERA = 0, OR_KIND_MEDIUM = 1, OR_KIND_WALL = 2, OR_KIND_SURF = 3 };
+enum { OR_HIT_NONE = 0, OR_HIT_OPEN = 1, OR_HIT_WALL = 2, OR_HIT_MISS = 3, OR_HIT_SURF = 4 };
+/* R33: a surface vertex sits this far off its triangle, on the incident side */
+#define OR_SURF_EPS 1e-4
+#define OR_MAX_MATERIALS 8
 
 typedef struct {
   double sigma_s, sigma_a, g;
@@ -58,6 +61,15 @@ typedef struct {
   double table_smin, table_smax;
   int32_t conn_sampling; /* OR_CONN_* */
   const double* response; /* RESPONSE: W per bin (n_bins values >= 0), else NULL */
+  /* Triangle meshes (R32, R33; surfaces of PAPER.md:105, 221, 301): thin,
+   * two-sided, opaque triangles inside the medium.  tris: n_tris x 9 (v0, v1,
+   * v2); tri_mat: material per triangle; mats[m] = (rho, ks, n) of the BSDF
+   * f = rho [(1 - ks) / pi + ks (n + 2) / (2 pi) max(0, wo . mirror(w))^n]. */
+  int32_t n_tris;
+  const double* tris;
+  const int32_t* tri_mat;
+  int32_t n_mats;
+  double mats[OR_MAX_MATERIALS][3];
 } or_scene;
 
 /* 16-bit quantised per-cell CDF of the EDA direction table (R8-R10):
@@ -110,6 +122,13 @@ double or_hg_sample_cos(double g, double u);
 void or_gauss_legendre(int n, double* x, double* w);
 int or_intersect(const or_scene* sc, const double o[3], const double d[3],
                  double* t_lo, double* t_hi, int* face);
+/* nearest triangle hit with 0 < t < t_max (brute force); returns the triangle or -1 */
+int or_mesh_hit(const or_scene* sc, const double o[3], const double d[3], double t_max, double* t);
+/* BSDF of R32 at triangle tri for incident direction w (propagation) and outgoing wo */
+double or_bsdf_eval(const or_scene* sc, int tri, const double w[3], const double wo[3]);
+/* R32 sampling with u4 (lobe), u5, u6: writes wo, returns f cos / p (0: below the surface) */
+double or_bsdf_sample(const or_scene* sc, int tri, const double w[3], double u4, double u5, double u6,
+                      double wo[3]);
 
 /* EDA table: the quadrature rule of R9, per-bin mass (double) and the
  * quantised CDF.  mass may be NULL.  Returns 0 on success. */

@@ -72,6 +72,8 @@ class OrScene(ctypes.Structure):
         ("table_smin", ctypes.c_double), ("table_smax", ctypes.c_double),
         ("conn_sampling", ctypes.c_int32),
         ("response", ctypes.c_void_p),
+        ("n_tris", ctypes.c_int32), ("tris", ctypes.c_void_p), ("tri_mat", ctypes.c_void_p),
+        ("n_mats", ctypes.c_int32), ("mats", D3 * 8),
     ]
 
 
@@ -156,6 +158,18 @@ def scene(c: dict) -> OrScene:
         assert w.shape == (c["n_bins"],)
         s._response_keepalive = w
         s.response = w.ctypes.data
+    m = c.get("mesh")
+    if m is not None and len(m["tris"]):
+        tris = np.ascontiguousarray(np.asarray(m["tris"], dtype=np.float64).reshape(-1, 9))
+        mat = np.ascontiguousarray(np.asarray(m["tri_mat"], dtype=np.int32))
+        assert mat.shape == (tris.shape[0],) and 1 <= len(m["mats"]) <= 8
+        s._mesh_keepalive = (tris, mat)
+        s.n_tris = tris.shape[0]
+        s.tris = tris.ctypes.data
+        s.tri_mat = mat.ctypes.data
+        s.n_mats = len(m["mats"])
+        for i, mm in enumerate(m["mats"]):
+            s.mats[i][:] = mm
     return s
 
 
@@ -209,6 +223,31 @@ def intersect(c: dict, o, d):
     face = ctypes.c_int()
     hit = lib().or_intersect(ctypes.byref(s), D3(*o), D3(*d), ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(face))
     return hit, lo.value, hi.value, face.value
+
+
+def mesh_hit(c: dict, o, d, t_max: float = float("inf")):
+    """(triangle, t) of the nearest triangle hit with 0 < t < t_max, or (-1, None)."""
+    sc = scene(c)
+    t = ctypes.c_double()
+    lib().or_mesh_hit.restype = ctypes.c_int
+    tri = lib().or_mesh_hit(ctypes.byref(sc), D3(*o), D3(*d), ctypes.c_double(t_max), ctypes.byref(t))
+    return (tri, t.value) if tri >= 0 else (-1, None)
+
+
+def bsdf_eval(c: dict, tri: int, w, wo) -> float:
+    sc = scene(c)
+    lib().or_bsdf_eval.restype = ctypes.c_double
+    return lib().or_bsdf_eval(ctypes.byref(sc), ctypes.c_int(tri), D3(*w), D3(*wo))
+
+
+def bsdf_sample(c: dict, tri: int, w, u4: float, u5: float, u6: float):
+    """(wo, f cos / p) of the R32 sampling."""
+    sc = scene(c)
+    wo = D3()
+    lib().or_bsdf_sample.restype = ctypes.c_double
+    wgt = lib().or_bsdf_sample(ctypes.byref(sc), ctypes.c_int(tri), D3(*w), ctypes.c_double(u4),
+                               ctypes.c_double(u5), ctypes.c_double(u6), wo)
+    return np.array(wo[:]), wgt
 
 
 def table_integrand(c: dict, C: float, S: float, mu: float) -> float:
