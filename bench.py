@@ -246,14 +246,17 @@ def run_gpu(args):
                 "paths_per_step": paths_per_step, "vertices_per_step": verts_per_step,
                 "parallelism": f"sample-range shards x{world}" + (
                     (" + fused peer-memory REDs" if args.reduce == "p2p" else " + NCCL reduce") if world > 1 else ""),
-                "l2": "histogram (%.2f GB) > L2 is re-zeroed every step" % (hist.numel() * 4 / 1e9),
+                "l2": ("histogram (%.2f GB) > L2 is re-zeroed every step" if hist.numel() * 4 > 126e6 else
+                       "histogram (%.4f GB) fits L2 (small config: a parity case, not the headline); re-zeroed every step")
+                      % (hist.numel() * 4 / 1e9),
             },
             "paths_per_s": paths_per_step / (ms / args.steps * 1e-3),
             "roofline": {
                 "bound": "alu", "achieved": achieved, "peak": peak_tips, "unit": "Tinst/s",
                 "frac": achieved / peak_tips, "traffic": traffic,
                 "basis": f"{alg} algorithmic thread-instructions per vertex (SURVEY 8d.2) x vertices / "
-                         f"render-kernel time; peak = 148 SM x 4 issue x 32 lanes x {sm_max:.0f} MHz",
+                         f"render-kernel time; peak = 148 SM x 4 issue x 32 lanes x {sm_max:.0f} MHz"
+                         + ("; BVH traversal of the mesh not counted" if c.get("mesh") else ""),
                 "kernel_ms": kern_avg,
             },
             "clocks": clocks,
@@ -412,7 +415,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5, 6])
     ap.add_argument("--direction-mode", choices=["reuse", "split"], default=None)
     ap.add_argument("--strategy", choices=["darts", "vanilla", "da_only", "eda_only"], default=None,
                     help="estimator (default: the config's, DARTS); other values are comparison runs, not bench lines")

@@ -88,7 +88,9 @@ _DEFAULTS = dict(
 
 
 def config(idx: int, **overrides) -> dict:
-    """Full scene dict for config ``idx`` (1..5) with defaults and overrides."""
+    """Full scene dict for config ``idx`` (1..5; 6 = mesh_config) with defaults and overrides."""
+    if idx == 6:
+        return mesh_config(**overrides)
     c = copy.deepcopy(_DEFAULTS)
     c.update(copy.deepcopy(CONFIGS[idx]))
     c.update(overrides)
@@ -199,6 +201,19 @@ def mesh_config(**overrides) -> dict:
     mat = np.concatenate([np.zeros(len(ico), np.int32), np.ones(len(st), np.int32)])
     c = config(4, t0=5.0, t1=5.2, n_bins=2, spp=64, width=256, height=256, name="cfg6_mesh_glossy_stairs", seed=6)
     c["mesh"] = dict(tris=tris.reshape(-1, 9), tri_mat=mat, mats=[(0.8, 0.9, 40.0), (0.6, 0.25, 15.0)])
+    c.update(overrides)
+    return c
+
+
+def plate_config(mats, **overrides) -> dict:
+    """A 4 x 4 square plate (two triangles) at z = 0 in an infinite, almost
+    non-scattering medium (sigma_s = 1e-4), a pulse emitter and a fluence
+    detector above it: the single-bounce surface case of the mesh pins."""
+    c = config(1, sigma_s=1e-4, sigma_a=0.05, emitters=[((0.5, 0.0, 1.0), 0.0, 1.0)], cam_pos=(-0.5, 0.0, 1.0),
+               det_radius=0.02, t0=2.0, t1=6.0, n_bins=40, name="plate_single_bounce")
+    q = [(-2.0, -2.0, 0.0), (2.0, -2.0, 0.0), (2.0, 2.0, 0.0), (-2.0, 2.0, 0.0)]
+    tris = np.array([q[0] + q[1] + q[2], q[0] + q[2] + q[3]], float)
+    c["mesh"] = dict(tris=tris, tri_mat=np.zeros(2, np.int32), mats=mats)
     c.update(overrides)
     return c
 

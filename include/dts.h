@@ -45,6 +45,7 @@ extern "C" {
 
 #define DTS_ABI_VERSION 1
 #define DTS_MAX_EMITTERS 8
+#define DTS_MAX_MATERIALS 8
 #define DTS_TABLE_COS_BINS 256 /* "[-1, 1] is uniformly subdivided into 256 bins" */
 
 typedef struct dts_scene* dts_scene_t; /* opaque, library-owned */
@@ -110,6 +111,27 @@ typedef struct {
   float parity_r_excl;               /* TEST ONLY: drop contributions whose last segment < r (0 = off) */
   float parity_s_excess;             /* TEST ONLY: require S - C >= eps for medium-last paths (0 = off) */
   int32_t conn_sampling;             /* DTS_CONN_* (0 = paper) */
+  /* Triangle meshes (the opaque surfaces of PAPER.md:105, 221,
+   * 301, Table 1; readings R32, R33 in DESIGN.md): thin, two-sided, opaque
+   * triangles strictly inside the medium (every vertex >= 1e-3 inside a BOX,
+   * inside a SPHERE's radius - 1e-3; SPHERE media take no mesh).  A ray's medium
+   * interval ends at the nearest triangle (case II of PAPER.md:301); a surface
+   * vertex sits 1e-4 off its triangle on the incident side (R33), does the
+   * time-checked NEE of R14 with the BSDF, samples the BSDF and connects like a
+   * wall vertex.  BSDF of material m (R32):
+   *   f = rho [(1 - ks) / pi + ks (n + 2) / (2 pi) max(0, wo . mirror(w))^n]
+   * (Lambertian for ks = 0, glossy Phong lobe for ks = 1, plastic between).
+   * n_tris = 0: no mesh (tris, tri_mat ignored).  tris / tri_mat are HOST
+   * arrays copied by dts_scene_create (a BVH is built over them); the caller
+   * keeps ownership.  Rejected (DTS_E_INVALID_ARG): n_tris < 0, null arrays,
+   * material index outside [0, n_mats), 1 > n_mats or n_mats > DTS_MAX_MATERIALS,
+   * rho or ks outside [0, 1], n < 0, a vertex outside the medium margin,
+   * degenerate (zero-area) triangles.  dts_sample_debug does not take mesh scenes. */
+  int32_t n_tris;
+  const float* tris;                 /* HOST, n_tris x 9 floats: v0, v1, v2 */
+  const int32_t* tri_mat;            /* HOST, n_tris material indices */
+  int32_t n_mats;
+  float mats[DTS_MAX_MATERIALS][3];  /* rho, ks, n */
 } dts_scene_desc;
 
 /* EDA table axes (R8): n_ratio uniform bins of C/S in [0,1), n_s log-spaced

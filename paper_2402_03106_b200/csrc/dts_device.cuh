@@ -31,10 +31,11 @@ constexpr float kInv4Pi = 0.0795774715459476679f;
 constexpr float kLog2e = 1.44269504088896341f;
 constexpr float kLn2 = 0.693147180559945309f;
 
-enum { HIT_NONE = 0, HIT_OPEN = 1, HIT_WALL = 2, HIT_MISS = 3 };
-enum { KIND_CAMERA = 0, KIND_MEDIUM = 1, KIND_WALL = 2 };
+enum { HIT_NONE = 0, HIT_OPEN = 1, HIT_WALL = 2, HIT_MISS = 3, HIT_SURF = 4 };
+enum { KIND_CAMERA = 0, KIND_MEDIUM = 1, KIND_WALL = 2, KIND_SURF = 3 };
 // compile-time scene variant flags of the render / debug kernels
-enum { FL_WALLS = 1, FL_SPLIT = 2, FL_MULTI_E = 4 };
+enum { FL_WALLS = 1, FL_SPLIT = 2, FL_MULTI_E = 4, FL_MESH = 8 };
+constexpr float kSurfEps = 1e-4f;  // R33: surface vertices sit this far off their triangle
 
 // Launch-uniform scene constants, passed by value as a kernel parameter (lives
 // in the constant bank: every lane reads the same address).
@@ -78,6 +79,17 @@ struct DevScene {
   float ln_smin, inv_dls;  // ns / (ln smax - ln smin)
   uint32_t seed_lo, seed_hi;
   uint32_t rk[20];  // Philox round keys (k0_r, k1_r), r = 0..9, of the launch's seed
+  // triangle meshes (R32, R33): BVH nodes in depth-first order, 2 float4 each:
+  // (lo.xyz, int a), (hi.xyz, int n): n > 0 leaf of triangles [a, a + n), n = 0
+  // inner node with children node + 1 and a; triangles in leaf order, 3 float4
+  // each: (v0.xyz, int material), (e1.xyz, -), (e2.xyz, -)
+  const float4* bvh;
+  const float4* tri4;
+  int32_t n_tris;
+  // R32 per material: select ks, f = kd + kl pow(ca, n), p = pd cos + pl pow(ca, n), 1 / (n + 1)
+  float mat_ks[DTS_MAX_MATERIALS], mat_kd[DTS_MAX_MATERIALS], mat_kl[DTS_MAX_MATERIALS];
+  float mat_pd[DTS_MAX_MATERIALS], mat_pl[DTS_MAX_MATERIALS], mat_n[DTS_MAX_MATERIALS];
+  float mat_inv_n1[DTS_MAX_MATERIALS];
 };
 
 // ----------------------------------------------------------------- vectors
@@ -291,9 +303,93 @@ __device__ __forceinline__ int intersect_inside(const DevScene& S, f3 o, f3 d, f
   return ((S.wall_mask >> ff) & 1u) ? HIT_WALL : HIT_OPEN;
 }
 
+// ----------------------------------------------------------------- triangle meshes (R32, R33)
+__device__ __forceinline__ f3 cross(f3 a, f3 b) {
+  return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+// Nearest triangle hit with 0 < t < t_max over the BVH (ANY: the first hit
+// found, for visibility); returns the triangle (leaf order) or -1.  Moller-
+// Trumbore with inclusive edges, the test of the oracle in fp32.
+// (Out of line, so each mesh kernel carries one copy; takes the two array
+// pointers rather than the scene, whose address would force a local copy.)
+template <bool ANY>
+__device__ __noinline__ int mesh_trace_impl(const float4* __restrict__ bvh, const float4* __restrict__ tri4, f3 o, f3 d,
+                                            float t_max, float& t_hit) {
+  const f3 inv = mk(__fdividef(1.0f, d.x), __fdividef(1.0f, d.y), __fdividef(1.0f, d.z));
+  int stack[40];
+  int sp = 0, node = 0, best = -1;
+  float tb = t_max;
+  while (true) {
+    const float4 a = __ldg(bvh + 2 * node), b = __ldg(bvh + 2 * node + 1);
+    const float ax = (a.x - o.x) * inv.x, bx = (b.x - o.x) * inv.x;
+    const float ay = (a.y - o.y) * inv.y, by = (b.y - o.y) * inv.y;
+    const float az = (a.z - o.z) * inv.z, bz = (b.z - o.z) * inv.z;
+    const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+    const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fmaxf(az, bz));
+    if (tn <= tf && tn < tb) {
+      const int first = __float_as_int(a.w), cnt = __float_as_int(b.w);
+      if (cnt == 0) {  // inner node: near side first is not needed for correctness
+        stack[sp++] = first;
+        ++node;
+        continue;
+      }
+      for (int i = first; i < first + cnt; ++i) {
+        const float4 t0 = __ldg(tri4 + 3 * i), t1 = __ldg(tri4 + 3 * i + 1), t2 = __ldg(tri4 + 3 * i + 2);
+        const f3 e1 = mk(t1.x, t1.y, t1.z), e2 = mk(t2.x, t2.y, t2.z);
+        const f3 pv = cross(d, e2);
+        const float det = dot(e1, pv);
+        const float idet = __fdividef(1.0f, det);
+        const f3 sv = o - mk(t0.x, t0.y, t0.z);
+        const float u = dot(sv, pv) * idet;
+        const f3 qv = cross(sv, e1);
+        const float v = dot(d, qv) * idet;
+        const float t = dot(e2, qv) * idet;
+        if (det != 0.0f && u >= 0.0f && v >= 0.0f && u + v <= 1.0f && t > 0.0f && t < tb) {
+          tb = t;
+          best = i;
+          if (ANY) {
+            t_hit = tb;
+            return best;
+          }
+        }
+      }
+    }
+    if (sp == 0) break;
+    node = stack[--sp];
+  }
+  t_hit = tb;
+  return best;
+}
+template <bool ANY>
+__device__ __forceinline__ int mesh_trace(const DevScene& S, f3 o, f3 d, float t_max, float& t_hit) {
+  return mesh_trace_impl<ANY>(S.bvh, S.tri4, o, d, t_max, t_hit);
+}
+// geometric normal of triangle tri turned to the side the direction w arrives from
+__device__ __forceinline__ f3 tri_side_normal(const DevScene& S, int tri, f3 w, int& mat) {
+  const float4 t0 = __ldg(S.tri4 + 3 * tri), t1 = __ldg(S.tri4 + 3 * tri + 1), t2 = __ldg(S.tri4 + 3 * tri + 2);
+  f3 n = cross(mk(t1.x, t1.y, t1.z), mk(t2.x, t2.y, t2.z));
+  n = n * rsqrtf(dot(n, n));
+  mat = __float_as_int(t0.w);
+  return dot(n, w) > 0.0f ? n * -1.0f : n;
+}
+// max(0, c)^n with 0^0 = 1 (pow of the oracle)
+__device__ __forceinline__ float lobe_pow(float c, float n) {
+  return c > 0.0f ? exp2f(n * __log2f(c)) : (n == 0.0f ? 1.0f : 0.0f);
+}
+// R32: f(w -> wo) = rho [(1 - ks) / pi + ks (n + 2) / (2 pi) max(0, wo . r)^n], r = mirror of w
+__device__ __forceinline__ float bsdf_eval(const DevScene& S, int mat, f3 n, f3 w, f3 wo) {
+  if (!(dot(wo, n) > 0.0f)) return 0.0f;
+  const f3 r = w - n * (2.0f * dot(w, n));
+  return fmaf(S.mat_kl[mat], lobe_pow(dot(wo, r), S.mat_n[mat]), S.mat_kd[mat]);
+}
+
 // medium length and visibility of the segment p -> xe (p inside the medium)
-template <int SH, bool WALLS>
+template <int SH, bool WALLS, bool MESH = false>
 __device__ __forceinline__ float segment_tr(const DevScene& S, f3 p, f3 xe, float r, f3 dir) {
+  if (MESH) {  // R32: a triangle on the segment occludes it
+    float tm;
+    if (mesh_trace<true>(S, p, dir, r, tm) >= 0) return 0.0f;
+  }
   if (SH == DTS_MEDIUM_INFINITE) return fexp(-S.sigma_t * r);
   float lo, hi;
   int face;
@@ -410,7 +506,7 @@ __device__ __forceinline__ SRange conn_range(const DevScene& S, f3 x, f3 wc, f3 
 // (E2 throughput: sigma_s, transmittance of both legs, HG at x_ell, inverse
 // square, pulse intensity), divided by p_t.  coef = beta (x the MIS/SPLIT
 // connection weight, x 1/n_cell for a deferred splat).  pSt > 0: r2 = S - t.
-template <int SH, bool WALLS>
+template <int SH, bool WALLS, bool MESH = false>
 __device__ __forceinline__ float conn_contrib(const DevScene& S, f3 x, f3 wc, f3 xe, float ek, float t, float pt,
                                               float pSt, float clo, float coef, f3* xell_out, float* r2_out) {
   const f3 xell = fma3(wc, t, x);
@@ -423,7 +519,7 @@ __device__ __forceinline__ float conn_contrib(const DevScene& S, f3 x, f3 wc, f3
     r2sq = pSt * pSt;
   }
   const float rho = hg_eval(S, dot(wc, we));
-  const float tr = fexp(-S.sigma_t * (t - clo)) * segment_tr<SH, WALLS>(S, xell, xe, r2, we);
+  const float tr = fexp(-S.sigma_t * (t - clo)) * segment_tr<SH, WALLS, MESH>(S, xell, xe, r2, we);
   float c = coef * S.sigma_s * tr * rho * ek * __fdividef(1.0f, r2sq * pt);
   if (S.r_excl > 0.0f && r2 < S.r_excl) c = 0.0f;
   if (xell_out) *xell_out = xell;
@@ -437,14 +533,14 @@ __device__ __forceinline__ float conn_contrib(const DevScene& S, f3 x, f3 wc, f3
 template <int SH, int FL>
 __device__ __forceinline__ float conn_job_run(const DevScene& S, f3 x, f3 wc, float dlo, float width, float coef,
                                               uint32_t m7e) {
-  constexpr bool WALLS = (FL & FL_WALLS) != 0;
+  constexpr bool WALLS = (FL & FL_WALLS) != 0, MESH = (FL & FL_MESH) != 0;
   const int e = (FL & FL_MULTI_E) ? (int)(m7e >> 23) : 0;
   const f3 xe = ld3(S.em_pos[e]);
   const f3 cv = xe - x;
   const float C = sqrtf(dot(cv, cv));
   const float q = dot(wc, cv);
   const EllSample es = ell_sample(S, cv, C, q, wc, dlo, width, mant01(m7e & 0x7FFFFFu));
-  return conn_contrib<SH, WALLS>(S, x, wc, xe, S.em_k[e], es.t, es.pt, es.pSt, 0.0f, coef, nullptr, nullptr);
+  return conn_contrib<SH, WALLS, MESH>(S, x, wc, xe, S.em_k[e], es.t, es.pt, es.pSt, 0.0f, coef, nullptr, nullptr);
 }
 
 // Deferred connections (render kernel only): a medium or wall vertex whose
@@ -643,7 +739,8 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   conn_nonempty = false;
   wall_nee = false;
   end_reason = 0;
-  constexpr bool WALLS = (FL & FL_WALLS) != 0, SPLIT = (FL & FL_SPLIT) != 0;
+  constexpr bool WALLS = (FL & FL_WALLS) != 0, SPLIT = (FL & FL_SPLIT) != 0, MESH = (FL & FL_MESH) != 0;
+  static_assert(!(MESH && (DEFER || DBG)), "mesh scenes run the immediate render kernels only");
   const int e = (FL & FL_MULTI_E) ? ps.e : 0;  // one emitter: constant-bank operands
   const f3 xe = ld3(S.em_pos[e]);
   const float ek = S.em_k[e];
@@ -698,7 +795,8 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     float nee = 0.0f;
     if (cw > 0.0f && resm - C <= 0.0f && resM - C > 0.0f) {  // E + C in [Rm, RM)
       // R14: time-checked direct NEE at a wall vertex
-      nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr<SH, WALLS>(S, ps.x, xe, C, we) * __fdividef(1.0f, C * C);
+      nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr<SH, WALLS, MESH>(S, ps.x, xe, C, we) *
+            __fdividef(1.0f, C * C);
       if (S.r_excl > 0.0f && C < S.r_excl) nee = 0.0f;
       contrib += nee;
       wall_nee = nee > 0.0f;
@@ -714,6 +812,46 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       dbg->tech = 3;
       dbg->beta_dir = alb;
     }
+  } else if (MESH && ps.kind == KIND_SURF) {
+    // R32: surface vertex on triangle ps.face: time-checked NEE as at walls
+    // (R14) with the BSDF, then a BSDF-sampled direction for the connection and the walk
+    int mat;
+    const f3 n = tri_side_normal(S, ps.face, ps.w, mat);
+    const f3 cv = xe - ps.x;
+    const float C = sqrtf(dot(cv, cv));
+    const f3 we = cv * __fdividef(1.0f, C);
+    const float cw = dot(n, we);
+    const float resm = d2f(ps.resM - S.dt);
+    if (cw > 0.0f && resm - C <= 0.0f && resM - C > 0.0f) {  // E + C in [Rm, RM)
+      float nee = ps.beta * bsdf_eval(S, mat, n, ps.w, we) * cw * ek *
+                  segment_tr<SH, WALLS, MESH>(S, ps.x, xe, C, we) * __fdividef(1.0f, C * C);
+      if (S.r_excl > 0.0f && C < S.r_excl) nee = 0.0f;
+      contrib += nee;
+      wall_nee = nee > 0.0f;
+      if (nsamp && nee != 0.0f) ++*nsamp;
+    }
+    // lobe (u4 < ks: cos alpha = u5^{1/(n+1)} about the mirror direction r) or
+    // cosine hemisphere (cos theta = sqrt(1 - u5) about n); phi = 2 pi u6;
+    // weight f cos / ((1 - ks) cos / pi + ks p_lobe)
+    const float u4 = unif(r[4]), u5 = unif(r[5]);
+    const float phi = 2.0f * kPi * unif(r[6]);
+    const f3 rm = ps.w - n * (2.0f * dot(ps.w, n));
+    f3 wo;
+    if (u4 < S.mat_ks[mat]) {
+      const float ca = lobe_pow(u5, S.mat_inv_n1[mat]);
+      wo = from_frame(rm, 1.0f + ca, 1.0f - ca, phi);
+    } else {
+      const float lz = sqrtf(1.0f - u5);
+      wo = from_frame(n, 1.0f + lz, __fdividef(u5, 1.0f + lz), phi);
+    }
+    const float co = dot(wo, n);
+    if (!(co > 0.0f)) {  // below the surface: the path ends
+      end_reason = DTS_CTR_ESCAPES;
+      return false;
+    }
+    const float pw = lobe_pow(dot(wo, rm), S.mat_n[mat]);
+    ps.beta *= fmaf(S.mat_kl[mat], pw, S.mat_kd[mat]) * co * __fdividef(1.0f, fmaf(S.mat_pd[mat], co, S.mat_pl[mat] * pw));
+    wc = ww = wo;
   } else {
     // medium vertex: one-sample MIS of EDA and HG
     if (SPLIT && skip_conn) {
@@ -759,8 +897,13 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   // ---- intersection, reused by the connection and the walk ----
   float lo = 0.0f, hi = 0.0f;
   int face = -1;
-  const int hit = ps.kind == KIND_CAMERA ? intersect<SH, WALLS>(S, ps.x, ww, lo, hi, face)
-                                         : intersect_inside<SH, WALLS>(S, ps.x, ww, lo, hi, face);
+  int hit = ps.kind == KIND_CAMERA ? intersect<SH, WALLS>(S, ps.x, ww, lo, hi, face)
+                                   : intersect_inside<SH, WALLS>(S, ps.x, ww, lo, hi, face);
+  if (MESH && hit != HIT_MISS) {  // the interval ends at the nearest triangle (PAPER.md:301 case II)
+    float tm;
+    const int tri = mesh_trace<false>(S, ps.x, ww, hi, tm);
+    if (tri >= 0) { hi = tm; hit = HIT_SURF; face = tri; }
+  }
   // render kernel: non-empty connections of medium/wall vertices are queued (df)
   const bool defer = DEFER && !DBG && ps.kind != KIND_CAMERA;
 
@@ -774,6 +917,10 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     } else {
       int fc;
       hitc = intersect_inside<SH, WALLS>(S, ps.x, wc, clo, chi, fc);
+      if (MESH && hitc != HIT_MISS) {
+        float tm;
+        if (mesh_trace<false>(S, ps.x, wc, chi, tm) >= 0) { chi = tm; hitc = HIT_SURF; }
+      }
     }
   }
   if (DBG) {
@@ -858,7 +1005,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       conn_nonempty = true;
       f3 xell;
       float r2;
-      const float c = conn_contrib<SH, WALLS>(S, ps.x, wc, xe, ek, t, pt, pSt, clo, ps.beta * wconn, &xell, &r2);
+      const float c = conn_contrib<SH, WALLS, MESH>(S, ps.x, wc, xe, ek, t, pt, pSt, clo, ps.beta * wconn, &xell, &r2);
       contrib += c;
       if (nsamp && c != 0.0f) ++*nsamp;
       if (DBG) {
@@ -1019,6 +1166,15 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       ps.face = face;
       ps.w = ww;
       if (DBG) { dbg->event = 2; dbg->d = hi; dbg->beta_ris = 1.0f; }
+    } else if (MESH && hit == HIT_SURF) {
+      // R32/R33: the walk reaches the triangle; the vertex sits kSurfEps off it on the incident side
+      int mat;
+      const f3 n = tri_side_normal(S, face, ww, mat);
+      ps.x = fma3(n, kSurfEps, fma3(ww, hi, ps.x));
+      ps.resM -= f2d(counts * hi);
+      ps.kind = KIND_SURF;
+      ps.face = face;
+      ps.w = ww;
     } else {
       if (DBG) { dbg->event = 3; dbg->terminate = 1; dbg->beta_out = ps.beta; }
       end_reason = DTS_CTR_ESCAPES;

@@ -52,6 +52,8 @@ struct dts_scene {
   uint16_t* d_zero_cell = nullptr; // debug kernel table for vanilla scenes
   float* d_qover = nullptr;        // deferred-connection queue overflow slots
   size_t qover_n = 0;
+  float4* d_bvh = nullptr;         // mesh BVH nodes (R32)
+  float4* d_tri4 = nullptr;        // mesh triangles in leaf order
   int num_sms = 0;
   int device = 0;
 };
@@ -207,7 +209,11 @@ constexpr int kBlock = DTS_BLOCK;  // deferred-connection kernels: the queues ta
 #endif
 // immediate-connection kernels: 28 warps at <= 72 registers (A/B in profiles/README.md)
 constexpr int kBlockImm = DTS_BLOCK_IMM;
-__host__ __device__ constexpr int render_block(bool defer) { return defer ? kBlock : kBlockImm; }
+// mesh kernels (BVH traversal: a call, its stack and more live values) run 640 threads at <= 96 registers
+constexpr int kBlockMesh = 640;
+__host__ __device__ constexpr int render_block(bool defer, bool mesh = false) {
+  return mesh ? kBlockMesh : (defer ? kBlock : kBlockImm);
+}
 constexpr uint32_t kChunk = 128;
 #ifndef DTS_RIS_WARP
 #define DTS_RIS_WARP 0
@@ -428,7 +434,7 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
 #define DTS_TABLE_SMEM 1
 #endif
 template <bool SMEM, int SH, int FL, bool DEFER>
-__global__ void __launch_bounds__(render_block(DEFER), DTS_MINB) render_darts_kernel(const RenderParams P) {
+__global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_MINB) render_darts_kernel(const RenderParams P) {
   constexpr bool WALLS = (FL & FL_WALLS) != 0;
   extern __shared__ __align__(16) uint16_t s_dyn[];
   __shared__ uint64_t s_bar;
@@ -730,7 +736,7 @@ __device__ __forceinline__ int vanilla_splat(const RenderParams& P, uint32_t pl,
   return 0;
 }
 
-template <int SH, bool WALLS>
+template <int SH, bool WALLS, bool MESH = false>
 __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderParams P) {
   const DevScene& S = P.S;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -813,10 +819,35 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
         const float lx = rr * cp, ly = rr * sp, lz = sqrtf(fmaxf(0.0f, 1.0f - u5));
         w = mk(b1.x * lx + b2.x * ly + n.x * lz, b1.y * lx + b2.y * ly + n.y * lz, b1.z * lx + b2.z * ly + n.z * lz);
         beta *= S.wall_albedo[face];
+      } else if (MESH && kind == KIND_SURF) {
+        // R32 sampling (lobe u3, direction u1 u2; the oracle's vanilla order)
+        int mat;
+        const f3 n = tri_side_normal(S, face, w, mat);
+        const float u5 = unif(r.b);
+        const float phi = 2.0f * kPi * unif(r.c);
+        const f3 rm = w - n * (2.0f * dot(w, n));
+        f3 wo;
+        if (unif(r.d) < S.mat_ks[mat]) {
+          const float ca = lobe_pow(u5, S.mat_inv_n1[mat]);
+          wo = from_frame(rm, 1.0f + ca, 1.0f - ca, phi);
+        } else {
+          const float lz = sqrtf(1.0f - u5);
+          wo = from_frame(n, 1.0f + lz, __fdividef(u5, 1.0f + lz), phi);
+        }
+        const float co = dot(wo, n);
+        if (!(co > 0.0f)) { ++c_esc; alive = false; break; }
+        const float pw = lobe_pow(dot(wo, rm), S.mat_n[mat]);
+        beta *= fmaf(S.mat_kl[mat], pw, S.mat_kd[mat]) * co * __fdividef(1.0f, fmaf(S.mat_pd[mat], co, S.mat_pl[mat] * pw));
+        w = wo;
       }
       float lo, hi;
       int hf;
-      const int hit = intersect<SH, WALLS>(S, x, w, lo, hi, hf);
+      int hit = intersect<SH, WALLS>(S, x, w, lo, hi, hf);
+      if (MESH && hit != HIT_MISS) {
+        float tm;
+        const int tri = mesh_trace<false>(S, x, w, hi, tm);
+        if (tri >= 0) { hi = tm; hit = HIT_SURF; hf = tri; }
+      }
       if (hit == HIT_MISS) { ++c_esc; alive = false; break; }
       const float counts = (S.warped || kind != KIND_CAMERA) ? 1.0f : 0.0f;
       const f3 d0 = x - xe;
@@ -837,6 +868,14 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
         E += (double)(counts * hi);
         kind = KIND_WALL;
         face = hf;
+      } else if (MESH && hit == HIT_SURF) {
+        d = hi;
+        int mat;
+        const f3 n = tri_side_normal(S, hf, w, mat);
+        x = fma3(n, kSurfEps, fma3(w, hi, x));
+        E += (double)(counts * hi);
+        kind = KIND_SURF;
+        face = hf;
       } else { ++c_esc; alive = false; break; }
       const f3 cv = xe - x;
       const float C = sqrtf(dot(cv, cv));
@@ -847,10 +886,14 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
       if (kind == KIND_MEDIUM) {
         c = beta * hg_eval(S, dot(w, we));
         if (S.s_excess > 0.0f && d + C - Cprev < S.s_excess) c = 0.0f;
+      } else if (MESH && kind == KIND_SURF) {
+        int mat;
+        const f3 n = tri_side_normal(S, face, w, mat);
+        c = beta * bsdf_eval(S, mat, n, w, we) * fmaxf(0.0f, dot(n, we));
       } else {
         c = beta * (S.wall_albedo[face] * (1.0f / kPi)) * fmaxf(0.0f, dot(inward_normal(face), we));
       }
-      c *= segment_tr<SH, WALLS>(S, x, xe, C, we) * __fdividef(ek, C * C);
+      c *= segment_tr<SH, WALLS, MESH>(S, x, xe, C, we) * __fdividef(ek, C * C);
       if (S.r_excl > 0.0f && C < S.r_excl) c = 0.0f;
       if (c != 0.0f && isfinite(c)) {
         ++c_samp;
@@ -931,13 +974,28 @@ static int scene_flags(const dts_scene_desc& d) {
   return (d.wall_mask ? FL_WALLS : 0) | (d.direction_mode == DTS_DIR_SPLIT ? FL_SPLIT : 0) |
          (d.n_emitters > 1 ? FL_MULTI_E : 0);
 }
+// mesh scenes (FL_MESH): immediate kernels with the table in shared memory, BOX or INFINITE media
+template <int FL>
+struct PickMesh {
+  static const void* box() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_BOX, FL | FL_MESH, false>; }
+  static const void* inf() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_INFINITE, FL | FL_MESH, false>; }
+  static const void* sph() { return nullptr; }
+};
 static const void* darts_kernel_ptr(bool smem, bool defer, const dts_scene_desc& d) {
   const int sh = d.medium_shape, fl = scene_flags(d);
+  if (d.n_tris > 0) return (smem && !defer) ? pick_fl<PickMesh>(sh, fl) : nullptr;
   if (smem) return defer ? pick_fl<PickRender<true, true>::F>(sh, fl) : pick_fl<PickRender<true, false>::F>(sh, fl);
   return defer ? pick_fl<PickRender<false, true>::F>(sh, fl) : pick_fl<PickRender<false, false>::F>(sh, fl);
 }
 static const void* debug_kernel_ptr(const dts_scene_desc& d) { return pick_fl<PickDebug>(d.medium_shape, scene_flags(d)); }
-static const void* vanilla_kernel_ptr(int shape, bool walls) {
+static const void* vanilla_kernel_ptr(int shape, bool walls, bool mesh) {
+  if (mesh) {
+    if (shape == DTS_MEDIUM_INFINITE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_INFINITE, false, true>;
+    if (shape == DTS_MEDIUM_BOX)
+      return walls ? (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, true, true>
+                   : (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, false, true>;
+    return nullptr;
+  }
   if (shape == DTS_MEDIUM_INFINITE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_INFINITE, false>;
   if (shape == DTS_MEDIUM_SPHERE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_SPHERE, false>;
   if (shape == DTS_MEDIUM_BOX)
@@ -1000,6 +1058,117 @@ static dts_status validate(const dts_scene_desc& d) {
   if (d.direction_mode != DTS_DIR_REUSE && d.direction_mode != DTS_DIR_SPLIT) return bad("unknown direction_mode");
   if (d.spp_mode < DTS_SPP_PER_CELL || d.spp_mode > DTS_SPP_RESPONSE) return bad("unknown spp_mode");
   if (!(d.parity_r_excl >= 0.0f) || !(d.parity_s_excess >= 0.0f)) return bad("parity restrictions must be >= 0");
+  if (d.n_tris < 0) return bad("n_tris must be >= 0");
+  if (d.n_tris > 0) {  // R32, R33
+    if (!d.tris || !d.tri_mat) return bad("mesh arrays are NULL");
+    if (d.medium_shape == DTS_MEDIUM_SPHERE) return bad("mesh scenes need a BOX or INFINITE medium");
+    if (d.n_mats < 1 || d.n_mats > DTS_MAX_MATERIALS) return bad("n_mats must be 1..8");
+    for (int m = 0; m < d.n_mats; ++m)
+      if (!(d.mats[m][0] >= 0.0f && d.mats[m][0] <= 1.0f) || !(d.mats[m][1] >= 0.0f && d.mats[m][1] <= 1.0f) ||
+          !(d.mats[m][2] >= 0.0f && d.mats[m][2] <= 1e4f))
+        return bad("material needs rho, ks in [0, 1] and 0 <= n <= 1e4");
+    for (int i = 0; i < d.n_tris; ++i) {
+      if (d.tri_mat[i] < 0 || d.tri_mat[i] >= d.n_mats) return bad("triangle material index out of range");
+      const float* v = d.tris + 9 * (size_t)i;
+      for (int k = 0; k < 9; ++k)
+        if (!std::isfinite(v[k])) return bad("non-finite triangle vertex");
+      if (d.medium_shape == DTS_MEDIUM_BOX)
+        for (int k = 0; k < 3; ++k)
+          for (int a = 0; a < 3; ++a)
+            if (!(v[3 * k + a] >= d.bmin[a] + 1e-3f && v[3 * k + a] <= d.bmax[a] - 1e-3f))
+              return bad("mesh vertices must lie >= 1e-3 inside the box");
+      double e1[3], e2[3], n[3];
+      for (int a = 0; a < 3; ++a) { e1[a] = (double)v[3 + a] - v[a]; e2[a] = (double)v[6 + a] - v[a]; }
+      vcross(e1, e2, n);
+      if (!(n[0] * n[0] + n[1] * n[1] + n[2] * n[2] > 0.0)) return bad("degenerate (zero-area) triangle");
+    }
+  }
+  return DTS_OK;
+}
+
+// Median-split BVH over the triangles' centroids (leaves of <= 4 triangles,
+// nodes in depth-first order: an inner node's first child follows it).
+static int bvh_node(const float* tris, std::vector<int>& ord, int b, int e, std::vector<float4>& nodes) {
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  float clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int i = b; i < e; ++i) {
+    const float* v = tris + 9 * (size_t)ord[i];
+    for (int a = 0; a < 3; ++a) {
+      const float c = (v[a] + v[3 + a] + v[6 + a]) / 3.0f;
+      clo[a] = std::fmin(clo[a], c);
+      chi[a] = std::fmax(chi[a], c);
+      for (int k = 0; k < 3; ++k) {
+        lo[a] = std::fmin(lo[a], v[3 * k + a]);
+        hi[a] = std::fmax(hi[a], v[3 * k + a]);
+      }
+    }
+  }
+  const int id = (int)nodes.size() / 2;
+  nodes.push_back(make_float4(lo[0], lo[1], lo[2], 0.0f));
+  nodes.push_back(make_float4(hi[0], hi[1], hi[2], 0.0f));
+  int a_field, n_field;
+  if (e - b <= 4) {
+    a_field = b;
+    n_field = e - b;
+  } else {
+    int ax = 0;
+    for (int a = 1; a < 3; ++a)
+      if (chi[a] - clo[a] > chi[ax] - clo[ax]) ax = a;
+    const int mid = (b + e) / 2;
+    auto cen = [&](int t) { const float* v = tris + 9 * (size_t)t; return v[ax] + v[3 + ax] + v[6 + ax]; };
+    std::nth_element(ord.begin() + b, ord.begin() + mid, ord.begin() + e, [&](int x, int y) { return cen(x) < cen(y); });
+    bvh_node(tris, ord, b, mid, nodes);  // = id + 1
+    a_field = bvh_node(tris, ord, mid, e, nodes);
+    n_field = 0;
+  }
+  int ai = a_field, ni = n_field;
+  float af, nf;
+  memcpy(&af, &ai, 4);
+  memcpy(&nf, &ni, 4);
+  nodes[2 * id].w = af;
+  nodes[2 * id + 1].w = nf;
+  return id;
+}
+
+static dts_status upload_mesh(dts_scene* s) {
+  const dts_scene_desc& d = s->desc;
+  std::vector<int> ord(d.n_tris);
+  for (int i = 0; i < d.n_tris; ++i) ord[i] = i;
+  std::vector<float4> nodes;
+  nodes.reserve(4 * (size_t)d.n_tris / 2 + 2);
+  bvh_node(d.tris, ord, 0, d.n_tris, nodes);
+  std::vector<float4> tri4(3 * (size_t)d.n_tris);
+  for (int i = 0; i < d.n_tris; ++i) {
+    const float* v = d.tris + 9 * (size_t)ord[i];
+    int m = d.tri_mat[ord[i]];
+    float mf;
+    memcpy(&mf, &m, 4);
+    tri4[3 * (size_t)i] = make_float4(v[0], v[1], v[2], mf);
+    tri4[3 * (size_t)i + 1] = make_float4(v[3] - v[0], v[4] - v[1], v[5] - v[2], 0.0f);
+    tri4[3 * (size_t)i + 2] = make_float4(v[6] - v[0], v[7] - v[1], v[8] - v[2], 0.0f);
+  }
+  if (cudaMalloc(&s->d_bvh, nodes.size() * sizeof(float4)) != cudaSuccess ||
+      cudaMalloc(&s->d_tri4, tri4.size() * sizeof(float4)) != cudaSuccess)
+    return fail(DTS_E_OOM, "cudaMalloc(mesh) failed");
+  CUDA_TRY(cudaMemcpy(s->d_bvh, nodes.data(), nodes.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(s->d_tri4, tri4.data(), tri4.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  DevScene& S = s->S;
+  S.bvh = s->d_bvh;
+  S.tri4 = s->d_tri4;
+  S.n_tris = d.n_tris;
+  for (int m = 0; m < d.n_mats; ++m) {  // R32 constants
+    const double rho = d.mats[m][0], ks = d.mats[m][1], n = d.mats[m][2];
+    S.mat_ks[m] = (float)ks;
+    S.mat_kd[m] = (float)(rho * (1.0 - ks) / M_PI);
+    S.mat_kl[m] = (float)(rho * ks * (n + 2.0) / (2.0 * M_PI));
+    S.mat_pd[m] = (float)((1.0 - ks) / M_PI);
+    S.mat_pl[m] = (float)(ks * (n + 1.0) / (2.0 * M_PI));
+    S.mat_n[m] = (float)n;
+    S.mat_inv_n1[m] = (float)(1.0 / (n + 1.0));
+  }
+  // the caller keeps its arrays: forget their addresses
+  s->desc.tris = nullptr;
+  s->desc.tri_mat = nullptr;
   return DTS_OK;
 }
 
@@ -1128,6 +1297,13 @@ dts_status dts_scene_create(const dts_scene_desc* desc, dts_scene_t* out) {
     delete s;
     return fail(DTS_E_OOM, "cudaMalloc(work counter) failed");
   }
+  if (desc->n_tris > 0) {
+    st = upload_mesh(s);
+    if (st != DTS_OK) {
+      dts_scene_destroy(s);
+      return st;
+    }
+  }
   *out = s;
   return DTS_OK;
 }
@@ -1144,6 +1320,8 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaFree(s->d_resp_w);
   cudaFree(s->d_zero_cell);
   cudaFree(s->d_qover);
+  cudaFree(s->d_bvh);
+  cudaFree(s->d_tri4);
   delete s;
   return DTS_OK;
 }
@@ -1318,7 +1496,8 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     bool want_defer = false;
     const char* dv = getenv("DTS_DEFER");
     if (dv && (dv[0] == '0' || dv[0] == '1')) want_defer = dv[0] == '1';
-    const bool defer = want_defer && !d_hist_sq &&
+    if (d.n_tris > 0 && !smem) return fail(DTS_E_INVALID_ARG, "mesh scenes need the EDA table in shared memory");
+    const bool defer = want_defer && !d_hist_sq && d.n_tris == 0 &&
                        (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + qbytes <= kSmemCap;
     P.defer = defer ? 1u : 0u;
     const char* rk = getenv("DTS_REFILL_K");
@@ -1335,7 +1514,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
     int blocks_per_sm = 1;
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    const int blk = render_block(defer);
+    const int blk = render_block(defer, d.n_tris > 0);
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, blk, dyn));
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     uint64_t grid = (uint64_t)s->num_sms * blocks_per_sm;
@@ -1363,7 +1542,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   } else {
     P.total = npix * ns;
     int bps = 1;
-    const void* kfn = vanilla_kernel_ptr(d.medium_shape, d.wall_mask != 0u);
+    const void* kfn = vanilla_kernel_ptr(d.medium_shape, d.wall_mask != 0u, d.n_tris > 0);
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, kBlock, 0));
     uint64_t grid = (uint64_t)s->num_sms * (bps < 1 ? 1 : bps) * 4;
@@ -1407,6 +1586,7 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
 
 dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, dts_debug_out* d_out, void* stream) {
   if (!s || (n > 0 && (!d_in || !d_out)) || n < 0) return fail(DTS_E_INVALID_ARG, "bad arguments");
+  if (s->desc.n_tris > 0) return fail(DTS_E_INVALID_ARG, "dts_sample_debug does not take mesh scenes");
   if (n == 0) return DTS_OK;
   if (s->desc.strategy != DTS_STRATEGY_VANILLA && !s->d_table) return fail(DTS_E_STATE, "table not built");
   const uint16_t* tab = s->d_table;

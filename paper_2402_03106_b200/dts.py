@@ -48,6 +48,8 @@ class SceneDesc(ctypes.Structure):
         ("max_bounces", ctypes.c_int32), ("direction_mode", ctypes.c_int32), ("spp_mode", ctypes.c_int32),
         ("parity_r_excl", ctypes.c_float), ("parity_s_excess", ctypes.c_float),
         ("conn_sampling", ctypes.c_int32),
+        ("n_tris", ctypes.c_int32), ("tris", ctypes.c_void_p), ("tri_mat", ctypes.c_void_p),
+        ("n_mats", ctypes.c_int32), ("mats", (ctypes.c_float * 3) * 8),
     ]
 
 
@@ -178,6 +180,17 @@ def scene_desc(c: dict) -> SceneDesc:
     d.spp_mode = _SPP[c["spp_mode"]]
     d.parity_r_excl, d.parity_s_excess = c["parity_r_excl"], c["parity_s_excess"]
     d.conn_sampling = _CONN[c.get("conn_sampling", "exp")]
+    m = c.get("mesh")
+    if m is not None and len(m["tris"]):
+        tris = np.ascontiguousarray(np.asarray(m["tris"], dtype=np.float32).reshape(-1, 9))
+        mat = np.ascontiguousarray(np.asarray(m["tri_mat"], dtype=np.int32))
+        d._mesh_keepalive = (tris, mat)   # read by dts_scene_create (copied there)
+        d.n_tris = tris.shape[0]
+        d.tris = tris.ctypes.data
+        d.tri_mat = mat.ctypes.data
+        d.n_mats = len(m["mats"])
+        for i, mm in enumerate(m["mats"]):
+            d.mats[i][:] = mm
     return d
 
 

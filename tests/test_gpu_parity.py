@@ -163,6 +163,12 @@ SAME_KEY = [
     ("cfg5_small_da_only", lambda: I.small(I.config(5, strategy="da_only"), 7, 9, n_bins=120, t1=12.0), 150),
     ("cfg1_vanilla", lambda: I.config(1, strategy="vanilla"), 4096),
     ("cfg4_vanilla", lambda: I.small(I.config(4, strategy="vanilla"), 16, 16), 256),
+    # triangle meshes (R32, R33): BVH traversal on the GPU, brute force in the oracle
+    ("cfg6_mesh", lambda: I.small(I.mesh_config(), 24, 24), 32),
+    ("cfg6_mesh_split", lambda: I.small(I.mesh_config(direction_mode="split"), 16, 16), 16),
+    ("cfg6_mesh_vanilla", lambda: I.small(I.mesh_config(strategy="vanilla"), 16, 16), 256),
+    ("plate_lambert", lambda: I.plate_config([(0.8, 0.0, 1.0)]), 2000),
+    ("plate_plastic_vanilla", lambda: I.plate_config([(0.7, 0.5, 10.0)], strategy="vanilla"), 100000),
 ]
 
 
@@ -198,6 +204,7 @@ FULL = [
     ("cfg3_full_crop", 3, (126, 126, 130, 130)),
     ("cfg5_full_crop", 5, (510, 510, 514, 514)),
     ("cfg4_full_crop", 4, (250, 250, 262, 262)),
+    ("cfg6_full_crop", 6, (120, 100, 136, 116)),
 ]
 
 
@@ -394,3 +401,13 @@ def test_render_same_key_both_variants(dts, oracle, monkeypatch, name, mk, spp, 
     assert abs(ctr["conn_nonempty"] - o["stats"]["conn_nonempty"]) <= 0.01 * o["stats"]["conn_nonempty"] + 2
     print(f"{name}/DTS_DEFER={defer}: same-key relative L2 {rel:.3e}")
     assert rel <= 0.01
+
+
+def test_mesh_scene_debug_is_rejected(dts):
+    """dts_sample_debug does not take mesh scenes (include/dts.h)."""
+    c = I.as_f32(I.small(I.mesh_config(), 4, 4))
+    sc = _scene(dts, c)
+    recs = I.debug_records(I.as_f32(I.small(I.config(4), 4, 4)), 8, seed=1)
+    with pytest.raises(dts.DtsError, match="mesh"):
+        dts.debug(sc, recs)
+    sc.close()

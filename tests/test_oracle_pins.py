@@ -835,14 +835,7 @@ def test_sharding_and_determinism(oracle):
 
 # ---------------------------------------------------------------- triangle meshes (R32, R33)
 def _plate_scene(mats, **kw):
-    """Infinite, almost non-scattering medium; a 4 x 4 square plate (two
-    triangles) at z = 0; pulse emitter and fluence detector above it."""
-    c = I.config(1, sigma_s=1e-4, sigma_a=0.05, emitters=[((0.5, 0.0, 1.0), 0.0, 1.0)], cam_pos=(-0.5, 0.0, 1.0),
-                 det_radius=0.02, t0=2.0, t1=6.0, n_bins=40, **kw)
-    q = [(-2.0, -2.0, 0.0), (2.0, -2.0, 0.0), (2.0, 2.0, 0.0), (-2.0, 2.0, 0.0)]
-    tris = np.array([q[0] + q[1] + q[2], q[0] + q[2] + q[3]], float)
-    c["mesh"] = dict(tris=tris, tri_mat=np.zeros(2, np.int32), mats=mats)
-    return I.as_f32(c)
+    return I.as_f32(I.plate_config(mats, **kw))
 
 
 def test_mesh_ray_triangle_hits(oracle):
