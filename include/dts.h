@@ -235,7 +235,7 @@ size_t dts_hist_cells(dts_scene_t scene);
  * measured optima of profiles/README.md): DTS_DEFER=1 selects the kernels
  * with per-warp connection queues (default off: the immediate kernels are as
  * fast or faster on every config); DTS_FLUSH_AT (1..32, default 28) is the queue length
- * that triggers a batch; DTS_REFILL_K (default 16) is the idle
+ * that triggers a batch; DTS_REFILL_K (default 8) is the idle
  * lane-iterations that trigger a lane refill.  None changes any result
  * beyond fp32 summation order. */
 dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,

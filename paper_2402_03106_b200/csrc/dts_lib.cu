@@ -1501,8 +1501,9 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
                        (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + qbytes <= kSmemCap;
     P.defer = defer ? 1u : 0u;
     const char* rk = getenv("DTS_REFILL_K");
-    P.refill_k = rk ? (uint32_t)atoi(rk) : 16u;
-    if (P.refill_k < 1 || P.refill_k > 4096) P.refill_k = 16u;
+    // 8: A/B in profiles/ab_r01_refill*.log (configs 6 / 4 +4 % / +2 %, 5 and 3 +0.2 % / +0.4 % vs 16)
+    P.refill_k = rk ? (uint32_t)atoi(rk) : 8u;
+    if (P.refill_k < 1 || P.refill_k > 4096) P.refill_k = 8u;
     const char* f1 = getenv("DTS_FLUSH1_AT");
     P.flush1_at = f1 ? (uint32_t)atoi(f1) : 16u;
     if (P.flush1_at < 1 || P.flush1_at > (uint32_t)kQueue) P.flush1_at = 16u;
