@@ -310,10 +310,18 @@ __device__ __forceinline__ f3 cross(f3 a, f3 b) {
 // Nearest triangle hit with 0 < t < t_max over the BVH (ANY: the first hit
 // found, for visibility); returns the triangle (leaf order) or -1.  Moller-
 // Trumbore with inclusive edges, the test of the oracle in fp32.
-// (Out of line, so each mesh kernel carries one copy; takes the two array
-// pointers rather than the scene, whose address would force a local copy.)
+// (Inlined by default, DTS_MESH_INLINE=0 builds it out of line; takes the two
+// array pointers rather than the scene, whose address would force a local copy.)
+#ifndef DTS_MESH_INLINE
+#define DTS_MESH_INLINE 1
+#endif
+#if DTS_MESH_INLINE
+#define DTS_MESH_FN __forceinline__
+#else
+#define DTS_MESH_FN __noinline__
+#endif
 template <bool ANY>
-__device__ __noinline__ int mesh_trace_impl(const float4* __restrict__ bvh, const float4* __restrict__ tri4, f3 o, f3 d,
+__device__ DTS_MESH_FN int mesh_trace_impl(const float4* __restrict__ bvh, const float4* __restrict__ tri4, f3 o, f3 d,
                                             float t_max, float& t_hit) {
   const f3 inv = mk(__fdividef(1.0f, d.x), __fdividef(1.0f, d.y), __fdividef(1.0f, d.z));
   int stack[40];
