@@ -139,7 +139,8 @@ def run_gpu(args):
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    c = I.as_f32(I.config(args.config))
+    c = I.as_f32(I.config(args.config, **({"ico_subdiv": args.mesh_subdiv} if args.config == 6 and
+                                          args.mesh_subdiv is not None else {})))
     if args.direction_mode:
         c["direction_mode"] = args.direction_mode
     if args.strategy:
@@ -244,6 +245,7 @@ def run_gpu(args):
                 "workload": c["name"], "config_index": args.config, "pixels": c["width"] * c["height"],
                 "bins": c["n_bins"], "spp": spp, "spp_mode": c["spp_mode"], "direction_mode": mode,
                 "paths_per_step": paths_per_step, "vertices_per_step": verts_per_step,
+                **({"triangles": len(c["mesh"]["tris"])} if c.get("mesh") else {}),
                 "parallelism": f"sample-range shards x{world}" + (
                     (" + fused peer-memory REDs" if args.reduce == "p2p" else " + NCCL reduce") if world > 1 else ""),
                 "l2": ("histogram (%.2f GB) > L2 is re-zeroed every step" if hist.numel() * 4 > 126e6 else
@@ -417,6 +419,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5, 6])
     ap.add_argument("--direction-mode", choices=["reuse", "split"], default=None)
+    ap.add_argument("--mesh-subdiv", type=int, default=None,
+                    help="config 6: icosphere subdivision level (2 = 320 triangles, 6 = 81920)")
     ap.add_argument("--strategy", choices=["darts", "vanilla", "da_only", "eda_only"], default=None,
                     help="estimator (default: the config's, DARTS); other values are comparison runs, not bench lines")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")

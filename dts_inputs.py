@@ -190,12 +190,13 @@ def staircase(x0, x1, y0, z0, n_steps: int, rise: float, run: float) -> np.ndarr
     return np.asarray(out, float)
 
 
-def mesh_config(**overrides) -> dict:
+def mesh_config(ico_subdiv: int = 2, **overrides) -> dict:
     """Config 6: config 4's fog cube with walls and two
     emitters, plus a glossy icosphere (rho 0.8, ks 0.9, Phong n 40; 320
     triangles) and a plastic staircase (rho 0.6, ks 0.25, n 15; 16 triangles),
-    time-gated in two bins of width 0.1."""
-    ico = icosphere((0.35, -0.45, 0.2), 0.35, 2)
+    time-gated in two bins of width 0.1.  ico_subdiv 4 / 6: 5120 / 81920
+    sphere triangles (BVH depth checks)."""
+    ico = icosphere((0.35, -0.45, 0.2), 0.35, ico_subdiv)
     st = staircase(-0.9, -0.1, -0.98, -0.2, 4, 0.2, 0.25)
     tris = np.concatenate([ico, st]).astype(np.float32).astype(np.float64)
     mat = np.concatenate([np.zeros(len(ico), np.int32), np.ones(len(st), np.int32)])

@@ -167,6 +167,7 @@ SAME_KEY = [
     ("cfg6_mesh", lambda: I.small(I.mesh_config(), 24, 24), 32),
     ("cfg6_mesh_split", lambda: I.small(I.mesh_config(direction_mode="split"), 16, 16), 16),
     ("cfg6_mesh_vanilla", lambda: I.small(I.mesh_config(strategy="vanilla"), 16, 16), 256),
+    ("cfg6_dense_mesh", lambda: I.small(I.mesh_config(ico_subdiv=4), 16, 16), 32),
     ("plate_lambert", lambda: I.plate_config([(0.8, 0.0, 1.0)]), 2000),
     ("plate_plastic_vanilla", lambda: I.plate_config([(0.7, 0.5, 10.0)], strategy="vanilla"), 100000),
 ]
