@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 
 import dts_inputs as I  # noqa: E402
 
-CROPS = {1: None, 2: None, 3: 32, 4: 128, 5: 32}
+CROPS = {1: None, 2: None, 3: 32, 4: 128, 5: 32, 6: None}
 
 
 def _render(dts, torch, c, spp, seed):
