@@ -557,7 +557,10 @@ __device__ __forceinline__ float conn_job_run(const DevScene& S, f3 x, f3 wc, fl
 // (conn_job_run), so the ~5-10 % of vertices that connect no longer run the
 // S sample and contribution at a few active lanes.
 constexpr int kJobWords = 11;  // x[3] w[3] dlo width coef m7e cell
-constexpr int kQueue = 32;     // slots per warp
+#ifndef DTS_QUEUE
+#define DTS_QUEUE 32
+#endif
+constexpr int kQueue = DTS_QUEUE;  // slots per warp
 constexpr int kJob1Words = 14;  // stage-1 job: x[3] w_prev[3] resM(hi, lo) coef r4 r5 r6 m7e cell
 // Stage-1 deferral (SPLIT: the whole connection stage queued) is a build
 // option (-DDTS_STAGE1=1): it executes 8 % fewer instructions on config 5 but

@@ -1504,12 +1504,16 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     // 8: A/B in profiles/ab_r01_refill*.log (configs 6 / 4 +4 % / +2 %, 5 and 3 +0.2 % / +0.4 % vs 16)
     P.refill_k = rk ? (uint32_t)atoi(rk) : 8u;
     if (P.refill_k < 1 || P.refill_k > 4096) P.refill_k = 8u;
+    // a warp flushes at >= flush_at queued jobs and then pushes <= 32 more: the
+    // shared slots plus the kQueue global overflow slots must hold flush_at - 1 + 32
+    static_assert(kQueue >= 16, "queue too short for a warp's pushes");
+    const uint32_t qcap = std::min<uint32_t>((uint32_t)kQueue, 2u * (uint32_t)kQueue - 31u);
     const char* f1 = getenv("DTS_FLUSH1_AT");
-    P.flush1_at = f1 ? (uint32_t)atoi(f1) : 16u;
-    if (P.flush1_at < 1 || P.flush1_at > (uint32_t)kQueue) P.flush1_at = 16u;
+    P.flush1_at = f1 ? (uint32_t)atoi(f1) : std::min<uint32_t>(16u, qcap);
+    if (P.flush1_at < 1 || P.flush1_at > qcap) P.flush1_at = std::min<uint32_t>(16u, qcap);
     const char* fa = getenv("DTS_FLUSH_AT");
-    P.flush_at = fa ? (uint32_t)atoi(fa) : 28u;
-    if (P.flush_at < 1 || P.flush_at > (uint32_t)kQueue) P.flush_at = 28u;
+    P.flush_at = fa ? (uint32_t)atoi(fa) : std::min<uint32_t>(28u, qcap);
+    if (P.flush_at < 1 || P.flush_at > qcap) P.flush_at = std::min<uint32_t>(28u, qcap);
     const size_t dyn = (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + (defer ? qbytes : 0);
     const void* kfn = darts_kernel_ptr(smem, defer, d);
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
