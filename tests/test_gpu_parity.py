@@ -285,6 +285,21 @@ def test_edge_cases(dts):
         dts.Scene(dict(c, crop=(0, 0, 5, 4)))
     with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
         dts.Scene(dict(c, n_ris=16))
+    with pytest.raises(dts.DtsError, match="exceeds 64 bits"):  # path ids (s N_pix + p) B + b
+        sc.render(1 << 62, 1, 0, 8, h)
+    # mesh scenes need the table in shared memory (a 32 x 32 table is not)
+    cm = I.as_f32(I.small(I.mesh_config(table_nr=32, table_ns=32), 4, 4))
+    sm = _scene(dts, cm)
+    hm = torch.zeros(sm.hist_shape(), device="cuda")
+    with pytest.raises(dts.DtsError, match="shared memory"):
+        sm.render(8, 1, 0, 8, hm)
+    # a single triangle
+    c1 = I.as_f32(I.small(I.mesh_config(), 4, 4))
+    c1["mesh"] = dict(c1["mesh"], tris=c1["mesh"]["tris"][-1:], tri_mat=c1["mesh"]["tri_mat"][-1:])
+    s1 = _scene(dts, c1)
+    h1, _, _ = dts.render_to_tensor(s1, 8, 2)
+    torch.cuda.synchronize()
+    assert torch.isfinite(h1).all()
 
 
 def test_sharding_sums_and_accumulates(dts):
