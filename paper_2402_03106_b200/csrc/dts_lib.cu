@@ -93,9 +93,10 @@ __device__ double e17_integrand(const TableParams& P, double C, double S, double
         const double t = pa + 0.5 * h * (1.0 + kGLx8[i]);
         const double r2 = t * t - 2.0 * t * C * cth + C * C;
         const double dt = S - t;
-        double phi = 0.0;
-        if (dt > 0.0) phi = norm * exp(-r2 * k / dt - P.sigma_a * dt) / (dt * sqrt(dt));
-        total += 0.5 * h * kGLw8[i] * P.sigma_s * exp(-P.sigma_t * t) * phi;
+        // sigma_s e^{-sigma_t t} Phi(r, dt): one exp of the summed exponents
+        if (dt > 0.0)
+          total += 0.5 * h * kGLw8[i] * P.sigma_s * norm * exp(-P.sigma_t * t - r2 * k / dt - P.sigma_a * dt) /
+                   (dt * sqrt(dt));
       }
     }
   }
