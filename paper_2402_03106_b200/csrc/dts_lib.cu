@@ -103,21 +103,29 @@ __device__ double e17_integrand(const TableParams& P, double C, double S, double
   return total;
 }
 
-// grid = cells, block = 256 (one thread per cos bin)
-__global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_t* __restrict__ q, size_t n_total) {
+// grid = cells, block = 1024: four threads per cos bin, two of its eight
+// cos-direction Gauss-Legendre nodes each (fp64 latency needs the occupancy:
+// 256 cells x 256 threads left 14 warps per SM)
+constexpr int kTableThreads = 1024;
+__global__ void __launch_bounds__(kTableThreads) table_build_kernel(TableParams P, uint16_t* __restrict__ q,
+                                                                   size_t n_total) {
   __shared__ double F[256];
   const int cell = blockIdx.x;
   const int ir = cell / P.ns, is = cell % P.ns;
   const double ratio = (ir + 0.5) / P.nr;
   const double S = P.smin * pow(P.smax / P.smin, (is + 0.5) / P.ns);
   const double C = ratio * S;
-  const int j = threadIdx.x;
+  const int bin = threadIdx.x >> 2, part = threadIdx.x & 3;
   const double dc = 2.0 / 256.0;
-  const double c0 = -1.0 + j * dc;
+  const double c0 = -1.0 + bin * dc;
   double acc = 0.0;
-  for (int n = 0; n < 8; ++n) acc += 0.5 * dc * kGLw8[n] * e17_integrand(P, C, S, c0 + 0.5 * dc * (1.0 + kGLx8[n]));
-  F[j] = acc;
+  for (int n = 2 * part; n < 2 * part + 2; ++n)
+    acc += 0.5 * dc * kGLw8[n] * e17_integrand(P, C, S, c0 + 0.5 * dc * (1.0 + kGLx8[n]));
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  if (part == 0) F[bin] = acc;
   __syncthreads();
+  const int j = threadIdx.x;
   __shared__ uint16_t Q[256];
   if (j == 0) {
     double total = 0.0;
@@ -132,6 +140,7 @@ __global__ void __launch_bounds__(256) table_build_kernel(TableParams P, uint16_
     }
   }
   __syncthreads();
+  if (j >= 256) return;
   // guide row (acceleration structure of the same inverse transform):
   // guide[g] = largest i with Q[i] <= 256 g
   int lo = 0, hi = 255;
@@ -1361,7 +1370,7 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
   P.smax = smax;
   P.nr = nr;
   P.ns = ns;
-  table_build_kernel<<<nr * ns, 256, 0, (cudaStream_t)stream>>>(P, s->d_table, n);
+  table_build_kernel<<<nr * ns, kTableThreads, 0, (cudaStream_t)stream>>>(P, s->d_table, n);
   s->S.table_n = (uint32_t)n;
   CUDA_TRY(cudaGetLastError());
   s->S.nr = nr;
