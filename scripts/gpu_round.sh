@@ -10,7 +10,7 @@ bash scripts/build_variants.sh "checks:-DDTS_CHECKS=1" > /dev/null 2>&1
 DTS_LIB=libdts_checks.so timeout 300 python scripts/sanitize_case.py > gpurun_out/checks.log 2>&1; echo "checks rc=$?"
 timeout 1800 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-for c in 1 2 3 4; do
+for c in 1 2 3 4 6; do
   timeout 900 python bench.py --config $c --cpu-budget 10 > gpurun_out/bench_${TAG}_c$c.json 2> gpurun_out/bench_${TAG}_c$c.err
 done
 timeout 900 python bench.py > gpurun_out/bench_${TAG}_c5.json 2> gpurun_out/bench_${TAG}_c5.err; echo "bench rc=$?"
