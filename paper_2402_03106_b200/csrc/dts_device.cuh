@@ -391,21 +391,48 @@ __device__ __forceinline__ float bsdf_eval(const DevScene& S, int mat, f3 n, f3 
   return fmaf(S.mat_kl[mat], lobe_pow(dot(wo, r), S.mat_n[mat]), S.mat_kd[mat]);
 }
 
-// medium length and visibility of the segment p -> xe (p inside the medium)
+// R32 sampling at a surface vertex with normal n (incident side) and incident
+// direction w: u_lobe < ks picks the lobe (cos alpha = u^{1/(n+1)} about the
+// mirror direction), else the cosine hemisphere (cos theta = sqrt(1 - u));
+// phi = 2 pi u_phi.  Writes wo; returns f cos / p_mix, 0 below the surface.
+__device__ __forceinline__ float bsdf_sample(const DevScene& S, int mat, f3 n, f3 w, float u_lobe, float u,
+                                             float u_phi, f3& wo) {
+  const float phi = 2.0f * kPi * u_phi;
+  const f3 rm = w - n * (2.0f * dot(w, n));
+  if (u_lobe < S.mat_ks[mat]) {
+    const float ca = lobe_pow(u, S.mat_inv_n1[mat]);
+    wo = from_frame(rm, 1.0f + ca, 1.0f - ca, phi);
+  } else {
+    const float lz = sqrtf(1.0f - u);
+    wo = from_frame(n, 1.0f + lz, __fdividef(u, 1.0f + lz), phi);
+  }
+  const float co = dot(wo, n);
+  if (!(co > 0.0f)) return 0.0f;
+  const float pw = lobe_pow(dot(wo, rm), S.mat_n[mat]);
+  return fmaf(S.mat_kl[mat], pw, S.mat_kd[mat]) * co * __fdividef(1.0f, fmaf(S.mat_pd[mat], co, S.mat_pl[mat] * pw));
+}
+
+// medium length of the segment p -> xe (p inside the medium, dir its unit
+// direction, r its length), or -1 if the segment is occluded
 template <int SH, bool WALLS, bool MESH = false>
-__device__ __forceinline__ float segment_tr(const DevScene& S, f3 p, f3 xe, float r, f3 dir) {
+__device__ __forceinline__ float segment_len(const DevScene& S, f3 p, float r, f3 dir) {
   if (MESH) {  // R32: a triangle on the segment occludes it
     float tm;
-    if (mesh_trace<true>(S, p, dir, r, tm) >= 0) return 0.0f;
+    if (mesh_trace<true>(S, p, dir, r, tm) >= 0) return -1.0f;
   }
-  if (SH == DTS_MEDIUM_INFINITE) return fexp(-S.sigma_t * r);
+  if (SH == DTS_MEDIUM_INFINITE) return r;
   float lo, hi;
   int face;
   const int hit = intersect_inside<SH, WALLS>(S, p, dir, lo, hi, face);
-  if (hit == HIT_MISS) return 1.0f;
-  if (WALLS && hit == HIT_WALL && hi < r) return 0.0f;  // occluded by a wall (R15)
-  const float len = fmaxf(0.0f, fminf(hi, r) - lo);
-  return fexp(-S.sigma_t * len);
+  if (hit == HIT_MISS) return 0.0f;
+  if (WALLS && hit == HIT_WALL && hi < r) return -1.0f;  // occluded by a wall (R15)
+  return fmaxf(0.0f, fminf(hi, r) - lo);
+}
+// its transmittance (0 when occluded)
+template <int SH, bool WALLS, bool MESH = false>
+__device__ __forceinline__ float segment_tr(const DevScene& S, f3 p, f3 xe, float r, f3 dir) {
+  const float len = segment_len<SH, WALLS, MESH>(S, p, r, dir);
+  return len < 0.0f ? 0.0f : fexp(-S.sigma_t * len);
 }
 
 __device__ __forceinline__ f3 inward_normal(int face) {
@@ -519,15 +546,19 @@ __device__ __forceinline__ float conn_contrib(const DevScene& S, f3 x, f3 wc, f3
                                               float pSt, float clo, float coef, f3* xell_out, float* r2_out) {
   const f3 xell = fma3(wc, t, x);
   const f3 de = xe - xell;
-  float r2sq = dot(de, de);
-  float r2 = sqrtf(r2sq);
-  const f3 we = de * __fdividef(1.0f, r2);
+  float r2, r2sq;
   if (pSt > 0.0f) {  // on the ellipse r2 = S - t, formed without cancellation
     r2 = pSt;
     r2sq = pSt * pSt;
+  } else {
+    r2sq = dot(de, de);
+    r2 = sqrtf(r2sq);
   }
+  const f3 we = de * __fdividef(1.0f, r2);
   const float rho = hg_eval(S, dot(wc, we));
-  const float tr = fexp(-S.sigma_t * (t - clo)) * segment_tr<SH, WALLS, MESH>(S, xell, xe, r2, we);
+  // transmittance of both legs in one exponential
+  const float len2 = segment_len<SH, WALLS, MESH>(S, xell, r2, we);
+  const float tr = len2 < 0.0f ? 0.0f : fexp(-S.sigma_t * ((t - clo) + len2));
   float c = coef * S.sigma_s * tr * rho * ek * __fdividef(1.0f, r2sq * pt);
   if (S.r_excl > 0.0f && r2 < S.r_excl) c = 0.0f;
   if (xell_out) *xell_out = xell;
@@ -841,27 +872,14 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       wall_nee = nee > 0.0f;
       if (nsamp && nee != 0.0f) ++*nsamp;
     }
-    // lobe (u4 < ks: cos alpha = u5^{1/(n+1)} about the mirror direction r) or
-    // cosine hemisphere (cos theta = sqrt(1 - u5) about n); phi = 2 pi u6;
-    // weight f cos / ((1 - ks) cos / pi + ks p_lobe)
-    const float u4 = unif(r[4]), u5 = unif(r[5]);
-    const float phi = 2.0f * kPi * unif(r[6]);
-    const f3 rm = ps.w - n * (2.0f * dot(ps.w, n));
+    // lobe u4, direction u5, u6
     f3 wo;
-    if (u4 < S.mat_ks[mat]) {
-      const float ca = lobe_pow(u5, S.mat_inv_n1[mat]);
-      wo = from_frame(rm, 1.0f + ca, 1.0f - ca, phi);
-    } else {
-      const float lz = sqrtf(1.0f - u5);
-      wo = from_frame(n, 1.0f + lz, __fdividef(u5, 1.0f + lz), phi);
-    }
-    const float co = dot(wo, n);
-    if (!(co > 0.0f)) {  // below the surface: the path ends
+    const float wgt = bsdf_sample(S, mat, n, ps.w, unif(r[4]), unif(r[5]), unif(r[6]), wo);
+    if (!(wgt > 0.0f)) {  // below the surface: the path ends
       end_reason = DTS_CTR_ESCAPES;
       return false;
     }
-    const float pw = lobe_pow(dot(wo, rm), S.mat_n[mat]);
-    ps.beta *= fmaf(S.mat_kl[mat], pw, S.mat_kd[mat]) * co * __fdividef(1.0f, fmaf(S.mat_pd[mat], co, S.mat_pl[mat] * pw));
+    ps.beta *= wgt;
     wc = ww = wo;
   } else {
     // medium vertex: one-sample MIS of EDA and HG

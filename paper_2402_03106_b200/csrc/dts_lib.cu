@@ -833,21 +833,10 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
         // R32 sampling (lobe u3, direction u1 u2; the oracle's vanilla order)
         int mat;
         const f3 n = tri_side_normal(S, face, w, mat);
-        const float u5 = unif(r.b);
-        const float phi = 2.0f * kPi * unif(r.c);
-        const f3 rm = w - n * (2.0f * dot(w, n));
         f3 wo;
-        if (unif(r.d) < S.mat_ks[mat]) {
-          const float ca = lobe_pow(u5, S.mat_inv_n1[mat]);
-          wo = from_frame(rm, 1.0f + ca, 1.0f - ca, phi);
-        } else {
-          const float lz = sqrtf(1.0f - u5);
-          wo = from_frame(n, 1.0f + lz, __fdividef(u5, 1.0f + lz), phi);
-        }
-        const float co = dot(wo, n);
-        if (!(co > 0.0f)) { ++c_esc; alive = false; break; }
-        const float pw = lobe_pow(dot(wo, rm), S.mat_n[mat]);
-        beta *= fmaf(S.mat_kl[mat], pw, S.mat_kd[mat]) * co * __fdividef(1.0f, fmaf(S.mat_pd[mat], co, S.mat_pl[mat] * pw));
+        const float wgt = bsdf_sample(S, mat, n, w, unif(r.d), unif(r.b), unif(r.c), wo);
+        if (!(wgt > 0.0f)) { ++c_esc; alive = false; break; }
+        beta *= wgt;
         w = wo;
       }
       float lo, hi;
