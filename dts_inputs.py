@@ -206,6 +206,21 @@ def mesh_config(ico_subdiv: int = 2, **overrides) -> dict:
     return c
 
 
+def sphere_mesh_config(**overrides) -> dict:
+    """Config 2's sphere (unwarped camera) with a glossy icosphere (r 0.3, 80
+    triangles) and a Lambertian square plate (two triangles) inside: meshes in a
+    SPHERE medium and the R17 shell intervals cut at a surface."""
+    ico = icosphere((0.2, 0.1, 0.25), 0.3, 1)
+    q = [(-0.6, -0.6, -0.3), (0.6, -0.6, -0.3), (0.6, 0.6, -0.3), (-0.6, 0.6, -0.3)]
+    plate = np.array([[q[0], q[1], q[2]], [q[0], q[2], q[3]]], float)
+    tris = np.concatenate([ico, plate]).astype(np.float32).astype(np.float64)
+    mat = np.concatenate([np.zeros(len(ico), np.int32), np.ones(2, np.int32)])
+    c = config(2, name="cfg2_sphere_mesh")
+    c["mesh"] = dict(tris=tris.reshape(-1, 9), tri_mat=mat, mats=[(0.8, 0.7, 30.0), (0.7, 0.0, 1.0)])
+    c.update(overrides)
+    return c
+
+
 def plate_config(mats, **overrides) -> dict:
     """A 4 x 4 square plate (two triangles) at z = 0 in an infinite, almost
     non-scattering medium (sigma_s = 1e-4), a pulse emitter and a fluence
@@ -240,16 +255,20 @@ def _unit(rng, n):
     return v / np.linalg.norm(v, axis=1, keepdims=True)
 
 
-def debug_records(c: dict, n: int, seed: int, kinds=("camera", "medium", "wall")) -> dict:
+def debug_records(c: dict, n: int, seed: int, kinds=("camera", "medium", "wall", "surface")) -> dict:
     """Random vertex states for ``dts_sample_debug`` parity.  Returns a dict of
-    numpy arrays (kind, face, bin, emitter, x[n,3], w[n,3], E, beta, r[n,12])."""
+    numpy arrays (kind, face, bin, emitter, x[n,3], w[n,3], E, beta, r[n,12]).
+    Surface records (mesh scenes): a uniform point of a random triangle, moved
+    1e-4 off it on the side the incoming direction arrives from (R33)."""
     rng = np.random.default_rng(seed)
     kind = np.zeros(n, np.int32)
     face = np.full(n, -1, np.int32)
     x = np.zeros((n, 3))
     w = _unit(rng, n)
-    names = {"camera": 0, "medium": 1, "wall": 2}
+    names = {"camera": 0, "medium": 1, "wall": 2, "surface": 3}
     allowed = [names[k] for k in kinds]
+    if c.get("mesh") is None and 3 in allowed:
+        allowed.remove(3)
     if c["medium"] == "box" and c["wall_mask"] == 0 and 2 in allowed:
         allowed.remove(2)
     if c["medium"] != "box" and 2 in allowed:
@@ -269,6 +288,19 @@ def debug_records(c: dict, n: int, seed: int, kinds=("camera", "medium", "wall")
                 x[i] = np.asarray(c["cam_pos"]) + _unit(rng, 1)[0] * c["det_radius"] * rng.uniform() ** (1 / 3)
         elif kind[i] == 1:
             x[i] = _inside(c, rng)
+        elif kind[i] == 3:
+            tris = np.asarray(c["mesh"]["tris"], float).reshape(-1, 3, 3)
+            t = int(rng.integers(0, len(tris)))
+            face[i] = t
+            u, v = rng.uniform(size=2)
+            if u + v > 1.0:
+                u, v = 1.0 - u, 1.0 - v
+            pt = tris[t, 0] + u * (tris[t, 1] - tris[t, 0]) + v * (tris[t, 2] - tris[t, 0])
+            nrm = np.cross(tris[t, 1] - tris[t, 0], tris[t, 2] - tris[t, 0])
+            nrm /= np.linalg.norm(nrm)
+            if w[i] @ nrm > 0.0:
+                nrm = -nrm
+            x[i] = pt + 1e-4 * nrm
         else:
             faces = [f for f in range(6) if (c["wall_mask"] >> f) & 1]
             f = int(rng.choice(faces))

@@ -113,8 +113,8 @@ typedef struct {
   int32_t conn_sampling;             /* DTS_CONN_* (0 = paper) */
   /* Triangle meshes (the opaque surfaces of PAPER.md:105, 221,
    * 301, Table 1; readings R32, R33 in DESIGN.md): thin, two-sided, opaque
-   * triangles strictly inside the medium (every vertex >= 1e-3 inside a BOX,
-   * inside a SPHERE's radius - 1e-3; SPHERE media take no mesh).  A ray's medium
+   * triangles strictly inside the medium (every vertex >= 1e-3 inside a BOX or
+   * within a SPHERE's radius - 1e-3).  A ray's medium
    * interval ends at the nearest triangle (case II of PAPER.md:301); a surface
    * vertex sits 1e-4 off its triangle on the incident side (R33), does the
    * time-checked NEE of R14 with the BSDF, samples the BSDF and connects like a
@@ -126,7 +126,7 @@ typedef struct {
    * keeps ownership.  Rejected (DTS_E_INVALID_ARG): n_tris < 0, null arrays,
    * material index outside [0, n_mats), 1 > n_mats or n_mats > DTS_MAX_MATERIALS,
    * rho or ks outside [0, 1], n < 0, a vertex outside the medium margin,
-   * degenerate (zero-area) triangles.  dts_sample_debug does not take mesh scenes. */
+   * degenerate (zero-area) triangles. */
   int32_t n_tris;
   const float* tris;                 /* HOST, n_tris x 9 floats: v0, v1, v2 */
   const int32_t* tri_mat;            /* HOST, n_tris material indices */
@@ -144,7 +144,10 @@ typedef struct {
 
 /* Debug record: one DARTS vertex with caller-fixed state and raw Philox words.
  * kind: 0 camera/detector vertex (k = 0, direction fixed = w), 1 medium vertex
- * (w = incoming direction w_{k-1}), 2 wall vertex (face = wall index).
+ * (w = incoming direction w_{k-1}), 2 wall vertex (face = wall index), 3 surface
+ * vertex of a mesh scene (face = triangle index in the caller's order, x the
+ * vertex position off the triangle, R33; a record whose index is out of range
+ * is returned with terminate = 1 and nothing else set).
  * u_i = (r_i >> 9) * 2^-23 (R24): u0 event, u1 Sobol row, u2 CP shift, u3 RIS
  * select, u4 technique, u5 cos/bin, u6 phi, u7 connection; the SPLIT walk's
  * u8/u9 come from the low bits of r0..r2 / r3..r5; r8..r11 are reserved. */
@@ -158,16 +161,16 @@ typedef struct {
 } dts_debug_in;
 
 typedef struct {
-  int32_t tech;   /* 0 HG, 1 EDA, 2 camera (fixed), 3 wall cosine */
+  int32_t tech;   /* 0 HG, 1 EDA, 2 camera (fixed), 3 wall cosine, 4 surface BSDF (R32) */
   float gamma, p_eda, p_hg, p_mix;
   float wc[3], ww[3]; /* connection direction, walk direction */
   float beta_dir, wconn;
   float t_lo, t_hi, tc_lo, tc_hi; /* medium interval along ww / wc */
-  int32_t hit, face_hit;          /* 0 none (infinite), 1 open boundary, 2 wall, 3 miss */
+  int32_t hit, face_hit;          /* 0 none (infinite), 1 open boundary, 2 wall, 3 miss, 4 triangle (face_hit: caller's index) */
   float S_lo, S_hi, S, t, x_ell[3], p_t, contrib, nee;
   int32_t conn_valid;
   float p_m;
-  int32_t event; /* 0 miss, 1 medium (RIS), 2 wall, 3 escape, 4 RIS all-invalid */
+  int32_t event; /* 0 miss, 1 medium (RIS), 2 wall, 3 escape, 4 RIS all-invalid, 5 triangle */
   float cand_d[8], cand_wn[8];
   int32_t istar;
   float d, x_next[3], beta_ris;

@@ -17,6 +17,7 @@
 
 #include <math.h>
 #include <pthread.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -82,9 +83,11 @@ static void cross3(const double a[3], const double b[3], double o[3]) {
 }
 static void normalize3(double a[3]) { double n = norm3(a); a[0] /= n; a[1] /= n; a[2] /= n; }
 
-/* R12: orthonormal frame about n (Duff et al. 2017, branchless). */
+/* R12: orthonormal frame about n (Duff et al. 2017); the chart is +z for
+ * n_z >= -1e-6 (a tie-break: a horizontal normal whose n_z rounds to +-0 or
+ * +-tiny picks one frame on both sides), else -z. */
 static void onb(const double n[3], double b1[3], double b2[3]) {
-  double sign = copysign(1.0, n[2]);
+  double sign = n[2] >= -1e-6 ? 1.0 : -1.0;
   double a = -1.0 / (sign + n[2]);
   double b = n[0] * n[1] * a;
   b1[0] = 1.0 + sign * n[0] * n[0] * a; b1[1] = sign * b; b1[2] = -sign * n[0];
@@ -1081,6 +1084,11 @@ static int response_bin(const or_scene* sc, const uint32_t* cdf, uint32_t m, dou
   return b;
 }
 
+/* Test-only trace of one path id to stderr (OR_TRACE_ID, read at first render). */
+static uint64_t g_trace_id = ~0ull;
+static FILE* g_trace_file = NULL;
+static or_debug_out g_trace_out;
+
 /* One DARTS path; returns acc (sum of its contributions). */
 static double darts_path(const or_scene* sc, const derived* dv, const uint16_t* q, uint64_t seed,
                          uint64_t id, int px, int py, int b, double* order_acc, int n_orders,
@@ -1124,7 +1132,17 @@ static double darts_path(const or_scene* sc, const derived* dv, const uint16_t* 
     draw4(seed, id, (uint32_t)k, 1, r + 4);
     r[8] = r[9] = r[10] = r[11] = 0u; /* reserved */
     double c;
-    alive = darts_vertex(sc, dv, q, &ps, r, &c, NULL, st);
+    if (g_trace_id == id && g_trace_file)
+      fprintf(g_trace_file, "IN %d %d %d %.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g\n", k, ps.kind, ps.face,
+              ps.x[0], ps.x[1], ps.x[2], ps.w[0], ps.w[1], ps.w[2], ps.E, ps.beta);
+    alive = darts_vertex(sc, dv, q, &ps, r, &c, g_trace_id == id ? &g_trace_out : NULL, st);
+    if (g_trace_id == id && g_trace_file)
+      fprintf(g_trace_file, "OUT %d contrib %.9g event %d hit %d face_hit %d t_hi %.9g tc_hi %.9g S %.9g t %.9g p_t %.9g "
+              "istar %d d %.9g beta_out %.9g m_event %.3g m_select %.3g m_tech %.3g m_cell %.3g m_valid %.3g m_conn %.3g\n",
+              k, c, g_trace_out.event, g_trace_out.hit, g_trace_out.face_hit, g_trace_out.t_hi, g_trace_out.tc_hi,
+              g_trace_out.S, g_trace_out.t, g_trace_out.p_t, g_trace_out.istar, g_trace_out.d, g_trace_out.beta_out,
+              g_trace_out.m_event, g_trace_out.m_select, g_trace_out.m_tech, g_trace_out.m_cell, g_trace_out.m_valid,
+              g_trace_out.m_conn);
     if (st) st->vertices++;
     if (nvert) (*nvert)++;
     acc += c;
@@ -1407,6 +1425,11 @@ int or_render_ids(const or_scene* sc, const uint16_t* q, uint64_t spp, uint64_t 
   uint64_t B = (uint64_t)sc->n_bins;
   uint64_t Npix = (uint64_t)sc->width * sc->height;
   (void)spp;
+  const char* tr = getenv("OR_TRACE_ID");
+  const char* tf = getenv("OR_TRACE_FILE");
+  g_trace_id = (tr && tf) ? strtoull(tr, NULL, 10) : ~0ull;
+  if (g_trace_file) fclose(g_trace_file);
+  g_trace_file = (tr && tf) ? fopen(tf, "w") : NULL;
   for (int i = 0; i < n; ++i) {
     uint64_t id = ids[i];
     uint64_t p;
@@ -1430,5 +1453,6 @@ int or_render_ids(const or_scene* sc, const uint16_t* q, uint64_t spp, uint64_t 
     int px = (int)(p % (uint64_t)sc->width), py = (int)(p / (uint64_t)sc->width);
     acc[i] = darts_path(sc, &dv, q, seed, id, px, py, b, NULL, 0, NULL, nvert ? &nvert[i] : NULL);
   }
+  if (g_trace_file) { fclose(g_trace_file); g_trace_file = NULL; }
   return 0;
 }

@@ -85,6 +85,8 @@ struct DevScene {
   // each: (v0.xyz, int material), (e1.xyz, -), (e2.xyz, -)
   const float4* bvh;
   const float4* tri4;
+  const int32_t* tri_leaf;  // caller's triangle index -> leaf order (debug records)
+  const int32_t* tri_orig;  // leaf order -> caller's triangle index (debug output)
   int32_t n_tris;
   // R32 per material: select ks, f = kd + kl pow(ca, n), p = pd cos + pl pow(ca, n), 1 / (n + 1)
   float mat_ks[DTS_MAX_MATERIALS], mat_kd[DTS_MAX_MATERIALS], mat_kl[DTS_MAX_MATERIALS];
@@ -186,7 +188,9 @@ __device__ __forceinline__ float fexp(float x) { return exp2f(x * kLog2e); }
 // from opc = 1 + cos and omc = 1 - cos, each computed without cancellation by
 // the caller, so directions near the pole (HG with g = 0.9) keep fp32 accuracy.
 __device__ __forceinline__ f3 from_frame(f3 n, float opc, float omc, float phi) {
-  const float sign = copysignf(1.0f, n.z);
+  // R12 tie-break: n_z >= -1e-6 takes the +z chart, so a structurally horizontal
+  // normal (mesh facets) picks the same frame whatever the sign of its rounded n_z
+  const float sign = n.z >= -1e-6f ? 1.0f : -1.0f;
   const float a = __fdividef(-1.0f, sign + n.z);  // sign + n.z in [1, 2]
   const float b = n.x * n.y * a;
   const f3 b1 = mk(1.0f + sign * n.x * n.x * a, sign * b, -sign * n.x);
@@ -400,8 +404,10 @@ __device__ __forceinline__ float bsdf_sample(const DevScene& S, int mat, f3 n, f
   const float phi = 2.0f * kPi * u_phi;
   const f3 rm = w - n * (2.0f * dot(w, n));
   if (u_lobe < S.mat_ks[mat]) {
-    const float ca = lobe_pow(u, S.mat_inv_n1[mat]);
-    wo = from_frame(rm, 1.0f + ca, 1.0f - ca, phi);
+    // 1 - cos alpha = 1 - u^{1/(n+1)} = 1 - e^{ln(u)/(n+1)} without cancellation
+    // (a sharp lobe puts cos alpha within 1e-5 of 1)
+    const float omc = one_m_exp(-__log2f(u) * (kLn2 * S.mat_inv_n1[mat]));
+    wo = from_frame(rm, 2.0f - omc, omc, phi);
   } else {
     const float lz = sqrtf(1.0f - u);
     wo = from_frame(n, 1.0f + lz, __fdividef(u, 1.0f + lz), phi);
@@ -782,7 +788,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   wall_nee = false;
   end_reason = 0;
   constexpr bool WALLS = (FL & FL_WALLS) != 0, SPLIT = (FL & FL_SPLIT) != 0, MESH = (FL & FL_MESH) != 0;
-  static_assert(!(MESH && (DEFER || DBG)), "mesh scenes run the immediate render kernels only");
+  static_assert(!(MESH && DEFER), "mesh scenes run the immediate render kernels only");
   const int e = (FL & FL_MULTI_E) ? ps.e : 0;  // one emitter: constant-bank operands
   const f3 xe = ld3(S.em_pos[e]);
   const float ek = S.em_k[e];
@@ -871,11 +877,17 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       contrib += nee;
       wall_nee = nee > 0.0f;
       if (nsamp && nee != 0.0f) ++*nsamp;
+      if (DBG) dbg->nee = nee;
     }
     // lobe u4, direction u5, u6
     f3 wo;
     const float wgt = bsdf_sample(S, mat, n, ps.w, unif(r[4]), unif(r[5]), unif(r[6]), wo);
+    if (DBG) {
+      dbg->tech = 4;
+      dbg->beta_dir = wgt;
+    }
     if (!(wgt > 0.0f)) {  // below the surface: the path ends
+      if (DBG) { dbg->event = 3; dbg->terminate = 1; dbg->beta_out = ps.beta; }
       end_reason = DTS_CTR_ESCAPES;
       return false;
     }
@@ -1204,6 +1216,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       ps.kind = KIND_SURF;
       ps.face = face;
       ps.w = ww;
+      if (DBG) { dbg->event = 5; dbg->d = hi; dbg->beta_ris = 1.0f; }
     } else {
       if (DBG) { dbg->event = 3; dbg->terminate = 1; dbg->beta_out = ps.beta; }
       end_reason = DTS_CTR_ESCAPES;

@@ -54,6 +54,7 @@ struct dts_scene {
   size_t qover_n = 0;
   float4* d_bvh = nullptr;         // mesh BVH nodes (R32)
   float4* d_tri4 = nullptr;        // mesh triangles in leaf order
+  int32_t* d_tri_map = nullptr;    // caller -> leaf order, then leaf -> caller order (2 n_tris)
   int num_sms = 0;
   int device = 0;
 };
@@ -162,12 +163,17 @@ __global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n
   memset(&o, 0, sizeof(o));
   o.istar = -1;
   const dts_debug_in rec = in[i];
+  if ((FL & FL_MESH) && rec.kind == KIND_SURF && (uint32_t)rec.face >= (uint32_t)S.n_tris) {
+    o.terminate = 1;
+    out[i] = o;
+    return;
+  }
   PathState ps;
   ps.x = mk(rec.x[0], rec.x[1], rec.x[2]);
   ps.w = mk(rec.w[0], rec.w[1], rec.w[2]);
   ps.beta = rec.beta;
   ps.kind = rec.kind;
-  ps.face = rec.face;
+  ps.face = ((FL & FL_MESH) && rec.kind == KIND_SURF) ? S.tri_leaf[rec.face] : rec.face;
   ps.e = rec.emitter;
   const double RM = S.t0 + (double)(rec.bin + 1) * S.dt - (double)S.em_t[rec.emitter];
   ps.resM = RM - rec.E;
@@ -177,6 +183,7 @@ __global__ void debug_kernel(DevScene S, const uint16_t* __restrict__ tab, int n
   bool cn, wn;
   int reason;
   darts_vertex<true, false, SH, FL>(S, tab, ps, r, c, &o, cn, wn, reason);
+  if ((FL & FL_MESH) && o.hit == HIT_SURF) o.face_hit = S.tri_orig[o.face_hit];
   o.E_next = RM - ps.resM;
   out[i] = o;
 }
@@ -821,7 +828,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
         const float rr = sqrtf(u5);
         float sp, cp;
         __sincosf(2.0f * kPi * u6, &sp, &cp);
-        const float sign = copysignf(1.0f, n.z);
+        const float sign = n.z >= -1e-6f ? 1.0f : -1.0f;  // R12 tie-break (from_frame)
         const float aa = __fdividef(-1.0f, sign + n.z);
         const float bq = n.x * n.y * aa;
         const f3 b1 = mk(1.0f + sign * n.x * n.x * aa, sign * bq, -sign * n.x);
@@ -969,16 +976,21 @@ template <int FL> struct PickDebug {
   static const void* inf() { return dk_ptr<DTS_MEDIUM_INFINITE, FL>(); }
   static const void* sph() { return dk_ptr<DTS_MEDIUM_SPHERE, FL>(); }
 };
+template <int FL> struct PickDebugMesh {
+  static const void* box() { return dk_ptr<DTS_MEDIUM_BOX, FL | FL_MESH>(); }
+  static const void* inf() { return dk_ptr<DTS_MEDIUM_INFINITE, FL | FL_MESH>(); }
+  static const void* sph() { return dk_ptr<DTS_MEDIUM_SPHERE, FL | FL_MESH>(); }
+};
 static int scene_flags(const dts_scene_desc& d) {
   return (d.wall_mask ? FL_WALLS : 0) | (d.direction_mode == DTS_DIR_SPLIT ? FL_SPLIT : 0) |
          (d.n_emitters > 1 ? FL_MULTI_E : 0);
 }
-// mesh scenes (FL_MESH): immediate kernels with the table in shared memory, BOX or INFINITE media
+// mesh scenes (FL_MESH): immediate kernels with the table in shared memory
 template <int FL>
 struct PickMesh {
   static const void* box() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_BOX, FL | FL_MESH, false>; }
   static const void* inf() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_INFINITE, FL | FL_MESH, false>; }
-  static const void* sph() { return nullptr; }
+  static const void* sph() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_SPHERE, FL | FL_MESH, false>; }
 };
 static const void* darts_kernel_ptr(bool smem, bool defer, const dts_scene_desc& d) {
   const int sh = d.medium_shape, fl = scene_flags(d);
@@ -986,10 +998,14 @@ static const void* darts_kernel_ptr(bool smem, bool defer, const dts_scene_desc&
   if (smem) return defer ? pick_fl<PickRender<true, true>::F>(sh, fl) : pick_fl<PickRender<true, false>::F>(sh, fl);
   return defer ? pick_fl<PickRender<false, true>::F>(sh, fl) : pick_fl<PickRender<false, false>::F>(sh, fl);
 }
-static const void* debug_kernel_ptr(const dts_scene_desc& d) { return pick_fl<PickDebug>(d.medium_shape, scene_flags(d)); }
+static const void* debug_kernel_ptr(const dts_scene_desc& d) {
+  return d.n_tris > 0 ? pick_fl<PickDebugMesh>(d.medium_shape, scene_flags(d))
+                      : pick_fl<PickDebug>(d.medium_shape, scene_flags(d));
+}
 static const void* vanilla_kernel_ptr(int shape, bool walls, bool mesh) {
   if (mesh) {
     if (shape == DTS_MEDIUM_INFINITE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_INFINITE, false, true>;
+    if (shape == DTS_MEDIUM_SPHERE) return (const void*)render_vanilla_kernel<DTS_MEDIUM_SPHERE, false, true>;
     if (shape == DTS_MEDIUM_BOX)
       return walls ? (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, true, true>
                    : (const void*)render_vanilla_kernel<DTS_MEDIUM_BOX, false, true>;
@@ -1060,7 +1076,6 @@ static dts_status validate(const dts_scene_desc& d) {
   if (d.n_tris < 0) return bad("n_tris must be >= 0");
   if (d.n_tris > 0) {  // R32, R33
     if (!d.tris || !d.tri_mat) return bad("mesh arrays are NULL");
-    if (d.medium_shape == DTS_MEDIUM_SPHERE) return bad("mesh scenes need a BOX or INFINITE medium");
     if (d.n_mats < 1 || d.n_mats > DTS_MAX_MATERIALS) return bad("n_mats must be 1..8");
     for (int m = 0; m < d.n_mats; ++m)
       if (!(d.mats[m][0] >= 0.0f && d.mats[m][0] <= 1.0f) || !(d.mats[m][1] >= 0.0f && d.mats[m][1] <= 1.0f) ||
@@ -1076,6 +1091,12 @@ static dts_status validate(const dts_scene_desc& d) {
           for (int a = 0; a < 3; ++a)
             if (!(v[3 * k + a] >= d.bmin[a] + 1e-3f && v[3 * k + a] <= d.bmax[a] - 1e-3f))
               return bad("mesh vertices must lie >= 1e-3 inside the box");
+      if (d.medium_shape == DTS_MEDIUM_SPHERE)
+        for (int k = 0; k < 3; ++k) {
+          double r2 = 0.0;
+          for (int a = 0; a < 3; ++a) r2 += ((double)v[3 * k + a] - d.center[a]) * ((double)v[3 * k + a] - d.center[a]);
+          if (!(std::sqrt(r2) <= (double)d.radius - 1e-3)) return bad("mesh vertices must lie >= 1e-3 inside the sphere");
+        }
       double e1[3], e2[3], n[3];
       for (int a = 0; a < 3; ++a) { e1[a] = (double)v[3 + a] - v[a]; e2[a] = (double)v[6 + a] - v[a]; }
       vcross(e1, e2, n);
@@ -1151,9 +1172,18 @@ static dts_status upload_mesh(dts_scene* s) {
     return fail(DTS_E_OOM, "cudaMalloc(mesh) failed");
   CUDA_TRY(cudaMemcpy(s->d_bvh, nodes.data(), nodes.size() * sizeof(float4), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(s->d_tri4, tri4.data(), tri4.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  std::vector<int32_t> tmap(2 * (size_t)d.n_tris);
+  for (int i = 0; i < d.n_tris; ++i) {
+    tmap[(size_t)ord[i]] = i;              // caller's index -> leaf position
+    tmap[(size_t)d.n_tris + i] = ord[i];   // leaf position -> caller's index
+  }
+  if (cudaMalloc(&s->d_tri_map, tmap.size() * sizeof(int32_t)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(mesh) failed");
+  CUDA_TRY(cudaMemcpy(s->d_tri_map, tmap.data(), tmap.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   DevScene& S = s->S;
   S.bvh = s->d_bvh;
   S.tri4 = s->d_tri4;
+  S.tri_leaf = s->d_tri_map;
+  S.tri_orig = s->d_tri_map + d.n_tris;
   S.n_tris = d.n_tris;
   for (int m = 0; m < d.n_mats; ++m) {  // R32 constants
     const double rho = d.mats[m][0], ks = d.mats[m][1], n = d.mats[m][2];
@@ -1321,6 +1351,7 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaFree(s->d_qover);
   cudaFree(s->d_bvh);
   cudaFree(s->d_tri4);
+  cudaFree(s->d_tri_map);
   delete s;
   return DTS_OK;
 }
@@ -1590,7 +1621,6 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
 
 dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, dts_debug_out* d_out, void* stream) {
   if (!s || (n > 0 && (!d_in || !d_out)) || n < 0) return fail(DTS_E_INVALID_ARG, "bad arguments");
-  if (s->desc.n_tris > 0) return fail(DTS_E_INVALID_ARG, "dts_sample_debug does not take mesh scenes");
   if (n == 0) return DTS_OK;
   if (s->desc.strategy != DTS_STRATEGY_VANILLA && !s->d_table) return fail(DTS_E_STATE, "table not built");
   const uint16_t* tab = s->d_table;

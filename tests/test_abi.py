@@ -83,7 +83,7 @@ MESH_BAD = [
     ("no_materials", dict(n_mats=0), "n_mats"),
     ("material_index", dict(mat_index=5), "material index"),
     ("outside_box", dict(shift=(0.0, -0.05, 0.0)), "inside the box"),
-    ("sphere_medium", dict(medium="sphere", radius=3.0), "BOX or INFINITE"),
+    ("outside_sphere", dict(medium="sphere", radius=1.2), "inside the sphere"),
     ("degenerate", dict(degenerate=True), "degenerate"),
     ("rho", dict(mats=[(1.5, 0.0, 1.0)]), "rho, ks"),
 ]

@@ -61,7 +61,9 @@ DEBUG_CASES = [(1, "reuse", {}), (2, "reuse", {}), (3, "split", {}), (3, "reuse"
                (5, "split", {}),
                # ablations and uniform-S elliptical sampling
                (2, "reuse", {"strategy": "da_only"}), (4, "reuse", {"strategy": "eda_only"}),
-               (5, "split", {"strategy": "eda_only"}), (3, "split", {"conn_sampling": "uniform"})]
+               (5, "split", {"strategy": "eda_only"}), (3, "split", {"conn_sampling": "uniform"}),
+               # triangle meshes (R32, R33): camera, medium, wall and surface records
+               (6, "reuse", {}), (6, "split", {})]
 
 
 @pytest.mark.parametrize("cfg,mode,extra", DEBUG_CASES,
@@ -83,16 +85,21 @@ def test_sample_debug_parity(dts, oracle, cfg, mode, extra):
     report = {}
     # ---- direction stage
     assert (g["tech"][s] == o["tech"][s]).all()
+    surf = o["tech"] == 4
     for k in ("p_hg", "p_eda", "p_mix", "gamma", "beta_dir", "wconn"):
-        r = _rel(g[k][s], o[k][s], 1e-6)
+        r = _rel(g[k][s & ~surf], o[k][s & ~surf], 1e-6)
         report[k] = float(r.max())
         assert np.quantile(r, 0.9999) < 1e-4 and r.max() < 1e-3, (k, r.max())
+    if surf.any():
+        _check_bsdf_weight(c, recs, g, o, s & surf)
     for k in ("wc", "ww"):
         err = np.abs(g[k][s] - o[k][s]).max()
         report[k] = float(err)
         assert err < 1e-4, (k, err)
     # ---- intersection
     assert (g["hit"][s] == o["hit"][s]).all()
+    wf = s & ((o["hit"] == 2) | (o["hit"] == 4))      # wall / triangle hit: the same face or triangle
+    assert (g["face_hit"][wf] == o["face_hit"][wf]).all()
     fin = s & np.isfinite(o["t_hi"])
     # distances to the medium boundary: relative 1e-4, with an absolute floor of
     # 1e-6 scene units (~10 fp32 ulps of a unit-scale coordinate: a vertex within
@@ -168,6 +175,9 @@ SAME_KEY = [
     ("cfg6_mesh_split", lambda: I.small(I.mesh_config(direction_mode="split"), 16, 16), 16),
     ("cfg6_mesh_vanilla", lambda: I.small(I.mesh_config(strategy="vanilla"), 16, 16), 256),
     ("cfg6_dense_mesh", lambda: I.small(I.mesh_config(ico_subdiv=4), 16, 16), 32),
+    ("sphere_mesh_unwarped", lambda: I.small(I.sphere_mesh_config(), 24, 24, n_bins=64, t1=10.0), 16),
+    ("sphere_mesh_vanilla", lambda: I.small(I.sphere_mesh_config(strategy="vanilla"), 16, 16, n_bins=64, t1=10.0),
+     256),
     ("plate_lambert", lambda: I.plate_config([(0.8, 0.0, 1.0)]), 2000),
     ("plate_plastic_vanilla", lambda: I.plate_config([(0.7, 0.5, 10.0)], strategy="vanilla"), 100000),
 ]
@@ -419,11 +429,49 @@ def test_render_same_key_both_variants(dts, oracle, monkeypatch, name, mk, spp, 
     assert rel <= 0.01
 
 
-def test_mesh_scene_debug_is_rejected(dts):
-    """dts_sample_debug does not take mesh scenes (include/dts.h)."""
-    c = I.as_f32(I.small(I.mesh_config(), 4, 4))
+def _check_bsdf_weight(c, recs, g, o, m):
+    """R32 weight f cos / p_mix: cos = w_o . n is an fp32 dot product of unit
+    vectors (absolute error ~1e-7), and the weight is ~proportional to it where
+    the lobe dominates p_mix, so near the horizon the bound is 1e-4 + 2e-6 / cos."""
+    tris = np.asarray(c["mesh"]["tris"], float).reshape(-1, 3, 3)
+    t = tris[recs["face"][m]]
+    nrm = np.cross(t[:, 1] - t[:, 0], t[:, 2] - t[:, 0])
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    co = np.abs(np.sum(o["ww"][m] * nrm, axis=1))
+    w_in = recs["w"][m]
+    side = np.where(np.sum(w_in * nrm, axis=1, keepdims=True) > 0, -nrm, nrm)
+    mirror = w_in - 2.0 * np.sum(w_in * side, axis=1, keepdims=True) * side
+    ca = np.clip(np.sum(o["ww"][m] * mirror, axis=1), 0.0, 1.0)
+    ne = np.asarray(c["mesh"]["mats"], float)[np.asarray(c["mesh"]["tri_mat"])[recs["face"][m]], 2]
+    r = _rel(g["beta_dir"][m], o["beta_dir"][m], 1e-30)
+    live = o["beta_dir"][m] > 0
+    bound = 1e-4 + 2e-6 / np.maximum(co, 1e-30) + ne * 4e-7 / np.maximum(ca, 1e-30)
+    bad = live & (r > bound)
+    assert not bad.any(), np.c_[r[bad], co[bad], ca[bad], o["beta_dir"][m][bad]][:8]
+    assert (g["beta_dir"][m][~live] == 0).all()
+
+
+def test_mesh_debug_surface_records(dts, oracle):
+    """Surface-vertex debug records (kind 3) of the mesh scene: the BSDF
+    sample, its weight and the NEE match the oracle, and an out-of-range
+    triangle index is returned as terminated."""
+    c = I.as_f32(I.config(6))
     sc = _scene(dts, c)
-    recs = I.debug_records(I.as_f32(I.small(I.config(4), 4, 4)), 8, seed=1)
-    with pytest.raises(dts.DtsError, match="mesh"):
-        dts.debug(sc, recs)
+    recs = I.debug_records(c, 20_000, seed=77, kinds=("surface",))
+    g = dts.debug(sc, recs)
+    o = oracle.debug(c, oracle.build_table(c)[0], recs)
+    assert (o["tech"] == 4).all() and (g["tech"] == 4).all()
+    safe = (o["m_event"] > MARGIN) & (o["m_select"] > MARGIN) & (o["m_valid"] > MARGIN) & (o["m_conn"] > MARGIN)
+    assert safe.mean() > 0.99
+    _check_bsdf_weight(c, recs, g, o, safe)
+    live = safe & (o["beta_dir"] > 0)
+    assert np.abs(g["ww"][live] - o["ww"][live]).max() < 1e-4
+    assert (g["event"][safe] == o["event"][safe]).all()
+    nee = safe & (o["nee"] > 0)
+    assert nee.any()
+    assert _rel(g["nee"][nee], o["nee"][nee], 1e-30).max() < 1e-4
+    bad = {k: v[:4].copy() for k, v in recs.items()}
+    bad["face"][:] = len(c["mesh"]["tris"]) + 3
+    gb = dts.debug(sc, bad)
+    assert (gb["terminate"] == 1).all() and (gb["tech"] == 0).all()
     sc.close()
