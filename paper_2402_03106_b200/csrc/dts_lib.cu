@@ -1314,13 +1314,15 @@ dts_status dts_scene_create(const dts_scene_desc* desc, dts_scene_t* out) {
   if (st != DTS_OK) return st;
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
-  cudaDeviceProp prop;
-  CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
-  if (prop.major < 10) return fail(DTS_E_CUDA, "libdts needs an sm_100 (Blackwell) device");
+  // attribute queries (cudaGetDeviceProperties costs milliseconds per scene)
+  int major = 0, sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (major < 10) return fail(DTS_E_CUDA, "libdts needs an sm_100 (Blackwell) device");
   dts_scene* s = new dts_scene();
   s->desc = *desc;
   derive(*desc, s->S);
-  s->num_sms = prop.multiProcessorCount;
+  s->num_sms = sms;
   s->device = dev;
   if (cudaMalloc(&s->d_work, sizeof(unsigned long long)) != cudaSuccess) {
     delete s;
