@@ -37,6 +37,8 @@ static dts_status fail(dts_status s, const std::string& msg) {
     if (e_ != cudaSuccess) return fail(DTS_E_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
   } while (0)
 
+constexpr int kHostBands = 4;  // dts_render_host row bands for large histograms
+
 struct dts_scene {
   dts_scene_desc desc;
   DevScene S;
@@ -52,6 +54,9 @@ struct dts_scene {
   uint16_t* d_zero_cell = nullptr; // debug kernel table for vanilla scenes
   float* d_qover = nullptr;        // deferred-connection queue overflow slots
   size_t qover_n = 0;
+  cudaStream_t band_stream[2] = {nullptr, nullptr};  // dts_render_host row bands
+  cudaEvent_t band_ev[kHostBands + 1] = {};
+  unsigned long long* d_work_band = nullptr;
   float4* d_bvh = nullptr;         // mesh BVH nodes (R32)
   float4* d_tri4 = nullptr;        // mesh triangles in leaf order
   int32_t* d_tri_map = nullptr;    // caller -> leaf order, then leaf -> caller order (2 n_tris)
@@ -1351,6 +1356,11 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaFree(s->d_resp_w);
   cudaFree(s->d_zero_cell);
   cudaFree(s->d_qover);
+  for (int i = 0; i < 2; ++i)
+    if (s->band_stream[i]) cudaStreamDestroy(s->band_stream[i]);
+  for (int i = 0; i <= kHostBands; ++i)
+    if (s->band_ev[i]) cudaEventDestroy(s->band_ev[i]);
+  cudaFree(s->d_work_band);
   cudaFree(s->d_bvh);
   cudaFree(s->d_tri4);
   cudaFree(s->d_tri_map);
@@ -1456,8 +1466,15 @@ size_t dts_hist_cells(dts_scene_t s) {
   return (size_t)(d.crop[2] - d.crop[0]) * (size_t)(d.crop[3] - d.crop[1]) * (size_t)d.n_bins;
 }
 
-dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* d_hist,
-                      float* d_hist_sq, uint64_t* d_counters, void* stream) {
+}  // extern "C"
+
+// One render launch over crop rows [row0, row1) (relative to the crop) into
+// d_hist (that band's first cell), with its own work counter: dts_render runs
+// the whole crop; dts_render_host runs bands on two streams so each band's
+// device->host copy overlaps the next band's render.
+static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* d_hist,
+                              float* d_hist_sq, uint64_t* d_counters, void* stream, int row0, int row1,
+                              unsigned long long* work) {
   g_last_launches = 0;
   if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
   if (!d_hist) return fail(DTS_E_INVALID_ARG, "d_hist is NULL");
@@ -1466,7 +1483,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   const dts_scene_desc& d = s->desc;
   const bool darts = d.strategy != DTS_STRATEGY_VANILLA;  // DARTS and its ablations
   if (darts && !s->d_table) return fail(DTS_E_STATE, "dts_table_build must run before a DARTS render");
-  const uint64_t npix = (uint64_t)(d.crop[2] - d.crop[0]) * (uint64_t)(d.crop[3] - d.crop[1]);
+  const uint64_t npix = (uint64_t)(d.crop[2] - d.crop[0]) * (uint64_t)(row1 - row0);
   const uint64_t ns = se - sb;
   const uint64_t Npix = (uint64_t)d.width * d.height;
   // path ids must fit 64 bits: (s * Npix + p) * B + b
@@ -1482,12 +1499,14 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     P.resp_w = s->d_resp_w;
   }
   P.S = s->S;
+  P.S.crop[1] = d.crop[1] + row0;
+  P.S.crop[3] = d.crop[1] + row1;
   set_round_keys(P.S, seed);
   P.tab = s->d_table;
   P.hist = d_hist;
   P.hist_sq = d_hist_sq;
   P.counters = reinterpret_cast<unsigned long long*>(d_counters);
-  P.work = s->d_work;
+  P.work = work;
   P.s_begin = sb;
   P.n_s = ns;
   P.spp = spp;
@@ -1504,7 +1523,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   P.spp_mod_b = (uint32_t)(spp % (uint64_t)d.n_bins);
   cudaStream_t st = (cudaStream_t)stream;
   if (DTS_CHECKS) {
-    const uint32_t cells32 = (uint32_t)std::min<size_t>(dts_hist_cells(s), 0xFFFFFFFFu);
+    const uint32_t cells32 = (uint32_t)std::min<size_t>(npix * (size_t)d.n_bins, 0xFFFFFFFFu);
     CUDA_TRY(cudaMemcpyToSymbolAsync(g_check_cells, &cells32, sizeof cells32, 0, cudaMemcpyHostToDevice, st));
   }
   if (darts) {
@@ -1516,7 +1535,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
     P.table_u4 = (uint32_t)(tbytes / 16);
     const bool smem = DTS_TABLE_SMEM && tbytes <= 220 * 1024;
     // privatise small histograms (config 1: 128 cells) in shared memory
-    const size_t cells = dts_hist_cells(s);
+    const size_t cells = (size_t)npix * (size_t)d.n_bins;
     const size_t pbytes = cells * sizeof(float) * (d_hist_sq ? 2 : 1);
     const size_t kSmemCap = 227 * 1024 - 256;  // opt-in per-block maximum less the static shared memory (mbarrier, counters)
     if (cells <= kPrivMaxCells && (smem ? tbytes : 0) + pbytes <= kSmemCap) P.priv_cells = (uint32_t)cells;
@@ -1568,7 +1587,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
       }
       P.qover = s->d_qover;
     }
-    CUDA_TRY(cudaMemsetAsync(s->d_work, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
     void* args[] = {&P};
     CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(blk), args, dyn, st));
     CUDA_TRY(cudaGetLastError());
@@ -1596,6 +1615,15 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
   return DTS_OK;
 }
 
+extern "C" {
+
+dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* d_hist,
+                      float* d_hist_sq, uint64_t* d_counters, void* stream) {
+  if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
+  return render_impl(s, spp, seed, sb, se, d_hist, d_hist_sq, d_counters, stream, 0,
+                     s->desc.crop[3] - s->desc.crop[1], s->d_work);
+}
+
 dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* h_hist,
                            uint64_t* h_counters, void* stream) {
   if (!s || !h_hist) return fail(DTS_E_INVALID_ARG, "NULL argument");
@@ -1612,9 +1640,38 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
     return fail(DTS_E_OOM, "cudaMalloc(counters) failed");
   CUDA_TRY(cudaMemsetAsync(s->d_hist_host, 0, n * sizeof(float), st));
   CUDA_TRY(cudaMemsetAsync(s->d_ctr_host, 0, DTS_NUM_COUNTERS * sizeof(uint64_t), st));
-  dts_status r = dts_render(s, spp, seed, sb, se, s->d_hist_host, nullptr, s->d_ctr_host, stream);
-  if (r != DTS_OK) return r;
-  CUDA_TRY(cudaMemcpyAsync(h_hist, s->d_hist_host, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  const dts_scene_desc& d = s->desc;
+  const int rows = d.crop[3] - d.crop[1];
+  const size_t row_cells = (size_t)(d.crop[2] - d.crop[0]) * (size_t)d.n_bins;
+  // large histograms (config 5: 4.2 GB, ~80 ms over PCIe): kHostBands row bands
+  // on two streams; band k's copy to the host overlaps band k+1's render (and
+  // band k's tail overlaps band k+1's start).  Same paths, same ids.
+  const bool banded = n * sizeof(float) >= ((size_t)256 << 20) && rows >= 2 * kHostBands && sb < se;
+  if (!banded) {
+    dts_status r = dts_render(s, spp, seed, sb, se, s->d_hist_host, nullptr, s->d_ctr_host, stream);
+    if (r != DTS_OK) return r;
+    CUDA_TRY(cudaMemcpyAsync(h_hist, s->d_hist_host, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  } else {
+    if (!s->band_stream[0]) {
+      for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&s->band_stream[i], cudaStreamNonBlocking));
+      for (int i = 0; i <= kHostBands; ++i) CUDA_TRY(cudaEventCreateWithFlags(&s->band_ev[i], cudaEventDisableTiming));
+      if (cudaMalloc(&s->d_work_band, kHostBands * sizeof(unsigned long long)) != cudaSuccess)
+        return fail(DTS_E_OOM, "cudaMalloc(band work counters) failed");
+    }
+    CUDA_TRY(cudaEventRecord(s->band_ev[kHostBands], st));
+    for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamWaitEvent(s->band_stream[i], s->band_ev[kHostBands], 0));
+    for (int k = 0; k < kHostBands; ++k) {
+      const int r0 = rows * k / kHostBands, r1 = rows * (k + 1) / kHostBands;
+      cudaStream_t bs = s->band_stream[k & 1];
+      dts_status r = render_impl(s, spp, seed, sb, se, s->d_hist_host + (size_t)r0 * row_cells, nullptr,
+                                 s->d_ctr_host, bs, r0, r1, s->d_work_band + k);
+      if (r != DTS_OK) return r;
+      CUDA_TRY(cudaEventRecord(s->band_ev[k], bs));
+      CUDA_TRY(cudaStreamWaitEvent(st, s->band_ev[k], 0));
+      CUDA_TRY(cudaMemcpyAsync(h_hist + (size_t)r0 * row_cells, s->d_hist_host + (size_t)r0 * row_cells,
+                               (size_t)(r1 - r0) * row_cells * sizeof(float), cudaMemcpyDeviceToHost, st));
+    }
+  }
   if (h_counters)
     CUDA_TRY(cudaMemcpyAsync(h_counters, s->d_ctr_host, DTS_NUM_COUNTERS * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

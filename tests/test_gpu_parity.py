@@ -340,6 +340,23 @@ def test_render_host_e2e_matches_device(dts):
     assert int(hc[2]) == dts.counters_dict(ctr)["vertices"]
 
 
+def test_render_host_banded_matches_device(dts):
+    """Histograms >= 256 MB take dts_render_host's banded path (row bands on two
+    streams, each band's copy overlapping the next band's render): the same
+    paths and ids as one device render."""
+    c = I.as_f32(I.config(5, crop=(384, 384, 640, 640), spp=4))   # 256 x 256 x 1000 bins = 262 MB
+    sc = _scene(dts, c)
+    d, _, ctr = dts.render_to_tensor(sc, 4, 9)
+    hh = np.zeros(sc.hist_cells(), np.float32)
+    hc = np.zeros(dts.NUM_COUNTERS, np.uint64)
+    sc.render_host(4, 9, 0, 4, hh, hc)
+    dd = d.cpu().numpy().ravel()
+    assert np.linalg.norm(hh - dd) <= 1e-5 * np.linalg.norm(dd)
+    cd = dts.counters_dict(ctr)
+    assert int(hc[0]) == cd["paths"] and int(hc[2]) == cd["vertices"]
+    sc.close()
+
+
 def test_single_pixel_single_bin_and_table_in_global_memory(dts, oracle):
     """Degenerate sizes (1 pixel, 1 bin) and a 32x32 table too large for shared
     memory (the L1/global path of the kernel) still match the oracle."""
