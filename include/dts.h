@@ -247,7 +247,10 @@ dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t s
 
 /* End-to-end variant with HOST buffers: zeroes a library-owned device
  * histogram, renders, and copies the result to h_hist (dts_hist_cells floats,
- * OVERWRITTEN) and the counters to h_counters (nullable).  Synchronous. */
+ * OVERWRITTEN) and the counters to h_counters (nullable).  Synchronous.  For
+ * histograms >= 256 MB it renders 4 row bands of the crop on two library-owned
+ * streams (ordered after `stream`) and copies each band while the next renders;
+ * pinned h_hist lets the copies overlap.  The result is that of dts_render. */
 dts_status dts_render_host(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
                            uint64_t sample_end, float* h_hist, uint64_t* h_counters, void* stream);
 
