@@ -245,6 +245,18 @@ dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t s
                       uint64_t sample_end, float* d_hist, float* d_hist_sq, uint64_t* d_counters,
                       void* stream);
 
+/* dts_render over crop rows [row0, row1) only (0 <= row0 < row1 <= crop
+ * height), into d_hist_band = the band's first cell (row0 * crop width *
+ * n_bins floats further than the crop's).  The same paths and ids as the
+ * corresponding part of dts_render.  band (0..3) picks one of 4 library-owned
+ * work counters: launches that may run concurrently need distinct bands.
+ * Lets a caller pipeline a large histogram band by band (render / reduce /
+ * copy).  Errors as dts_render; DTS_E_INVALID_ARG for a bad row range or band.
+ * Asynchronous. */
+dts_status dts_render_rows(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
+                           uint64_t sample_end, int32_t row0, int32_t row1, int32_t band, float* d_hist_band,
+                           uint64_t* d_counters, void* stream);
+
 /* End-to-end variant with HOST buffers: zeroes a library-owned device
  * histogram, renders, and copies the result to h_hist (dts_hist_cells floats,
  * OVERWRITTEN) and the counters to h_counters (nullable).  Synchronous.  For

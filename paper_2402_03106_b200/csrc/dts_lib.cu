@@ -1624,6 +1624,26 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
                      s->desc.crop[3] - s->desc.crop[1], s->d_work);
 }
 
+static dts_status ensure_bands(dts_scene_t s) {
+  if (s->band_stream[0]) return DTS_OK;
+  for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&s->band_stream[i], cudaStreamNonBlocking));
+  for (int i = 0; i <= kHostBands; ++i) CUDA_TRY(cudaEventCreateWithFlags(&s->band_ev[i], cudaEventDisableTiming));
+  if (cudaMalloc(&s->d_work_band, kHostBands * sizeof(unsigned long long)) != cudaSuccess)
+    return fail(DTS_E_OOM, "cudaMalloc(band work counters) failed");
+  return DTS_OK;
+}
+
+dts_status dts_render_rows(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, int32_t row0,
+                           int32_t row1, int32_t band, float* d_hist_band, uint64_t* d_counters, void* stream) {
+  if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
+  const int rows = s->desc.crop[3] - s->desc.crop[1];
+  if (row0 < 0 || row1 > rows || row0 >= row1) return fail(DTS_E_INVALID_ARG, "need 0 <= row0 < row1 <= crop height");
+  if (band < 0 || band >= kHostBands) return fail(DTS_E_INVALID_ARG, "band must be 0..3");
+  dts_status r = ensure_bands(s);
+  if (r != DTS_OK) return r;
+  return render_impl(s, spp, seed, sb, se, d_hist_band, nullptr, d_counters, stream, row0, row1, s->d_work_band + band);
+}
+
 dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* h_hist,
                            uint64_t* h_counters, void* stream) {
   if (!s || !h_hist) return fail(DTS_E_INVALID_ARG, "NULL argument");
@@ -1652,12 +1672,8 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
     if (r != DTS_OK) return r;
     CUDA_TRY(cudaMemcpyAsync(h_hist, s->d_hist_host, n * sizeof(float), cudaMemcpyDeviceToHost, st));
   } else {
-    if (!s->band_stream[0]) {
-      for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&s->band_stream[i], cudaStreamNonBlocking));
-      for (int i = 0; i <= kHostBands; ++i) CUDA_TRY(cudaEventCreateWithFlags(&s->band_ev[i], cudaEventDisableTiming));
-      if (cudaMalloc(&s->d_work_band, kHostBands * sizeof(unsigned long long)) != cudaSuccess)
-        return fail(DTS_E_OOM, "cudaMalloc(band work counters) failed");
-    }
+    const dts_status eb = ensure_bands(s);
+    if (eb != DTS_OK) return eb;
     CUDA_TRY(cudaEventRecord(s->band_ev[kHostBands], st));
     for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamWaitEvent(s->band_stream[i], s->band_ev[kHostBands], 0));
     for (int k = 0; k < kHostBands; ++k) {

@@ -88,6 +88,8 @@ _lib.dts_hist_cells.argtypes = [_VP]
 _lib.dts_hist_cells.restype = ctypes.c_size_t
 _lib.dts_render.argtypes = [_VP, _U64, _U64, _U64, _U64, _VP, _VP, _VP, _VP]
 _lib.dts_render_host.argtypes = [_VP, _U64, _U64, _U64, _U64, _VP, _VP, _VP]
+_lib.dts_render_rows.argtypes = [_VP, _U64, _U64, _U64, _U64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _VP,
+                                 _VP, _VP]
 _lib.dts_sample_debug.argtypes = [_VP, ctypes.c_int32, _VP, _VP, _VP]
 _lib.dts_last_launch.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 4
 _lib.dts_set_response.argtypes = [_VP, _VP, ctypes.c_int32]
@@ -99,7 +101,7 @@ _lib.dts_abi_version.restype = ctypes.c_int32
 
 EXPORTED = ("dts_scene_create", "dts_scene_destroy", "dts_set_response", "dts_table_build", "dts_table_export",
             "dts_table_size", "dts_check_failures",
-            "dts_hist_cells", "dts_render", "dts_render_host", "dts_sample_debug", "dts_last_launch",
+            "dts_hist_cells", "dts_render", "dts_render_rows", "dts_render_host", "dts_sample_debug", "dts_last_launch",
             "dts_status_string", "dts_last_error", "dts_abi_version")
 
 
@@ -256,6 +258,12 @@ class Scene:
                stream=None):
         _check(_lib.dts_render(self.handle, spp, seed, sample_begin, sample_end, _ptr(hist), _ptr(hist_sq),
                                _ptr(counters), _stream(stream)), "dts_render")
+
+    def render_rows(self, spp: int, seed: int, sample_begin: int, sample_end: int, row0: int, row1: int, band: int,
+                    hist_band, counters=None, stream=None):
+        """dts_render over crop rows [row0, row1) into hist_band (that band's cells)."""
+        _check(_lib.dts_render_rows(self.handle, spp, seed, sample_begin, sample_end, row0, row1, band,
+                                    _ptr(hist_band), _ptr(counters), _stream(stream)), "dts_render_rows")
 
     def render_host(self, spp: int, seed: int, sample_begin: int, sample_end: int, h_hist: np.ndarray,
                     h_counters: np.ndarray | None = None, stream=None):

@@ -357,6 +357,30 @@ def test_render_host_banded_matches_device(dts):
     sc.close()
 
 
+def test_render_rows_bands_equal_full_render(dts):
+    """dts_render_rows over row bands (two bands on two streams at a time, as
+    a pipelining caller would) reproduces dts_render; bad ranges are errors."""
+    c = I.as_f32(I.small(I.config(3), 24, 20, n_bins=64, t1=9.0))
+    sc = _scene(dts, c)
+    full, _, cf = dts.render_to_tensor(sc, 8, 4)
+    h = torch.zeros(sc.hist_shape(), device="cuda")
+    ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    rowsz = c["width"] * c["n_bins"]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for st in streams:
+        st.wait_stream(torch.cuda.current_stream())
+    for k, (r0, r1) in enumerate([(0, 7), (7, 13), (13, 20)]):
+        sc.render_rows(8, 4, 0, 8, r0, r1, k, h.view(-1)[r0 * rowsz:r1 * rowsz], ctr, streams[k % 2].cuda_stream)
+    torch.cuda.synchronize()
+    f, g = full.cpu().numpy(), h.cpu().numpy()
+    assert np.linalg.norm(f - g) <= 1e-5 * np.linalg.norm(f)
+    assert dts.counters_dict(ctr) == dts.counters_dict(cf)
+    for r0, r1, band in [(5, 5, 0), (-1, 3, 0), (0, 21, 0), (0, 4, 4)]:
+        with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+            sc.render_rows(8, 4, 0, 8, r0, r1, band, h, ctr)
+    sc.close()
+
+
 def test_single_pixel_single_bin_and_table_in_global_memory(dts, oracle):
     """Degenerate sizes (1 pixel, 1 bin) and a 32x32 table too large for shared
     memory (the L1/global path of the kernel) still match the oracle."""
