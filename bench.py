@@ -295,7 +295,15 @@ def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts):
     hctr = np.zeros(dts.NUM_COUNTERS, np.uint64)
     spp = c["spp"]
     sb, se = _shard(spp, rank, world)
-    dev_hist = torch.zeros(sc.hist_shape(), dtype=torch.float32, device="cuda") if world > 1 else None
+    # N > 1 (and DTS_E2E_BANDED=1 at N = 1, for testing): large histograms go band
+    # by band -- render rows (dts_render_rows), reduce the band, and copy it to the
+    # host on a copy stream while the next band renders
+    banded_mode = world > 1 or os.environ.get("DTS_E2E_BANDED") == "1"
+    dev_hist = torch.zeros(sc.hist_shape(), dtype=torch.float32, device="cuda") if banded_mode else None
+    rows = c["crop"][3] - c["crop"][1]
+    rowsz = (c["crop"][2] - c["crop"][0]) * c["n_bins"]
+    nbands = 4 if (cells * 4 >= (256 << 20) and rows >= 8) else 1
+    copy_stream = torch.cuda.Stream() if banded_mode else None
     verts = 0
     ksteps = max(1, min(args.steps, 2))
     for i in range(ksteps + 1):
@@ -307,18 +315,29 @@ def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts):
             t0 = time.perf_counter()
         s2 = dts.Scene(c)
         s2.table_build(stream=stream)
-        if world == 1:
+        if not banded_mode:
             s2.render_host(spp, c["seed"] + 7 * i, sb, se, hnp, hctr, stream)
             if timed:
                 verts += int(hctr[2])
         else:
             dev_hist.zero_()
             ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
-            s2.render(spp, c["seed"] + 7 * i, sb, se, dev_hist, None, ctr, stream)
-            dist.reduce(dev_hist, dst=0)
-            dist.all_reduce(ctr)
-            if rank == 0:
-                host.copy_(dev_hist.view(-1), non_blocking=True)
+            flat = dev_hist.view(-1)
+            for k in range(nbands):
+                r0, r1 = rows * k // nbands, rows * (k + 1) // nbands
+                band = flat[r0 * rowsz:r1 * rowsz]
+                # every collective stays on the main stream, in the same order on every rank
+                s2.render_rows(spp, c["seed"] + 7 * i, sb, se, r0, r1, k % 4, band, ctr, stream)
+                if world > 1:
+                    dist.reduce(band, dst=0)
+                if rank == 0:
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    copy_stream.wait_event(ev)
+                    with torch.cuda.stream(copy_stream):
+                        host[r0 * rowsz:r1 * rowsz].copy_(band, non_blocking=True)
+            if world > 1:
+                dist.all_reduce(ctr)
             torch.cuda.synchronize()
             if timed:
                 verts += int(ctr[2].item())
