@@ -4,7 +4,7 @@
  * DARTS: "Diffusion Approximated Residual Time Sampling for Time-of-flight
  * Rendering in Homogeneous Scattering Media", arXiv 2402.03106.  Passages are
  * cited as PAPER.md:<line> (the paper text; equations E1..E22 numbered in order
- * of appearance) and readings R1..R29 of DESIGN.md section 3.
+ * of appearance) and readings R1..R33 of DESIGN.md section 3.
  *
  * One estimator is exposed: per-bin dedicated transient path tracing in a
  * homogeneous medium.  Every path vertex
@@ -17,7 +17,13 @@
  *   4. splats into a pixel x time-bin histogram (camera-warped or unwarped,
  *      PAPER.md:50, 76).
  * A vanilla estimator (exponential flight, phase sampling, direct shadow
- * connection) runs through the same kernels.
+ * connection) runs through the same kernels, as do the
+ * ablations of PAPER.md:426-435, a tabulated sensor response
+ * and opaque triangle meshes with glossy / plastic BSDFs (
+ * Table 1).
+ *
+ *  - "one scene may be used by one stream at a time" below: dts_render_rows
+ *    calls on distinct bands may run concurrently.
  *
  * Conventions (all calls):
  *  - lengths are times: c = eta = 1 (E3).
