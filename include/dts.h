@@ -22,9 +22,6 @@
  * and opaque triangle meshes with glossy / plastic BSDFs (
  * Table 1).
  *
- *  - "one scene may be used by one stream at a time" below: dts_render_rows
- *    calls on distinct bands may run concurrently.
- *
  * Conventions (all calls):
  *  - lengths are times: c = eta = 1 (E3).
  *  - "device" pointers are CUDA global-memory pointers of the current device
@@ -37,7 +34,8 @@
  *    passes in.  Errors never abort: a status is returned and a thread-local
  *    message is available from dts_last_error().  No call falls back to a CPU
  *    path: a missing/unsupported device returns DTS_E_CUDA.
- *  - one scene may be used by one stream at a time.
+ *  - one scene may be used by one stream at a time (dts_render_rows calls on
+ *    distinct bands excepted: they may run concurrently).
  */
 #ifndef DTS_H
 #define DTS_H
