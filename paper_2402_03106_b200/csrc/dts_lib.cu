@@ -231,8 +231,12 @@ constexpr int kBlock = DTS_BLOCK;  // deferred-connection kernels: the queues ta
 #endif
 // immediate-connection kernels: 28 warps at <= 72 registers (A/B in profiles/README.md)
 constexpr int kBlockImm = DTS_BLOCK_IMM;
-// mesh kernels (BVH traversal: a call, its stack and more live values) run 640 threads at <= 96 registers
-constexpr int kBlockMesh = 640;
+// mesh kernels (BVH traversal state: more live values) run 768 threads at <= 80 registers
+// (A/B: +2 % / +3.5 % on config 6 with 336 / 81936 triangles against 640)
+#ifndef DTS_BLOCK_MESH
+#define DTS_BLOCK_MESH 768
+#endif
+constexpr int kBlockMesh = DTS_BLOCK_MESH;
 __host__ __device__ constexpr int render_block(bool defer, bool mesh = false) {
   return mesh ? kBlockMesh : (defer ? kBlock : kBlockImm);
 }
