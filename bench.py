@@ -215,7 +215,7 @@ def run_gpu(args):
     paths_per_step = counts["paths"] / args.steps
 
     # ---- end to end through the C ABI with HOST buffers (pinned), N GPUs
-    e2e = run_e2e(args, c, sc, world, rank, stream, torch, dist, dts)
+    e2e = run_e2e(args, c, sc, world, rank, stream, torch, dist, dts, ms / args.steps)
 
     if rank == 0:
         peaks = _peaks()
@@ -285,7 +285,7 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts):
+def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts, step_ms=1e9):
     """Same metric through the public API with host buffers: per step the host
     scene description goes in (dts_scene_create + dts_table_build), the
     histogram comes back to pinned host memory."""
@@ -305,7 +305,15 @@ def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts):
     nbands = 4 if (cells * 4 >= (256 << 20) and rows >= 8) else 1
     copy_stream = torch.cuda.Stream() if banded_mode else None
     verts = 0
+    # at least 2 steps and ~0.5 s of work: millisecond configs are otherwise
+    # dominated by the noise of a couple of host-side calls
     ksteps = max(1, min(args.steps, 2))
+    if step_ms < 100.0:
+        ksteps = max(ksteps, min(50, int(500.0 / max(step_ms, 1.0))))
+    if world > 1:  # every rank must run the same number of collectives
+        kt = torch.tensor([ksteps], dtype=torch.int64, device="cuda")
+        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+        ksteps = int(kt[0])
     for i in range(ksteps + 1):
         timed = i > 0
         if timed and i == 1:
