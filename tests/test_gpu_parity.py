@@ -253,6 +253,8 @@ INDEP = [
     ("cfg3_split", lambda: I.small(I.config(3, parity_s_excess=0.05), 4, 4, n_bins=16, t1=6.0), 2000, 2000),
     ("cfg5_split", lambda: I.small(I.config(5, parity_s_excess=0.05, spp_mode="cell"), 2, 2, n_bins=8, t1=16.0),
      600, 600),
+    ("cfg6_mesh", lambda: I.small(I.mesh_config(parity_r_excl=0.3, parity_s_excess=0.05), 4, 4), 20000, 20000),
+    ("plate_glossy", lambda: I.plate_config([(0.7, 0.5, 10.0)]), 20000, 20000),
 ]
 
 
