@@ -218,6 +218,7 @@ struct RenderParams {
   uint32_t flush1_at;             // stage-1 queue length that triggers a batch (SPLIT)
   float* qover;                   // DEFER: global overflow queue slots, kQueue x (kJobWords + kJob1Words) per warp
   uint32_t refill_k;              // idle lane-iterations that trigger a refill
+  uint32_t one_cell_warps;        // 1: per-cell order with >= 32 samples per cell (splat fast path)
   uint32_t div32;                 // 1: work indices, sample indices + B fit 32 bits (fast divisions)
   FastDiv fd_ns, fd_npix, fd_cw, fd_b;  // division by n_s, npix, cw, n_bins (fastdiv.h)
 };
@@ -424,8 +425,32 @@ __constant__ uint32_t g_check_cells;  // histogram cells of the current launch (
 // (__match_any_sync + shuffles, one RED per distinct cell and warp); the RED
 // goes to a shared-memory copy of the histogram when the CTA privatises it
 // (small histograms, flushed once at kernel end), else to HBM/L2.
+// Called by all 32 lanes of a converged warp.
 __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, float v, float v2, float* g_hist,
-                                      float* g_sq, float* s_hist, float* s_sq, int lane) {
+                                      float* g_sq, float* s_hist, float* s_sq, int lane, bool try_one_cell = false) {
+  // try_one_cell (launch-uniform: per-cell issue order with >= 32 samples per
+  // cell, so a warp's paths are mostly consecutive samples of one cell): when
+  // every retiring lane is on one cell, a 5-step butterfly and one RED
+  const int first = __ffs(dmask) - 1;
+  const uint32_t c0 = try_one_cell ? __shfl_sync(0xffffffffu, cell, first) : 0u;
+  if (try_one_cell && __all_sync(0xffffffffu, !done || cell == c0)) {
+    const bool sq = (s_hist ? s_sq : g_sq) != nullptr;
+    float a = done ? v : 0.0f, a2 = done ? v2 : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (sq) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (lane != first || a == 0.0f) return;
+    DTS_CHECK(c0 < g_check_cells);
+    if (s_hist) {
+      atomicAdd(s_hist + c0, a);
+      if (s_sq) atomicAdd(s_sq + c0, a2);
+    } else {
+      atomicAdd(g_hist + c0, a);
+      if (g_sq) atomicAdd(g_sq + c0, a2);
+    }
+    return;
+  }
   if (!done) return;
   const unsigned peers = __match_any_sync(dmask, cell);
   const int leader = __ffs(peers) - 1;
@@ -719,7 +744,8 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     const unsigned dmask = __ballot_sync(FULL, done);
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
-      splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane);
+      splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane,
+            P.one_cell_warps != 0u);
       if (done) active = false;
     }
   }
@@ -1523,6 +1549,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
   P.fd_npix = fastdiv_make((uint32_t)npix);
   P.fd_cw = fastdiv_make(P.cw);
   P.fd_b = fastdiv_make((uint32_t)d.n_bins);
+  P.one_cell_warps = (d.spp_mode == DTS_SPP_PER_CELL && ns >= 32u) ? 1u : 0u;
   P.spp_div_b = (uint32_t)(spp / (uint64_t)d.n_bins);
   P.spp_mod_b = (uint32_t)(spp % (uint64_t)d.n_bins);
   cudaStream_t st = (cudaStream_t)stream;
