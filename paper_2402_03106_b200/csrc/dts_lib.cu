@@ -425,32 +425,34 @@ __constant__ uint32_t g_check_cells;  // histogram cells of the current launch (
 // (__match_any_sync + shuffles, one RED per distinct cell and warp); the RED
 // goes to a shared-memory copy of the histogram when the CTA privatises it
 // (small histograms, flushed once at kernel end), else to HBM/L2.
-// Called by all 32 lanes of a converged warp.
-__device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, float v, float v2, float* g_hist,
-                                      float* g_sq, float* s_hist, float* s_sq, int lane, bool try_one_cell = false) {
-  // try_one_cell (launch-uniform: per-cell issue order with >= 32 samples per
-  // cell, so a warp's paths are mostly consecutive samples of one cell): when
-  // every retiring lane is on one cell, a 5-step butterfly and one RED
+// Every retiring lane of the warp on one cell (per-cell issue order with >= 32
+// samples per cell: a warp's paths are mostly consecutive samples of one cell):
+// a 5-step butterfly and one RED.  Called by all 32 lanes of a converged warp;
+// returns false (nothing done) when the lanes are on several cells.
+__device__ __forceinline__ bool splat_one_cell(unsigned dmask, bool done, uint32_t cell, float v, float v2,
+                                               float* g_hist, float* g_sq, float* s_hist, float* s_sq, int lane) {
   const int first = __ffs(dmask) - 1;
-  const uint32_t c0 = try_one_cell ? __shfl_sync(0xffffffffu, cell, first) : 0u;
-  if (try_one_cell && __all_sync(0xffffffffu, !done || cell == c0)) {
-    const bool sq = (s_hist ? s_sq : g_sq) != nullptr;
-    float a = done ? v : 0.0f, a2 = done ? v2 : 0.0f;
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      if (sq) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-    }
-    if (lane != first || a == 0.0f) return;
-    DTS_CHECK(c0 < g_check_cells);
-    if (s_hist) {
-      atomicAdd(s_hist + c0, a);
-      if (s_sq) atomicAdd(s_sq + c0, a2);
-    } else {
-      atomicAdd(g_hist + c0, a);
-      if (g_sq) atomicAdd(g_sq + c0, a2);
-    }
-    return;
+  const uint32_t c0 = __shfl_sync(0xffffffffu, cell, first);
+  if (!__all_sync(0xffffffffu, !done || cell == c0)) return false;
+  const bool sq = (s_hist ? s_sq : g_sq) != nullptr;
+  float a = done ? v : 0.0f, a2 = done ? v2 : 0.0f;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (sq) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
   }
+  if (lane != first || a == 0.0f) return true;
+  DTS_CHECK(c0 < g_check_cells);
+  if (s_hist) {
+    atomicAdd(s_hist + c0, a);
+    if (s_sq) atomicAdd(s_sq + c0, a2);
+  } else {
+    atomicAdd(g_hist + c0, a);
+    if (g_sq) atomicAdd(g_sq + c0, a2);
+  }
+  return true;
+}
+__device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, float v, float v2, float* g_hist,
+                                      float* g_sq, float* s_hist, float* s_sq, int lane) {
   if (!done) return;
   const unsigned peers = __match_any_sync(dmask, cell);
   const int leader = __ffs(peers) - 1;
@@ -744,8 +746,9 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     const unsigned dmask = __ballot_sync(FULL, done);
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
-      splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane,
-            P.one_cell_warps != 0u);
+      if (!(P.one_cell_warps &&
+            splat_one_cell(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane)))
+        splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane);
       if (done) active = false;
     }
   }
