@@ -176,7 +176,7 @@ def run_gpu(args):
 
         if args.reduce == "p2p":
             # fused: every rank's kernel adds straight into rank 0's histogram (peer memory)
-            render_sharded_p2p(render_range, spp, hist)
+            render_sharded_p2p(render_range, spp, hist, enable_peer=dts.enable_peer)
         else:
             # render the shard, then ONE reduce of the histograms to rank 0 (NCCL over NVLink)
             hist.zero_()

@@ -202,7 +202,9 @@ enum {
 };
 
 /* Creates a scene (validates, derives constants, allocates the table storage
- * on the current device).  Synchronous.  *out is NULL on failure. */
+ * on the current device).  Synchronous.  *out is NULL on failure.  Histogram
+ * cell indices are 32-bit: crop_w * crop_h * n_bins >= 2^32 (e.g. a 2048 x 2048
+ * crop with 1024 bins) is rejected with DTS_E_RANGE. */
 dts_status dts_scene_create(const dts_scene_desc* desc, dts_scene_t* out);
 /* Frees the scene; waits for its pending work.  NULL is a no-op. */
 dts_status dts_scene_destroy(dts_scene_t scene);
@@ -244,7 +246,9 @@ size_t dts_hist_cells(dts_scene_t scene);
  * fast or faster on every config); DTS_FLUSH_AT (1..32, default 28) is the queue length
  * that triggers a batch; DTS_REFILL_K (default 8) is the idle
  * lane-iterations that trigger a lane refill.  None changes any result
- * beyond fp32 summation order. */
+ * beyond fp32 summation order.  DTS_DEFER applies to dts_render only: row-band
+ * launches (dts_render_rows, dts_render_host's bands), which may run
+ * concurrently on one scene, always take the immediate kernels. */
 dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
                       uint64_t sample_end, float* d_hist, float* d_hist_sq, uint64_t* d_counters,
                       void* stream);
@@ -282,6 +286,14 @@ dts_status dts_sample_debug(dts_scene_t scene, int32_t n, const dts_debug_in* d_
  * library was built with -DDTS_CHECKS=1 (scripts/build_variants.sh).
  * Synchronizes the device. */
 dts_status dts_check_failures(uint64_t* out);
+
+/* Enables peer access from the current device to device `peer` (a no-op when
+ * it is the current device or already enabled), so that a render kernel on
+ * this device can accumulate into a histogram that lives on `peer` and was
+ * mapped here through CUDA IPC (the fused render + reduce of shard.py).
+ * DTS_E_INVALID_ARG for a device index out of range, DTS_E_CUDA when the pair
+ * has no peer path.  Synchronous. */
+dts_status dts_enable_peer(int32_t peer);
 
 /* Kernel launches issued by the last dts_render on this thread (for the
  * bench's gpu_launches count) and the launch geometry. */

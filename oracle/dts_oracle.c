@@ -1000,8 +1000,9 @@ static int start_path(const or_scene* sc, uint64_t seed, uint64_t id, int px, in
   draw4(seed, id, 0xFFFFFFFFu, 0, a);
   draw4(seed, id, 0xFFFFFFFFu, 1, b);
   draw4(seed, id, 0xFFFFFFFFu, 2, c);
-  int e = (int)floor(sc->n_emitters * or_uniform(a[2]));
-  if (e >= sc->n_emitters) e = sc->n_emitters - 1;
+  /* R20: e = floor(N_e u) with u = m 2^-23, m the 23 high bits of a[2]: the
+   * exact integer floor(N_e m / 2^23) (index work, bit-exact on both sides) */
+  int e = or_uniform_index(sc->n_emitters, a[2]);
   *emitter = e;
   if (sc->camera_kind == OR_CAMERA_PINHOLE) {
     double fwd[3], right[3], upc[3];
@@ -1041,15 +1042,25 @@ static int start_path(const or_scene* sc, uint64_t seed, uint64_t id, int px, in
   return 0;
 }
 
-/* R21 per-pixel bin offset o_p for SPP_PER_PIXEL */
-static int pixel_offset(const or_scene* sc, uint64_t seed, uint64_t p) {
+/* floor(n u) for u = (r >> 9) 2^-23 (R24), as the exact integer
+ * (n (r >> 9)) >> 23: an index drawn from a uniform is index work and is taken
+ * in integer arithmetic (no rounding), so that every implementation of R20 and
+ * R21 picks the same index. */
+int or_uniform_index(int n, uint32_t r) { return (int)(((uint64_t)(uint32_t)n * (uint64_t)(r >> 9)) >> 23); }
+
+/* R21 per-pixel bin offset o_p for SPP_PER_PIXEL ("per-frame dedicated paths",
+ * PAPER.md:373): o_p = floor(B u), u the first word of the pixel's Philox draw
+ * at bounce 0xFFFFFFFE.  Sample s of pixel p goes to bin b = (s + o_p) mod B. */
+int or_pixel_offset(const or_scene* sc, uint64_t seed, uint64_t p) {
   uint32_t a[4];
   draw4(seed, p, 0xFFFFFFFEu, 0, a);
-  int o = (int)floor(sc->n_bins * or_uniform(a[0]));
-  return o >= sc->n_bins ? sc->n_bins - 1 : o;
+  return or_uniform_index(sc->n_bins, a[0]);
 }
 
-static uint64_t cell_count(const or_scene* sc, uint64_t spp, int o_p, int b) {
+/* n_pb: the number of samples s in [0, spp) of pixel p that land in bin b,
+ * i.e. of s with s = (b - o_p) mod B (mod B): the cell's estimate is the mean
+ * over these samples.  PER_CELL: spp. */
+uint64_t or_cell_count(const or_scene* sc, uint64_t spp, int o_p, int b) {
   if (sc->spp_mode == OR_SPP_PER_CELL) return spp;
   uint64_t B = (uint64_t)sc->n_bins;
   uint64_t rel = (uint64_t)(((long)b - o_p) % (long)B + (long)B) % B;
@@ -1299,6 +1310,10 @@ typedef struct {
   int tid, nthreads;
 } render_job;
 
+static int in_window(const or_scene* sc, int b) {
+  return !(sc->bin_window[1] > sc->bin_window[0]) || (b >= sc->bin_window[0] && b < sc->bin_window[1]);
+}
+
 static void* render_worker(void* arg) {
   render_job* jb = (render_job*)arg;
   const or_scene* sc = jb->sc;
@@ -1327,6 +1342,7 @@ static void* render_worker(void* arg) {
       uint64_t rest = i / ns;
       uint64_t pl = rest % npix_local;
       int b = (int)(rest / npix_local);
+      if (!in_window(sc, b)) continue;
       int px = sc->crop[0] + (int)(pl % cw), py = sc->crop[1] + (int)(pl / cw);
       uint64_t p = (uint64_t)py * sc->width + px;
       uint64_t id = (s * Npix + p) * B + (uint64_t)b;
@@ -1359,9 +1375,10 @@ static void* render_worker(void* arg) {
         b = response_bin(sc, cdf, a[3] >> 9, &scale);
         inv_n = 1.0 / (double)jb->spp; /* every path of the pixel is a sample of every cell (X = 0 off its bin) */
       } else {
-        op = pixel_offset(sc, jb->seed, p);
+        op = or_pixel_offset(sc, jb->seed, p);
         b = (int)((s + (uint64_t)op) % B);
-        inv_n = 1.0 / (double)cell_count(sc, jb->spp, op, b);
+        if (!in_window(sc, b)) continue;
+        inv_n = 1.0 / (double)or_cell_count(sc, jb->spp, op, b);
       }
       if (oacc) memset(oacc, 0, sizeof(double) * jb->n_orders);
       double acc = scale * darts_path(sc, &dv, jb->q, jb->seed, id, px, py, b, oacc, jb->n_orders, &jb->st, NULL);
@@ -1448,7 +1465,7 @@ int or_render_ids(const or_scene* sc, const uint16_t* q, uint64_t spp, uint64_t 
     } else {
       p = id % Npix;
       uint64_t s = id / Npix;
-      b = (int)((s + (uint64_t)pixel_offset(sc, seed, p)) % B);
+      b = (int)((s + (uint64_t)or_pixel_offset(sc, seed, p)) % B);
     }
     int px = (int)(p % (uint64_t)sc->width), py = (int)(p / (uint64_t)sc->width);
     acc[i] = darts_path(sc, &dv, q, seed, id, px, py, b, NULL, 0, NULL, nvert ? &nvert[i] : NULL);

@@ -70,6 +70,11 @@ typedef struct {
   const int32_t* tri_mat;
   int32_t n_mats;
   double mats[OR_MAX_MATERIALS][3];
+  /* Test-only work restriction: with bin_window[1] > bin_window[0], paths whose
+   * bin lies outside [bin_window[0], bin_window[1]) are not traced (their cells
+   * stay 0; every other cell, its sample count n_pb and its estimate are those
+   * of the full render).  {0, 0}: every bin. */
+  int32_t bin_window[2];
 } or_scene;
 
 /* 16-bit quantised per-cell CDF of the EDA direction table (R8-R10):
@@ -134,6 +139,14 @@ double or_bsdf_sample(const or_scene* sc, int tri, const double w[3], double u4,
  * quantised CDF.  mass may be NULL.  Returns 0 on success. */
 int or_table_build(const or_scene* sc, double* mass, uint16_t* q, int nthreads);
 double or_table_integrand(const or_scene* sc, double C, double S, double cos_theta);
+
+/* floor(n u) for the uniform u = (r >> 9) 2^-23 of R24, exactly: (n (r >> 9)) >> 23.
+ * R20's emitter index (n = N_e) and R21's pixel offset (n = n_bins). */
+int or_uniform_index(int n, uint32_t r);
+/* R21: the per-pixel bin offset o_p of pixel p (row-major image index) */
+int or_pixel_offset(const or_scene* sc, uint64_t seed, uint64_t p);
+/* R21: n_pb, the number of samples s in [0, spp) with (s + o_p) mod B = b (PER_CELL: spp) */
+uint64_t or_cell_count(const or_scene* sc, uint64_t spp, int o_p, int b);
 
 void or_debug(const or_scene* sc, const uint16_t* q, int n, const or_debug_in* in,
               or_debug_out* out);

@@ -74,6 +74,7 @@ class OrScene(ctypes.Structure):
         ("response", ctypes.c_void_p),
         ("n_tris", ctypes.c_int32), ("tris", ctypes.c_void_p), ("tri_mat", ctypes.c_void_p),
         ("n_mats", ctypes.c_int32), ("mats", D3 * 8),
+        ("bin_window", ctypes.c_int32 * 2),
     ]
 
 
@@ -158,6 +159,8 @@ def scene(c: dict) -> OrScene:
         assert w.shape == (c["n_bins"],)
         s._response_keepalive = w
         s.response = w.ctypes.data
+    if c.get("bin_window") is not None:
+        s.bin_window[:] = c["bin_window"]
     m = c.get("mesh")
     if m is not None and len(m["tris"]):
         tris = np.ascontiguousarray(np.asarray(m["tris"], dtype=np.float64).reshape(-1, 9))
@@ -302,6 +305,25 @@ def render(c: dict, q: np.ndarray | None, spp: int, seed: int, s_begin: int = 0,
         raise RuntimeError(f"or_render failed: {rc}")
     return dict(hist=hist.reshape(shape), hist_sq=None if hsq is None else hsq.reshape(shape),
                 order_hist=None if oh is None else oh.reshape((n_orders,) + shape), stats=st.as_dict())
+
+
+def uniform_index(n: int, r: int) -> int:
+    lib().or_uniform_index.restype = ctypes.c_int
+    return lib().or_uniform_index(ctypes.c_int(n), ctypes.c_uint32(r))
+
+
+def pixel_offset(c: dict, seed: int, p: int) -> int:
+    """R21: the bin offset o_p of image pixel p (row-major)."""
+    s = scene(c)
+    lib().or_pixel_offset.restype = ctypes.c_int
+    return lib().or_pixel_offset(ctypes.byref(s), ctypes.c_uint64(seed), ctypes.c_uint64(p))
+
+
+def cell_count(c: dict, spp: int, o_p: int, b: int) -> int:
+    """R21: n_pb, the samples of a pixel with offset o_p that land in bin b."""
+    s = scene(c)
+    lib().or_cell_count.restype = ctypes.c_uint64
+    return int(lib().or_cell_count(ctypes.byref(s), ctypes.c_uint64(spp), ctypes.c_int(o_p), ctypes.c_int(b)))
 
 
 def render_ids(c: dict, q: np.ndarray, spp: int, seed: int, ids: np.ndarray):

@@ -143,6 +143,12 @@ __device__ __forceinline__ u4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, u
 // R24: u = (r >> 9) 2^-23, built as a float in [1, 2) minus one (no int->float conversion)
 __device__ __forceinline__ float mant01(uint32_t m23) { return __uint_as_float(0x3f800000u | m23) - 1.0f; }
 __device__ __forceinline__ float unif(uint32_t r) { return mant01(r >> 9); }
+// floor(n u) for u = unif(r), exactly: (n (r >> 9)) >> 23 (R20 emitter index,
+// R21 bin offset).  Index work is integer work: an fp32 n * u rounds up across
+// a slice boundary for ~2e-5 of the draws when n is not a power of two.
+__device__ __forceinline__ uint32_t unif_index(uint32_t n, uint32_t r) {
+  return (uint32_t)(((uint64_t)n * (uint64_t)(r >> 9)) >> 23);
+}
 
 // Small integer <-> float conversions on the FMA/ALU pipes instead of the XU
 // pipe (I2F/F2I share it with MUFU, ~60 % busy in the DARTS vertex):

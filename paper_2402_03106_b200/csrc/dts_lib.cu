@@ -220,6 +220,7 @@ struct RenderParams {
   uint32_t refill_k;              // idle lane-iterations that trigger a refill
   uint32_t one_cell_warps;        // 1: per-cell order with >= 32 samples per cell (splat fast path)
   uint32_t div32;                 // 1: work indices, sample indices + B fit 32 bits (fast divisions)
+  uint32_t cells;                 // histogram cells of this launch (< 2^32; bounds checks of the check build)
   FastDiv fd_ns, fd_npix, fd_cw, fd_b;  // division by n_s, npix, cw, n_bins (fastdiv.h)
 };
 
@@ -324,7 +325,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   } else {
     // R21: bin = (s + o_p) mod B with a per-pixel Philox offset
     const u4 o = philox_rk((uint32_t)p, (uint32_t)(p >> 32), 0xFFFFFFFEu, 0u, S.rk);
-    const uint32_t op = min((uint32_t)((float)B * unif(o.a)), B - 1u);
+    const uint32_t op = unif_index(B, o.a);
     // b = (s + op) mod B; the cell's rank rel = (b - op) mod B = s mod B
     uint32_t rel;
     if (P.div32) fastdiv_divmod((uint32_t)s, P.fd_b, rel);
@@ -341,7 +342,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   pc.inv_n = inv_n;
   pc.acc = 0.0f;
   const u4 a = philox_rk(pc.id_lo, pc.id_hi, 0xFFFFFFFFu, 0u, S.rk);
-  const int e = (FL & FL_MULTI_E) ? min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1) : 0;
+  const int e = (FL & FL_MULTI_E) ? (int)unif_index((uint32_t)S.n_emitters, a.c) : 0;
   PathState& ps = pc.ps;
   ps.e = e;
   if (S.camera_kind == DTS_CAMERA_PINHOLE) {
@@ -418,7 +419,6 @@ __device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t 
 }
 
 // ---------------------------------------------------------------- histogram splat (step 4)
-__constant__ uint32_t g_check_cells;  // histogram cells of the current launch (check build)
 // Per-bin dedicated paths: a retiring path adds its whole
 // contribution to its own cell.  Lanes that retire in the same iteration on the
 // same cell (consecutive sample ids of one cell) are combined first
@@ -429,8 +429,10 @@ __constant__ uint32_t g_check_cells;  // histogram cells of the current launch (
 // samples per cell: a warp's paths are mostly consecutive samples of one cell):
 // a 5-step butterfly and one RED.  Called by all 32 lanes of a converged warp;
 // returns false (nothing done) when the lanes are on several cells.
+// (ncells: the launch's histogram cells, for the bounds checks of the check build)
 __device__ __forceinline__ bool splat_one_cell(unsigned dmask, bool done, uint32_t cell, float v, float v2,
-                                               float* g_hist, float* g_sq, float* s_hist, float* s_sq, int lane) {
+                                               float* g_hist, float* g_sq, float* s_hist, float* s_sq, int lane,
+                                               uint32_t ncells) {
   const int first = __ffs(dmask) - 1;
   const uint32_t c0 = __shfl_sync(0xffffffffu, cell, first);
   if (!__all_sync(0xffffffffu, !done || cell == c0)) return false;
@@ -441,7 +443,7 @@ __device__ __forceinline__ bool splat_one_cell(unsigned dmask, bool done, uint32
     if (sq) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
   }
   if (lane != first || a == 0.0f) return true;
-  DTS_CHECK(c0 < g_check_cells);
+  DTS_CHECK(c0 < ncells);
   if (s_hist) {
     atomicAdd(s_hist + c0, a);
     if (s_sq) atomicAdd(s_sq + c0, a2);
@@ -452,7 +454,7 @@ __device__ __forceinline__ bool splat_one_cell(unsigned dmask, bool done, uint32
   return true;
 }
 __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, float v, float v2, float* g_hist,
-                                      float* g_sq, float* s_hist, float* s_sq, int lane) {
+                                      float* g_sq, float* s_hist, float* s_sq, int lane, uint32_t ncells) {
   if (!done) return;
   const unsigned peers = __match_any_sync(dmask, cell);
   const int leader = __ffs(peers) - 1;
@@ -470,7 +472,7 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
     }
   }
   if (lane != leader || v == 0.0f) return;
-  DTS_CHECK(cell < g_check_cells);
+  DTS_CHECK(cell < ncells);
   if (s_hist) {
     atomicAdd(s_hist + cell, v);
     if (s_sq) atomicAdd(s_sq + cell, v2);
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     }
     const bool has = c != 0.0f;
     const unsigned m = __ballot_sync(FULL, has);
-    if (m) splat(m, has, cell, c, 0.0f, P.hist, nullptr, s_hist, nullptr, lane);
+    if (m) splat(m, has, cell, c, 0.0f, P.hist, nullptr, s_hist, nullptr, lane, P.cells);
     __syncwarp();
     const uint32_t rest = df.qn > (uint32_t)kQueue ? df.qn - kQueue : 0u;
     if ((uint32_t)lane < rest)
@@ -747,8 +749,9 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
       if (!(P.one_cell_warps &&
-            splat_one_cell(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane)))
-        splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane);
+            splat_one_cell(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane,
+                           P.cells)))
+        splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells);
       if (done) active = false;
     }
   }
@@ -784,7 +787,7 @@ __device__ __forceinline__ int vanilla_splat(const RenderParams& P, uint32_t pl,
   const DevScene& S = P.S;
   const int bin = arrive >= S.t0 ? (int)floor((arrive - S.t0) / S.dt) : -1;
   if (bin < 0 || bin >= S.n_bins) return 1;
-  DTS_CHECK((size_t)pl * S.n_bins + bin < g_check_cells);
+  DTS_CHECK((size_t)pl * S.n_bins + bin < P.cells);
   const float w = P.resp_w ? __ldg(P.resp_w + bin) : 1.0f;
   if (w == 0.0f) return 1;
   atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, __fdividef(w * c, (float)P.spp));
@@ -812,7 +815,7 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
     ++c_paths;
     const u4 a = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 0u, S.rk);
-    const int e = min((int)((float)S.n_emitters * unif(a.c)), S.n_emitters - 1);
+    const int e = (int)unif_index((uint32_t)S.n_emitters, a.c);
     const f3 xe = ld3(S.em_pos[e]);
     const double te = (double)S.em_t[e];
     const float ek = S.em_k[e];
@@ -1350,6 +1353,9 @@ dts_status dts_scene_create(const dts_scene_desc* desc, dts_scene_t* out) {
   if (!desc) return fail(DTS_E_INVALID_ARG, "desc is NULL");
   dts_status st = validate(*desc);
   if (st != DTS_OK) return st;
+  if ((uint64_t)(desc->crop[2] - desc->crop[0]) * (uint64_t)(desc->crop[3] - desc->crop[1]) * (uint64_t)desc->n_bins >
+      0xFFFFFFFFull)
+    return fail(DTS_E_RANGE, "crop_w * crop_h * n_bins must be < 2^32 (32-bit histogram cell indices)");
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   // attribute queries (cudaGetDeviceProperties costs milliseconds per scene)
@@ -1507,7 +1513,7 @@ size_t dts_hist_cells(dts_scene_t s) {
 // device->host copy overlaps the next band's render.
 static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* d_hist,
                               float* d_hist_sq, uint64_t* d_counters, void* stream, int row0, int row1,
-                              unsigned long long* work) {
+                              unsigned long long* work, bool allow_defer) {
   g_last_launches = 0;
   if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
   if (!d_hist) return fail(DTS_E_INVALID_ARG, "d_hist is NULL");
@@ -1556,10 +1562,9 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
   P.spp_div_b = (uint32_t)(spp / (uint64_t)d.n_bins);
   P.spp_mod_b = (uint32_t)(spp % (uint64_t)d.n_bins);
   cudaStream_t st = (cudaStream_t)stream;
-  if (DTS_CHECKS) {
-    const uint32_t cells32 = (uint32_t)std::min<size_t>(npix * (size_t)d.n_bins, 0xFFFFFFFFu);
-    CUDA_TRY(cudaMemcpyToSymbolAsync(g_check_cells, &cells32, sizeof cells32, 0, cudaMemcpyHostToDevice, st));
-  }
+  // histogram cell indices are 32-bit (dts_scene_create rejects larger crops)
+  if (npix * (uint64_t)d.n_bins > 0xFFFFFFFFull) return fail(DTS_E_RANGE, "crop_w * crop_h * n_bins must be < 2^32");
+  P.cells = (uint32_t)(npix * (uint64_t)d.n_bins);
   if (darts) {
     P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix * (uint64_t)d.n_bins * ns : npix * ns;
     // kernels stage the 16-bit CDF rows and the 8-bit guide rows; stage-1 SPLIT
@@ -1582,7 +1587,9 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     const char* dv = getenv("DTS_DEFER");
     if (dv && (dv[0] == '0' || dv[0] == '1')) want_defer = dv[0] == '1';
     if (d.n_tris > 0 && !smem) return fail(DTS_E_INVALID_ARG, "mesh scenes need the EDA table in shared memory");
-    const bool defer = want_defer && !d_hist_sq && d.n_tris == 0 &&
+    // (row-band launches, which may run concurrently on one scene, never defer:
+    // the queue overflow area is per scene and indexed by CTA and warp)
+    const bool defer = want_defer && allow_defer && !d_hist_sq && d.n_tris == 0 &&
                        (smem ? tbytes : 0) + (P.priv_cells ? pbytes : 0) + qbytes <= kSmemCap;
     P.defer = defer ? 1u : 0u;
     const char* rk = getenv("DTS_REFILL_K");
@@ -1655,7 +1662,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
                       float* d_hist_sq, uint64_t* d_counters, void* stream) {
   if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
   return render_impl(s, spp, seed, sb, se, d_hist, d_hist_sq, d_counters, stream, 0,
-                     s->desc.crop[3] - s->desc.crop[1], s->d_work);
+                     s->desc.crop[3] - s->desc.crop[1], s->d_work, true);
 }
 
 static dts_status ensure_bands(dts_scene_t s) {
@@ -1675,7 +1682,8 @@ dts_status dts_render_rows(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
   if (band < 0 || band >= kHostBands) return fail(DTS_E_INVALID_ARG, "band must be 0..3");
   dts_status r = ensure_bands(s);
   if (r != DTS_OK) return r;
-  return render_impl(s, spp, seed, sb, se, d_hist_band, nullptr, d_counters, stream, row0, row1, s->d_work_band + band);
+  return render_impl(s, spp, seed, sb, se, d_hist_band, nullptr, d_counters, stream, row0, row1, s->d_work_band + band,
+                     false);
 }
 
 dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* h_hist,
@@ -1714,7 +1722,7 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
       const int r0 = rows * k / kHostBands, r1 = rows * (k + 1) / kHostBands;
       cudaStream_t bs = s->band_stream[k & 1];
       dts_status r = render_impl(s, spp, seed, sb, se, s->d_hist_host + (size_t)r0 * row_cells, nullptr,
-                                 s->d_ctr_host, bs, r0, r1, s->d_work_band + k);
+                                 s->d_ctr_host, bs, r0, r1, s->d_work_band + k, false);
       if (r != DTS_OK) return r;
       CUDA_TRY(cudaEventRecord(s->band_ev[k], bs));
       CUDA_TRY(cudaStreamWaitEvent(st, s->band_ev[k], 0));
@@ -1758,6 +1766,24 @@ dts_status dts_check_failures(uint64_t* out) {
   CUDA_TRY(cudaMemcpyFromSymbol(&v, dts::g_dts_check_fail, sizeof v));
   CUDA_TRY(cudaMemcpyToSymbol(dts::g_dts_check_fail, &z, sizeof z));
   *out = (uint64_t)v;
+  return DTS_OK;
+}
+
+dts_status dts_enable_peer(int32_t peer) {
+  int dev = 0, n = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaGetDeviceCount(&n));
+  if (peer < 0 || peer >= n) return fail(DTS_E_INVALID_ARG, "peer device out of range");
+  if (peer == dev) return DTS_OK;
+  int can = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can, dev, peer));
+  if (!can) return fail(DTS_E_CUDA, "no peer access from the current device to the peer");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free error state
+    return DTS_OK;
+  }
+  CUDA_TRY(e);
   return DTS_OK;
 }
 

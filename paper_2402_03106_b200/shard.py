@@ -43,24 +43,36 @@ def render_sharded(render_range: Callable[[int, int], None], spp: int, hist, cou
 _PEER_CACHE: dict = {}
 
 
-def peer_histogram(hist, dst: int = 0):
+def peer_histogram(hist, dst: int = 0, enable_peer: Callable[[int], None] | None = None):
     """The histogram every rank renders into for the fused reduce: rank dst's
     own tensor there, elsewhere the same device memory mapped through CUDA IPC
-    (peer memory over NVLink / NVSwitch on a multi-GPU box).  Collective; the
-    mapping is made once per tensor."""
+    (peer memory over NVLink / NVSwitch on a multi-GPU box).  Collective: the
+    cache key is rank dst's (address, size), broadcast on every call, so all
+    ranks hit or miss together; a mapping is opened once per key.
+    ``enable_peer(device)`` (libdts' dts_enable_peer) is called with the device
+    that owns the mapping, so that this rank's kernels may access it."""
     import torch.distributed as dist
     from torch.multiprocessing.reductions import reduce_tensor
 
-    key = (hist.data_ptr(), hist.numel(), dst)
-    if key in _PEER_CACHE:
+    me = dist.get_rank()
+    hdr = [(hist.data_ptr(), hist.numel(), hist.device.index) if me == dst else None]
+    dist.broadcast_object_list(hdr, src=dst)
+    key = (hdr[0], dst)
+    hit = [key in _PEER_CACHE]
+    # every rank must agree on hit / miss before the (collective) mapping step
+    flags = [None] * dist.get_world_size()
+    dist.all_gather_object(flags, hit[0])
+    if all(flags):
         return _PEER_CACHE[key]
-    obj = [reduce_tensor(hist) if dist.get_rank() == dst else None]
+    obj = [reduce_tensor(hist) if me == dst else None]
     dist.broadcast_object_list(obj, src=dst)
-    if dist.get_rank() == dst:
+    if me == dst:
         target = hist
     else:
         fn, args = obj[0]
         target = fn(*args)
+        if enable_peer is not None and target.device.index is not None:
+            enable_peer(target.device.index)
     _PEER_CACHE[key] = target
     return target
 
@@ -70,21 +82,24 @@ def release_peer_histograms() -> None:
     _PEER_CACHE.clear()
 
 
-def render_sharded_p2p(render_range: Callable, spp: int, hist, counters=None, dst: int = 0, zero: bool = True):
+def render_sharded_p2p(render_range: Callable, spp: int, hist, counters=None, dst: int = 0, zero: bool = True,
+                       enable_peer: Callable[[int], None] | None = None):
     """Fused render + reduce: each rank's render kernel adds its contributions
     (fp32 REDs) directly into rank dst's histogram through peer memory, so no
     reduce collective follows -- the transfer overlaps the render path by path.
     ``render_range(begin, end, target)`` must render into ``target``.  With
     ``zero`` rank dst clears its histogram first (every rank waits for it).
     rank dst's ``hist`` holds the sum when this returns (every rank synchronises
-    and meets at a barrier); the other ranks' ``hist`` are untouched."""
+    and meets at a barrier); the other ranks' ``hist`` are untouched.
+    EXPERIMENTAL: checked with two processes on one GPU only (the pool has one
+    GPU per call); NCCL's reduce stays the default until a multi-GPU run."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank() if world > 1 else 0
     b, e = shard_range(spp, rank, world)
-    target = hist if world == 1 else peer_histogram(hist, dst)
+    target = hist if world == 1 else peer_histogram(hist, dst, enable_peer)
     if zero and rank == dst:
         hist.zero_()
     if world > 1:

@@ -42,7 +42,8 @@ def _worker(rank, world, port, c, spp, seed, out):
     ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
     for step in range(2):   # the second step reuses the mapping and re-zeroes rank 0's histogram
         c_step = torch.zeros_like(ctr)
-        render_sharded_p2p(lambda b, e, t: sc.render(spp, seed, b, e, t, None, c_step), spp, hist, c_step.cpu())
+        render_sharded_p2p(lambda b, e, t: sc.render(spp, seed, b, e, t, None, c_step), spp, hist, c_step.cpu(),
+                           enable_peer=dts.enable_peer)
     if rank == 0:
         np.save(out, hist.cpu().numpy())
     release_peer_histograms()

@@ -57,6 +57,25 @@ def _rel(a, b, floor):
     return np.abs(a - b) / np.maximum(np.abs(b), floor)
 
 
+def _flat(report, name, r, kappa=None, tol=1e-4, frac=0.999, cap=1e-3):
+    """The north_star bar for a debug quantity: relative error <= 1e-4 for
+    >= 99.9 % of the (decision-safe) records, and no record above ``cap`` unless
+    it is ill-conditioned in fp32 (kappa > 100: its error must then stay below
+    1e-4 + 1e-5 kappa).  Counts of the records above 1e-4, and how many of
+    them are ill-conditioned, go into the report."""
+    over = r > tol
+    f = 1.0 - over.mean() if r.size else 1.0
+    ill = (kappa > 100) if kappa is not None else np.zeros_like(over)
+    report[name] = f"max {r.max() if r.size else 0:.2e} >1e-4 {int(over.sum())}/{r.size} (ill-cond {int((over & ill).sum())})"
+    assert f >= frac, (name, f, r.max())
+    if kappa is None:
+        assert r.size == 0 or r.max() < cap, (name, r.max())
+    else:
+        k = np.where(np.isfinite(kappa), kappa, 0.0)
+        assert (r[~ill] < cap).all(), (name, r[~ill].max())
+        assert (r <= tol + 1e-5 * k).all(), (name, (r / np.maximum(k, 1)).max())
+
+
 DEBUG_CASES = [(1, "reuse", {}), (2, "reuse", {}), (3, "split", {}), (3, "reuse", {}), (4, "reuse", {}),
                (5, "split", {}),
                # ablations (PAPER.md:426-435) and uniform-S elliptical sampling (PAPER.md:295)
@@ -87,9 +106,7 @@ def test_sample_debug_parity(dts, oracle, cfg, mode, extra):
     assert (g["tech"][s] == o["tech"][s]).all()
     surf = o["tech"] == 4
     for k in ("p_hg", "p_eda", "p_mix", "gamma", "beta_dir", "wconn"):
-        r = _rel(g[k][s & ~surf], o[k][s & ~surf], 1e-6)
-        report[k] = float(r.max())
-        assert np.quantile(r, 0.9999) < 1e-4 and r.max() < 1e-3, (k, r.max())
+        _flat(report, k, _rel(g[k][s & ~surf], o[k][s & ~surf], 1e-6))
     if surf.any():
         _check_bsdf_weight(c, recs, g, o, s & surf)
     for k in ("wc", "ww"):
@@ -114,16 +131,12 @@ def test_sample_debug_parity(dts, oracle, cfg, mode, extra):
     assert cv.mean() > 0.02
     # fp32 conditioning of E21/E22 (oracle's m_cond = 1/kappa): where the
     # differences S - C, S - q or a geometric S-range width are small against
-    # S, fp32 keeps ~1e-7 kappa relative accuracy.  Well-conditioned records
-    # (kappa <= 100) must meet 1e-4; every record must meet 1e-4 + 1e-5 kappa.
-    wellc = o["m_cond"][cv] >= 1e-2
-    assert wellc.mean() > 0.5
+    # S, fp32 keeps ~1e-7 kappa relative accuracy.  Every quantity meets 1e-4 on
+    # >= 99.9 % of the records; the rest must be ill-conditioned (kappa > 100)
+    # and within 1e-4 + 1e-5 kappa.
     kappa = 1.0 / o["m_cond"][cv]
     for k in ("S", "t", "p_t", "contrib"):
-        r = _rel(g[k][cv], o[k][cv], 1e-30)
-        report[k] = float(r[wellc].max())
-        assert np.quantile(r[wellc], 0.9999) < 1e-4 and r[wellc].max() < 1e-3, (k, r[wellc].max())
-        assert (r <= 1e-4 + 1e-5 * np.where(np.isfinite(kappa), kappa, 0.0)).all(), (k, (r / kappa).max())
+        _flat(report, k, _rel(g[k][cv], o[k][cv], 1e-30), kappa)
     assert np.abs(g["x_ell"][cv] - o["x_ell"][cv]).max() < 1e-4 * max(1.0, np.abs(o["x_ell"][cv]).max())
     nee = s & (o["nee"] > 0)
     if nee.any():
@@ -147,9 +160,7 @@ def test_sample_debug_parity(dts, oracle, cfg, mode, extra):
     err = np.abs(g["d"][med] - o["d"][med])
     report["d"] = float((err / np.maximum(np.abs(o["d"][med]), 1e-3)).max())
     assert (err <= 1e-4 * np.abs(o["d"][med]) + 2e-6).all(), err.max()
-    r = _rel(g["beta_ris"][med], o["beta_ris"][med], 1e-30)
-    report["beta_ris"] = float(r.max())
-    assert np.quantile(r, 0.9999) < 1e-4 and r.max() < 1e-3, r.max()
+    _flat(report, "beta_ris", _rel(g["beta_ris"][med], o["beta_ris"][med], 1e-30))
     assert np.abs(g["x_next"][med] - o["x_next"][med]).max() < 1e-4 * max(1.0, np.abs(o["x_next"][med]).max())
     assert (g["terminate"][s] == o["terminate"][s]).all()
     print(f"cfg{cfg}/{mode}: safe {safe.mean():.5f} max-rel {report}")
@@ -179,8 +190,27 @@ SAME_KEY = [
     ("sphere_mesh_vanilla", lambda: I.small(I.sphere_mesh_config(strategy="vanilla"), 16, 16, n_bins=64, t1=10.0),
      256),
     ("plate_lambert", lambda: I.plate_config([(0.8, 0.0, 1.0)]), 2000),
+    # the kernels that read a table too large for shared memory (32 x 32 cells,
+    # 768 KiB) through L1, element-wise
+    ("cfg3_global_table", lambda: I.small(I.config(3, table_nr=32, table_ns=32), 6, 5, n_bins=64, t1=8.5), 8),
+    ("cfg5_global_table_pixelmode",
+     lambda: I.small(I.config(5, table_nr=32, table_ns=32), 7, 9, n_bins=120, t1=12.0), 150),
+    ("cfg4_global_table", lambda: I.small(I.config(4, table_nr=32, table_ns=32), 24, 24), 64),
     ("plate_plastic_vanilla", lambda: I.plate_config([(0.7, 0.5, 10.0)], strategy="vanilla"), 100000),
 ]
+
+
+# Same-key relative L2 bar: GPU and oracle trace the same Philox paths, and
+# only fp32-vs-fp64 decision flips (a few paths per thousand) separate them
+# (measured 1.8e-6 .. 4.7e-4 in round 1, profiles/README.md).
+SAME_KEY_L2 = 2e-3
+
+
+def _cell_outliers(g, o):
+    """(cells whose same-key value differs by > 1 % of the larger, cells with signal)"""
+    m = (g != 0) | (o != 0)
+    big = np.abs(g - o) > 0.01 * np.maximum(np.abs(g), np.abs(o))
+    return int((big & m).sum()), int(m.sum())
 
 
 def _same_key(dts, oracle, c, spp, seed):
@@ -206,8 +236,11 @@ def test_render_same_key(dts, oracle, name, mk, spp):
     assert abs(ctr["camera_miss"] - st["camera_miss"]) <= 1e-5 * st["paths"] + 2
     # vertex counts agree up to the few paths whose fp32/fp64 decisions diverge
     assert abs(ctr["vertices"] - st["vertices"]) <= 0.02 * st["vertices"]
-    print(f"{name}: same-key relative L2 {rel:.3e}, vertices gpu {ctr['vertices']} oracle {st['vertices']}")
-    assert rel <= 0.01
+    out = _cell_outliers(g, ho)
+    print(f"{name}: same-key relative L2 {rel:.3e}, vertices gpu {ctr['vertices']} oracle {st['vertices']}, "
+          f"cells off by > 1 % {out[0]}/{out[1]}")
+    assert rel <= SAME_KEY_L2
+    assert out[0] <= max(2, 0.01 * out[1])
 
 
 # ------------------------------------------------------------------ full BASELINE sizes, bench launch config
@@ -241,8 +274,10 @@ def test_full_size_sampled_crop(dts, oracle, name, cfg, crop):
     x0, y0, x1, y1 = crop
     gg = g[y0:y1, x0:x1]
     rel = np.linalg.norm(gg - o) / np.linalg.norm(o)
-    print(f"{name}: crop same-key rel L2 {rel:.3e}; counters {cnt}")
-    assert rel <= 0.01
+    out = _cell_outliers(gg, o)
+    print(f"{name}: crop same-key rel L2 {rel:.3e}, cells off by > 1 % {out[0]}/{out[1]}; counters {cnt}")
+    assert rel <= SAME_KEY_L2
+    assert out[0] <= max(2, 0.01 * out[1])
 
 
 # ------------------------------------------------------------------ independent seeds, 3 SE
@@ -251,6 +286,8 @@ INDEP = [
     ("cfg4", lambda: I.small(I.config(4, parity_r_excl=0.3, parity_s_excess=0.05), 4, 4), 20000, 20000),
     ("cfg2", lambda: I.small(I.config(2, parity_s_excess=0.05), 6, 6, n_bins=24, t1=9.0), 4000, 4000),
     ("cfg3_split", lambda: I.small(I.config(3, parity_s_excess=0.05), 4, 4, n_bins=16, t1=6.0), 2000, 2000),
+    # config 3 over its whole time range [4, 40) (16 bins of 2.25)
+    ("cfg3_split_full_range", lambda: I.small(I.config(3, parity_s_excess=0.05), 4, 4, n_bins=16), 2000, 2000),
     ("cfg5_split", lambda: I.small(I.config(5, parity_s_excess=0.05, spp_mode="cell"), 2, 2, n_bins=8, t1=16.0),
      600, 600),
     ("cfg6_mesh", lambda: I.small(I.mesh_config(parity_r_excl=0.3, parity_s_excess=0.05), 4, 4), 20000, 20000),
@@ -276,6 +313,106 @@ def test_render_independent_seeds(dts, oracle, name, mk, ng, no):
     assert (np.abs(z) >= 3).sum() <= max(1, int(0.01 * m.sum()))
 
 
+# ------------------------------------------------------------------ R21 bin assignment, headline config
+def test_r21_bin_assignment_full_width_band(dts, oracle):
+    """Config 5 (per-pixel mode, R21) on a full-width band of 1024 x 4 pixels
+    with one sample per pixel: every pixel's single path lands in bin o_p on the
+    GPU and in the oracle (integer floor(B u)), so the two
+    histograms have the same support pixel by pixel (zero bin-assignment
+    divergence), and the same-key band agrees to the usual L2."""
+    c = I.as_f32(I.config(5, crop=(0, 510, 1024, 514)))
+    sc = _scene(dts, c)
+    h, _, ctr = dts.render_to_tensor(sc, 1, c["seed"])
+    torch.cuda.synchronize()
+    g = h.cpu().numpy().astype(np.float64)
+    qo, _ = oracle.build_table(c)
+    o = oracle.render(c, qo, 1, c["seed"], sq=False)
+    ho = o["hist"]
+    assert dts.counters_dict(ctr)["paths"] == 4096 == o["stats"]["paths"]
+    wrong_bin = 0
+    support_diff = 0
+    for y in range(4):
+        for x in range(1024):
+            op = oracle.pixel_offset(c, c["seed"], (510 + y) * 1024 + x)
+            gz, oz = np.flatnonzero(g[y, x]), np.flatnonzero(ho[y, x])
+            wrong_bin += int(any(b != op for b in gz)) + int(any(b != op for b in oz))
+            support_diff += int(len(gz) != len(oz))
+    rel = np.linalg.norm(g - ho) / np.linalg.norm(ho)
+    nz = int((ho > 0).sum())
+    print(f"R21 band: pixels with signal {nz}, wrong bins {wrong_bin}, support differences {support_diff}, "
+          f"same-key rel L2 {rel:.3e}")
+    assert wrong_bin == 0
+    assert nz > 3000
+    # a same-key path may still end with zero vs non-zero contribution after an
+    # fp32/fp64 decision flip (a few per thousand), never in another bin
+    assert support_diff <= 0.005 * 4096
+    assert rel <= 2e-3
+
+
+def _supercell_sums(h, hsq, npb, by, bx, bb):
+    """Super-cell sums T = sum of cell estimates over by x bx pixels x bb bins and
+    their variance sum_cells hist_sq / n_pb (= sum over samples X^2 / n_pb^2, an
+    upper bound of Var T that is tight when the per-path coefficient of variation
+    is large, as it is in config 5: 12-35)."""
+    H, W, B = h.shape
+    v = np.where(npb > 0, hsq / np.maximum(npb, 1), 0.0)
+    t = h.reshape(H // by, by, W // bx, bx, B // bb, bb).sum(axis=(1, 3, 5))
+    var = v.reshape(H // by, by, W // bx, bx, B // bb, bb).sum(axis=(1, 3, 5))
+    return t, var
+
+
+def _npb(oracle, c, spp, seed):
+    """n_pb of every crop cell (R21), from the oracle's offsets and counts."""
+    x0, y0, x1, y1 = c["crop"]
+    B = c["n_bins"]
+    out = np.zeros((y1 - y0, x1 - x0, B))
+    q, r = divmod(spp, B)
+    for y in range(y0, y1):
+        for x in range(x0, x1):
+            op = oracle.pixel_offset(c, seed, y * c["width"] + x)
+            rel = (np.arange(B) - op) % B
+            out[y - y0, x - x0] = q + (rel < r)
+    return out
+
+
+def test_cfg5_supercells_independent_seeds(dts, oracle):
+    """Statistical parity where the headline lives ("verified to
+    converge to the same results"): config 5 in its per-pixel
+    mode (R21, 1024 spp per pixel over 1000 bins, about one path per cell), the
+    oracle and the GPU with independent seeds, compared on pooled 8 x 8-pixel x
+    10-bin super-cells over an early, a mid and a late window ([4, 20), [40, 60),
+    [80, 100)).  The oracle traces only the windows' paths (bin_window); the GPU
+    renders 16x the samples.  >= 200 super-cells, >= 99 % within 3 SE."""
+    crop = (488, 488, 536, 536)                                  # 48 x 48 px: 36 super-pixels
+    c = I.as_f32(I.config(5, crop=crop, parity_s_excess=0.05))
+    sc = _scene(dts, c)
+    spp_o, spp_g, seed_o, seed_g = 1024, 16384, 2002, 1001
+    h, hs, _ = dts.render_to_tensor(sc, spp_g, seed_g, with_sq=True)
+    torch.cuda.synchronize()
+    g, gs = h.cpu().numpy().astype(np.float64), hs.cpu().numpy().astype(np.float64)
+    qo, _ = oracle.build_table(c)
+    ho = np.zeros_like(g)
+    hso = np.zeros_like(g)
+    for b0, b1 in [(40, 200), (400, 600), (800, 1000)]:
+        o = oracle.render(dict(c, bin_window=(b0, b1)), qo, spp_o, seed_o)
+        ho[..., b0:b1] = o["hist"][..., b0:b1]
+        hso[..., b0:b1] = o["hist_sq"][..., b0:b1]
+    tg, vg = _supercell_sums(g, gs, _npb(oracle, c, spp_g, seed_g), 8, 8, 10)
+    to, vo = _supercell_sums(ho, hso, _npb(oracle, c, spp_o, seed_o), 8, 8, 10)
+    win = np.zeros(100, bool)
+    win[4:20] = win[40:60] = win[80:100] = True
+    tg, vg, to, vo = tg[..., win], vg[..., win], to[..., win], vo[..., win]
+    m = (tg > 0) | (to > 0)
+    z = ((tg - to) / np.sqrt(vg + vo + 1e-300))[m]
+    frac = np.mean(np.abs(z) < 3)
+    print(f"cfg5 super-cells: {m.sum()} compared, within 3 SE {frac:.4f}, mean z {z.mean():+.3f}, "
+          f"|z| max {np.abs(z).max():.2f}; windows' sums gpu {tg.sum():.4e} oracle {to.sum():.4e}")
+    assert m.sum() >= 200
+    assert frac >= 0.99
+    # the windows' totals agree within 3 SE as well
+    assert abs(tg.sum() - to.sum()) <= 3 * math.sqrt(vg.sum() + vo.sum())
+
+
 # ------------------------------------------------------------------ boundary edge cases
 def test_edge_cases(dts):
     c = I.as_f32(I.small(I.config(4), 4, 4))
@@ -299,6 +436,14 @@ def test_edge_cases(dts):
         dts.Scene(dict(c, n_ris=16))
     with pytest.raises(dts.DtsError, match="exceeds 64 bits"):  # path ids (s N_pix + p) B + b
         sc.render(1 << 62, 1, 0, 8, h)
+    # histogram cell indices are 32-bit: 2048 x 2048 pixels x 1024 bins = 2^32 cells is rejected
+    with pytest.raises(dts.DtsError, match="DTS_E_RANGE"):
+        dts.Scene(I.as_f32(I.config(5, width=2048, height=2048, n_bins=1024)))
+    dts.Scene(I.as_f32(I.config(5, width=2048, height=2048, n_bins=1023))).close()
+    # peer access: the current device is a no-op, a device out of range an error
+    dts.enable_peer(torch.cuda.current_device())
+    with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
+        dts.enable_peer(torch.cuda.device_count() + 5)
     # mesh scenes need the table in shared memory (a 32 x 32 table is not)
     cm = I.as_f32(I.small(I.mesh_config(table_nr=32, table_ns=32), 4, 4))
     sm = _scene(dts, cm)
@@ -342,10 +487,14 @@ def test_render_host_e2e_matches_device(dts):
     assert int(hc[2]) == dts.counters_dict(ctr)["vertices"]
 
 
-def test_render_host_banded_matches_device(dts):
+@pytest.mark.parametrize("defer", ["0", "1"])
+def test_render_host_banded_matches_device(dts, monkeypatch, defer):
     """Histograms >= 256 MB take dts_render_host's banded path (row bands on two
     streams, each band's copy overlapping the next band's render): the same
-    paths and ids as one device render."""
+    paths and ids as one device render.  With DTS_DEFER=1 the band launches,
+    which run concurrently, still take the immediate kernels (one scene-owned
+    queue overflow area)."""
+    monkeypatch.setenv("DTS_DEFER", defer)
     c = I.as_f32(I.config(5, crop=(384, 384, 640, 640), spp=4))   # 256 x 256 x 1000 bins = 262 MB
     sc = _scene(dts, c)
     d, _, ctr = dts.render_to_tensor(sc, 4, 9)
@@ -359,9 +508,12 @@ def test_render_host_banded_matches_device(dts):
     sc.close()
 
 
-def test_render_rows_bands_equal_full_render(dts):
+@pytest.mark.parametrize("defer", ["0", "1"])
+def test_render_rows_bands_equal_full_render(dts, monkeypatch, defer):
     """dts_render_rows over row bands (two bands on two streams at a time, as
-    a pipelining caller would) reproduces dts_render; bad ranges are errors."""
+    a pipelining caller would) reproduces dts_render; bad ranges are errors.
+    DTS_DEFER=1 must not change that (band launches never defer)."""
+    monkeypatch.setenv("DTS_DEFER", defer)
     c = I.as_f32(I.small(I.config(3), 24, 20, n_bins=64, t1=9.0))
     sc = _scene(dts, c)
     full, _, cf = dts.render_to_tensor(sc, 8, 4)
@@ -394,7 +546,8 @@ def test_single_pixel_single_bin_and_table_in_global_memory(dts, oracle):
     qo, _ = oracle.build_table(c)
     o = oracle.render(c, qo, 4096, 8, sq=False)["hist"]
     g = h.cpu().numpy()
-    assert abs(g.sum() - o.sum()) <= 0.01 * o.sum()
+    assert g.shape == o.shape == (1, 1, 1)
+    assert abs(g.sum() - o.sum()) <= SAME_KEY_L2 * o.sum()
 
 
 # ------------------------------------------------------------------ sensor response W(t)
@@ -416,7 +569,7 @@ def test_response_same_key_and_rejection(dts, oracle, strategy, spp):
     st = o["stats"]
     print(f"response/{strategy}: same-key rel L2 {rel:.3e}; samples gpu {ctr['samples']} oracle {st['samples']}; "
           f"rejected gpu {ctr['rejected']} ({ctr['rejected'] / max(1, ctr['samples']):.4f}) oracle {st['rejected']}")
-    assert rel <= 0.01
+    assert rel <= SAME_KEY_L2
     assert abs(ctr["samples"] - st["samples"]) <= 0.01 * st["samples"]
     assert abs(ctr["rejected"] - st["rejected"]) <= 0.01 * max(st["rejected"], 1)
     if strategy == "darts":
@@ -469,7 +622,7 @@ def test_render_same_key_both_variants(dts, oracle, monkeypatch, name, mk, spp, 
     assert ctr["paths"] == o["stats"]["paths"]
     assert abs(ctr["conn_nonempty"] - o["stats"]["conn_nonempty"]) <= 0.01 * o["stats"]["conn_nonempty"] + 2
     print(f"{name}/DTS_DEFER={defer}: same-key relative L2 {rel:.3e}")
-    assert rel <= 0.01
+    assert rel <= SAME_KEY_L2
 
 
 def _check_bsdf_weight(c, recs, g, o, m):
