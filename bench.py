@@ -215,7 +215,7 @@ def run_gpu(args):
     paths_per_step = counts["paths"] / args.steps
 
     # ---- end to end through the C ABI with HOST buffers (pinned), N GPUs
-    e2e = run_e2e(args, c, sc, world, rank, stream, torch, dist, dts, ms / args.steps)
+    e2e = None if args.no_e2e else run_e2e(args, c, sc, world, rank, stream, torch, dist, dts, ms / args.steps)
 
     if rank == 0:
         peaks = _peaks()
@@ -269,13 +269,9 @@ def run_gpu(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
-        mse = _profile_json("mse_vs_oracle_r01.json")
-        if mse and args.config == 5:
-            # the metric's second half, measured by scripts/mse_vs_oracle.py (not in this run)
-            line["mse_vs_oracle_equal_time"] = {
-                "ratio_cpu_over_gpu": mse.get("mse_ratio_cpu_over_gpu_equal_time"),
-                "mse_vs_spp_slope": mse.get("mse_vs_spp_slope"), "crop": mse.get("crop"),
-                "source": "profiles/mse_vs_oracle_r01.json (scripts/mse_vs_oracle.py)"}
+            if not args.no_mse:
+                # the metric's second half, measured in this run
+                line["mse_vs_oracle_equal_time"] = mse_equal_time(args.config, args.mse_seeds, args.mse_crop)
         print(json.dumps(line), flush=True)
     if world > 1:
         from paper_2402_03106_b200.shard import release_peer_histograms
@@ -363,14 +359,6 @@ def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts, step_ms=1e9):
             "timing": "host wall clock (perf_counter) around scene_create..histogram in pinned host memory, max over ranks"}
 
 
-def _profile_json(name):
-    try:
-        with open(os.path.join(ROOT, "profiles", name)) as f:
-            return json.load(f)
-    except (OSError, ValueError):
-        return None
-
-
 def _profile_traffic(cfg):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -409,6 +397,85 @@ def cpu_baseline(cfg_idx, budget_s=15.0):
             "sample": f"{c['name']} centre crop {w}x{w} px, all {c['n_bins']} bins, spp {c['spp']} "
                       f"({st['paths']} paths, {st['vertices']} vertices) in {el:.1f} s, fp64",
             "paths_per_s": st["paths"] / el}
+
+
+def mse_equal_time(cfg_idx, seeds=16, crop=8):
+    """BASELINE.json metric, second half: "MSE vs oracle at equal time"
+    (the paper's equal-time MSE methodology).
+    On a centre crop of the config (every bin, per-pixel spp as configured):
+      1. the fp64 oracle renders the crop at the config's spp with ``seeds``
+         seeds on all host cores; T_cpu = the median wall time of one render;
+      2. the GPU renders the same crop at the sample count spp_eq it finishes
+         in T_cpu (from a timed probe launch), DIRECTLY, with ``seeds`` seeds;
+         each launch is timed (CUDA events) to show it took ~T_cpu;
+      3. the reference for GPU seed k is the mean of the other seeds' renders
+         (leave-one-out: (seeds - 1) x spp_eq samples, independent of render k);
+         the oracle's reference is the mean of all GPU renders (seeds x spp_eq,
+         thousands of times the oracle's count).  MSE over all crop cells.
+    The reference's own error adds MSE_gpu / (seeds - 1) to each GPU MSE (reported,
+    and removed in the corrected figure).  Per-path contributions are heavy-tailed
+    (SURVEY 8(c.6)): the mean over seeds is dominated by rare paths, so the median
+    is reported beside it.  An equal-spp GPU render (the oracle's count, same
+    seeds protocol) checks that both estimators have the same MSE per sample."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2402_03106_b200 import dts
+    c0 = I.as_f32(I.config(cfg_idx))
+    crop = min(crop, c0["width"], c0["height"])
+    c = I.crop_center(c0, crop, crop)
+    spp = c["spp"]
+    q = O.build_table(c)[0]
+    h_o, t_o = [], []
+    for k in range(seeds):
+        t = time.perf_counter()
+        h_o.append(O.render(c, q, spp, 500 + k, sq=False, nthreads=os.cpu_count())["hist"])
+        t_o.append(time.perf_counter() - t)
+    t_cpu = statistics.median(t_o)
+    sc = dts.Scene(c)
+    sc.table_build()
+
+    def gpu(n, seed):
+        h = torch.zeros(sc.hist_shape(), dtype=torch.float32, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        sc.render(n, seed, 0, n, h)
+        e1.record()
+        torch.cuda.synchronize()
+        return h.double().cpu().numpy(), e0.elapsed_time(e1) * 1e-3
+
+    gpu(spp, 1)                                        # warm-up
+    probe = 64 * spp
+    _, t_probe = gpu(probe, 2)
+    spp_eq = max(spp, int(probe * t_cpu / t_probe))
+    h_g, t_g = [], []
+    for k in range(seeds):
+        h, t = gpu(spp_eq, 9000 + k)
+        h_g.append(h)
+        t_g.append(t)
+    tot = np.sum(h_g, axis=0)
+    mse_g_raw = [float(((h - (tot - h) / (seeds - 1)) ** 2).mean()) for h in h_g]
+    mse_g = [m * (seeds - 1) / seeds for m in mse_g_raw]   # minus the leave-one-out reference's variance
+    ref = tot / seeds
+    mse_o = [float(((h - ref) ** 2).mean()) for h in h_o]
+    h_s = [gpu(spp, 7000 + k)[0] for k in range(seeds)]
+    mse_s = [float(((h - ref) ** 2).mean()) for h in h_s]
+    med = statistics.median
+    sc.close()
+    return {
+        "ratio_cpu_over_gpu_mean": float(np.mean(mse_o) / np.mean(mse_g)),
+        "ratio_cpu_over_gpu_median": float(med(mse_o) / med(mse_g)),
+        "mse_cpu": {"mean": float(np.mean(mse_o)), "median": med(mse_o)},
+        "mse_gpu_equal_time": {"mean": float(np.mean(mse_g)), "median": med(mse_g),
+                               "mean_uncorrected": float(np.mean(mse_g_raw))},
+        "mse_gpu_equal_spp": {"mean": float(np.mean(mse_s)), "median": med(mse_s)},
+        "t_cpu_s": t_cpu, "cpu_cores": os.cpu_count(), "spp_cpu": spp, "spp_gpu_equal_time": spp_eq,
+        "t_gpu_s_median": med(t_g), "seeds": seeds,
+        "crop": f"{c['name']} centre {crop}x{crop} px x {c['n_bins']} bins",
+        "reference": f"GPU renders, leave-one-out mean of {seeds - 1} x spp_eq (GPU MSE), mean of {seeds} x spp_eq "
+                     "(oracle MSE)",
+    }
 
 
 def run_reference(args):
@@ -455,6 +522,10 @@ def main():
                     help="N > 1: one NCCL reduce after the renders (default), or p2p: every rank's render "
                          "kernel adds into rank 0's histogram through CUDA IPC peer memory (no reduce)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (A/B and profiling runs only)")
+    ap.add_argument("--no-mse", action="store_true", help="skip the equal-time MSE against the oracle")
+    ap.add_argument("--mse-seeds", type=int, default=16)
+    ap.add_argument("--mse-crop", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--spp", type=int, default=None, help="override spp (profiling runs only; not a bench line)")
     args = ap.parse_args()

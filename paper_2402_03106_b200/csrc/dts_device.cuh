@@ -165,6 +165,26 @@ __device__ __forceinline__ uint32_t f2u23(float x) {
   return (uint32_t)x;
 }
 
+// ----------------------------------------------------------------- packed fp32 (sm_100 FADD2/FMUL2/FFMA2)
+// Two independent IEEE fp32 operations per issue slot: the same round-to-
+// nearest results as the scalar instructions, half the issue cost.  The path
+// kernel is issue-bound, so the 8 RIS candidates are evaluated
+// in pairs.  DTS_F32X2=0 builds the scalar form (A/B).
+#ifndef DTS_F32X2
+#define DTS_F32X2 1
+#endif
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ float2 f2s(float x) { return make_float2(x, x); }
+#if DTS_F32X2
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+#else
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return f2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return f2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return f2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y)); }
+#endif
+
 // ----------------------------------------------------------------- accurate small-argument helpers
 // -ln(1 - x) for x in [0, 1): series x + x^2/2 + x^3/3 below 1/64 (relative
 // truncation error < x^3/4 < 1e-6), MUFU lg2 above (relative error < 1e-5).
@@ -1133,38 +1153,58 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float qd = dot(ww, cv);
     const f3 perp = cv - ww * qd;
     const float perp2 = dot(perp, perp);
-    float e2[8], sr[8];
+    // candidate i's 23-bit uniform: (m2 + bitrev3(i) 2^20 + bitrev5(row) 2^15) mod 2^23
+    const uint32_t vbase = m2 + (br5 << 15);
+    float e2[8], s3[8];
     float emax = -__int_as_float(0x7f800000);
+    // pairs (2j, 2j + 1) of candidates in packed fp32; per candidate:
+    //   E14 with the sign of R1: d = t_lo - ln(1 - p_m u) / sigma_t, with
+    //   1 - p_m u = (1 - u) + u (1 - p_m), 1 - u = 2 - (1 + u) exact (MUFU lg2
+    //   keeps the absolute error of d below ~1e-7 / sigma_t);
+    //   Delta = R_M - E - d (R4); r^2 = |x + w d - x_e|^2 = (d - q)^2 + perp^2;
+    //   s = Delta^{-1/2}; valid iff Delta > 0 and r <= Delta, tested as
+    //   r^2 s^2 < Delta (for Delta <= 0, s = 1e10 makes it false);
+    //   log2 of Phi' = Delta^{-3/2} exp(-r^2/(4 D Delta) - sigma_a Delta) (E9,
+    //   constants dropped) = log2(s^3) + k1 r^2 s^2 + k2 Delta.
+    const float2 Tm2 = f2s(T_m), lo2 = f2s(lo), negk = f2s(-S.inv_sigma_t * kLn2);
+    const float2 negc = f2s(-counts), resM2 = f2s(resM), negqd = f2s(-qd), p2 = f2s(perp2);
+    const float2 k1 = f2s(S.neg_inv4D_log2e), k2 = f2s(S.neg_sa_log2e);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t br3 = __brev((uint32_t)i) >> 29;
-      const uint32_t v = (m2 + ((br3 * 32u + br5) << 15)) & 0x7FFFFFu;
-      const float ui = mant01(v);
-      // E14 with the sign of R1: d = t_lo - ln(1 - p_m u) / sigma_t with
-      // 1 - p_m u = (1 - u) + u (1 - p_m) (1 - u exact); MUFU lg2 keeps the
-      // absolute error of d below ~1e-7 / sigma_t
-      const float di = fmaf(-__log2f(fmaf(ui, T_m, 1.0f - ui)), S.inv_sigma_t * kLn2, lo);
-      if (DBG) dbg->cand_d[i] = di;
-      const float Delta = resM - counts * di;  // R4
-      const float dq = di - qd;
-      const float r2i = fmaf(dq, dq, perp2);
-      // Delta > 0 and r <= Delta in one test (Delta |Delta| < 0 when Delta < 0;
-      // the boundary cases r = Delta, Delta = 0 have measure zero)
-      const bool valid = r2i < Delta * fabsf(Delta);
-      const float s = rsqrtf(fmaxf(Delta, 1e-20f));  // s^3 stays finite for invalid candidates
-      // log2 of Phi' = Delta^{-3/2} exp(-r^2/(4 D Delta) - sigma_a Delta) (E9, constants dropped)
-      const float ex = fmaf(S.neg_inv4D_log2e * r2i, s * s, S.neg_sa_log2e * Delta);
-      e2[i] = valid ? ex : -__int_as_float(0x7f800000);
-      sr[i] = s;
-      emax = fmaxf(emax, e2[i]);
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t v0 = (vbase + ((__brev((uint32_t)(2 * j)) >> 29) << 20)) & 0x7FFFFFu;
+      const uint32_t v1 = (vbase + ((__brev((uint32_t)(2 * j + 1)) >> 29) << 20)) & 0x7FFFFFu;
+      const float2 M = f2(__uint_as_float(0x3f800000u | v0), __uint_as_float(0x3f800000u | v1));  // 1 + u
+      const float2 u = add2(M, f2s(-1.0f));
+      const float2 omu = fma2(M, f2s(-1.0f), f2s(2.0f));   // 1 - u, exact
+      const float2 a = fma2(u, Tm2, omu);                   // 1 - p_m u
+      const float2 d = fma2(f2(__log2f(a.x), __log2f(a.y)), negk, lo2);
+      const float2 Delta = fma2(d, negc, resM2);
+      const float2 dq = add2(d, negqd);
+      const float2 r2 = fma2(dq, dq, p2);
+      const float2 sv = f2(rsqrtf(fmaxf(Delta.x, 1e-20f)), rsqrtf(fmaxf(Delta.y, 1e-20f)));
+      const float2 ss = mul2(sv, sv);
+      const float2 q = mul2(r2, ss);                        // r^2 / Delta
+      const float2 ex = fma2(q, k1, mul2(Delta, k2));
+      const float2 cube = mul2(ss, sv);                     // s^3 (finite for invalid candidates)
+      if (DBG) { dbg->cand_d[2 * j] = d.x; dbg->cand_d[2 * j + 1] = d.y; }
+      e2[2 * j] = q.x < Delta.x ? ex.x : -__int_as_float(0x7f800000);
+      e2[2 * j + 1] = q.y < Delta.y ? ex.y : -__int_as_float(0x7f800000);
+      s3[2 * j] = cube.x;
+      s3[2 * j + 1] = cube.y;
+      emax = fmaxf(emax, fmaxf(e2[2 * j], e2[2 * j + 1]));
     }
-    float W = 0.0f;
     if (emax == -__int_as_float(0x7f800000)) emax = 0.0f;  // all invalid: exp2(-inf) = 0, not NaN
+    // R7: weights relative to the largest exponent, w_i = s_i^3 2^(e_i - emax)
+    float2 W2 = f2s(0.0f);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {  // R7: weights relative to the largest exponent
-      e2[i] = sr[i] * sr[i] * sr[i] * exp2f(e2[i] - emax);
-      W += e2[i];
+    for (int j = 0; j < 4; ++j) {
+      const float2 x = add2(f2(e2[2 * j], e2[2 * j + 1]), f2s(-emax));
+      const float2 w = mul2(f2(s3[2 * j], s3[2 * j + 1]), f2(exp2f(x.x), exp2f(x.y)));
+      e2[2 * j] = w.x;
+      e2[2 * j + 1] = w.y;
+      W2 = add2(W2, w);
     }
+    const float W = W2.x + W2.y;
     if (DBG) {
       for (int i = 0; i < 8; ++i) dbg->cand_wn[i] = W > 0.0f ? e2[i] / W : 0.0f;
     }

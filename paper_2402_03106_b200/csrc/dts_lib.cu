@@ -548,6 +548,10 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
   // per-lane event counters, summed over the warp at the end
   uint32_t c_vert = 0, c_conn = 0, c_nee = 0;
   uint32_t c_samp = 0;  // non-zero contributions (path samples); DARTS never rejects one (its bin has W > 0)
+#ifndef DTS_COUNT_SKIP
+#define DTS_COUNT_SKIP 0
+#endif
+  uint32_t c_skip1 = 0, c_skip2 = 0;  // DTS_COUNT_SKIP builds: medium vertices whose connection provably cannot land
   uint32_t waste = 0;                // idle lane-iterations since the last refill
   // runs up to kQueue queued sampling jobs, one per lane, and splats them;
   // jobs left in the global overflow slots move down into the shared slots
@@ -698,6 +702,20 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
       const unsigned act_r = rep == 0 ? act : __ballot_sync(FULL, active && !done);
       if (act_r == 0u) break;
       const bool run = active && !done;
+      if (DTS_COUNT_SKIP && run && pc.ps.kind == KIND_MEDIUM && SH == DTS_MEDIUM_BOX) {
+        const float resm = d2f(pc.ps.resM - S.dt);
+        if (!may_connect_bound<SH>(S, pc.ps.x, resm)) ++c_skip1;
+        // tighter: max over the box corners y of |y - x| + |y - x_e| bounds S(t) on any chord
+        const f3 xe = ld3(S.em_pos[0]);
+        float mx = 0.0f;
+        for (int cidx = 0; cidx < 8; ++cidx) {
+          const f3 y = mk((cidx & 1) ? S.bmax[0] : S.bmin[0], (cidx & 2) ? S.bmax[1] : S.bmin[1],
+                          (cidx & 4) ? S.bmax[2] : S.bmin[2]);
+          const f3 a1 = y - pc.ps.x, a2 = y - xe;
+          mx = fmaxf(mx, sqrtf(dot(a1, a1)) + sqrtf(dot(a2, a2)));
+        }
+        if (resm > mx * 1.001f) ++c_skip2;
+      }
       bool pushed = false, pushed1 = false;
       bool cn = false, wnee = false, alive = false;
       int reason = 0;
@@ -761,12 +779,20 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     c_conn += __shfl_xor_sync(FULL, c_conn, o);
     c_nee += __shfl_xor_sync(FULL, c_nee, o);
     c_samp += __shfl_xor_sync(FULL, c_samp, o);
+    if (DTS_COUNT_SKIP) {
+      c_skip1 += __shfl_xor_sync(FULL, c_skip1, o);
+      c_skip2 += __shfl_xor_sync(FULL, c_skip2, o);
+    }
   }
   if (lane == 0 && P.counters) {  // per-vertex counters: 64-bit, straight to global
     atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
     atomicAdd(P.counters + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
     atomicAdd(P.counters + DTS_CTR_WALL_NEE, (unsigned long long)c_nee);
     atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
+    if (DTS_COUNT_SKIP) {  // (diagnostic build: reuses two counters DARTS leaves at 0)
+      atomicAdd(P.counters + DTS_CTR_REJECTED, (unsigned long long)c_skip1);
+      atomicAdd(P.counters + DTS_CTR_NONFINITE, (unsigned long long)c_skip2);
+    }
   }
   __syncthreads();
   if (P.priv_cells) {  // flush the CTA's private histogram (coalesced REDs of its non-zero cells)
