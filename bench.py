@@ -43,11 +43,26 @@ try:
 except (OSError, ValueError):
     pass
 
-# algorithmic thread-instructions per DARTS vertex
-# (REUSE 610; SPLIT adds an HG sample and a second intersection, +40).
-ALG_INSTR_PER_VERTEX = {"reuse": 610, "split": 650}
 # issue roofline: 148 SMs x 4 SMSPs x 32 lanes x 1 warp-instruction / clock
 SMS, SMSP, LANES = 148, 4, 32
+# the measured issue peak of the pipe microbenchmarks (FFMA + LOP3, 1965 MHz;
+# profiles/peaks_r01.log): 3.662e13 thread-instructions/s
+MEASURED_ISSUE_TIPS = 36.62
+
+
+def _opcounts():
+    with open(os.path.join(ROOT, "bench", "opcounts.json")) as f:
+        return {k: v["ops"] for k, v in json.load(f)["vertex_types"].items()}
+
+
+def algorithmic_instructions(counts: dict, mode: str) -> tuple[float, dict]:
+    """Frozen algorithmic thread-instructions (bench/opcounts.json) summed over
+    the measured vertex mix; returns (total, mix)."""
+    ops = _opcounts()
+    cam, wall, walk = counts["camera_vertices"], counts["wall_vertices"], counts["walk_vertices"]
+    med = counts["vertices"] - cam - wall - walk
+    mix = {"camera": cam, "wall": wall, "medium_split_walk_only": walk, f"medium_{mode}": med}
+    return sum(n * ops[k] for k, n in mix.items()), mix
 
 
 def _peaks():
@@ -221,9 +236,11 @@ def run_gpu(args):
         peaks = _peaks()
         sm_max = peaks.get("sm_max_mhz", 1965.0)
         mode = c["direction_mode"]
-        alg = ALG_INSTR_PER_VERTEX[mode]
+        alg_total, mix = algorithmic_instructions(counts, mode)
+        alg = alg_total / max(counts["vertices"], 1)              # per vertex, over the measured mix
         peak_tips = SMS * SMSP * LANES * sm_max * 1e6 / 1e12      # Tinst/s at the max SM clock
-        # the dominant kernel is the render kernel: per-rank vertices / its launch time
+        # the dominant kernel(s): the render's launches (two-stage: walk + connect),
+        # per-rank algorithmic instructions / their CUDA-event time on the stream
         achieved = (verts_per_step / world) * alg / (kern_avg * 1e-3) / 1e12
         value = verts_per_step / (ms / args.steps * 1e-3)
         traffic = None if (args.spp or args.strategy or args.direction_mode) else _profile_traffic(args.config)
@@ -255,15 +272,21 @@ def run_gpu(args):
             "paths_per_s": paths_per_step / (ms / args.steps * 1e-3),
             "roofline": {
                 "bound": "alu", "achieved": achieved, "peak": peak_tips, "unit": "Tinst/s",
-                "frac": achieved / peak_tips, "traffic": traffic,
-                "basis": f"{alg} algorithmic thread-instructions per vertex (SURVEY 8d.2) x vertices / "
-                         f"render-kernel time; peak = 148 SM x 4 issue x 32 lanes x {sm_max:.0f} MHz"
+                "frac": achieved / peak_tips, "frac_measured_peak": achieved / MEASURED_ISSUE_TIPS,
+                "traffic": traffic,
+                "basis": f"{alg:.1f} algorithmic thread-instructions per vertex: bench/opcounts.json frozen counts "
+                         f"x the measured vertex mix {{{', '.join(f'{k}: {v / max(counts['vertices'], 1):.4f}' for k, v in mix.items())}}}"
+                         f" x vertices / render time (CUDA events); peak = 148 SM x 4 issue x 32 lanes x {sm_max:.0f} MHz "
+                         f"(nominal); frac_measured_peak against the FFMA+LOP3 microbenchmark's {MEASURED_ISSUE_TIPS} Tinst/s"
                          + ("; BVH traversal of the mesh not counted" if c.get("mesh") else ""),
+                "alg_instr_per_vertex": alg,
                 "kernel_ms": kern_avg,
+                "launches_per_step": launch.get("n_launches"),
             },
             "clocks": clocks,
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps * world,
+            # per step and rank: the table build + the render's launches (two-stage: 2 per chunk)
+            "gpu_launches": (1 + launch.get("n_launches", 1)) * args.steps * world,
             "launch": launch,
             "counters": counts,
         }

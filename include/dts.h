@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define DTS_ABI_VERSION 1
+#define DTS_ABI_VERSION 2
 #define DTS_MAX_EMITTERS 8
 #define DTS_MAX_MATERIALS 8
 #define DTS_TABLE_COS_BINS 256 /* "[-1, 1] is uniformly subdivided into 256 bins" */
@@ -198,6 +198,10 @@ enum {
   DTS_CTR_WALL_NEE,        /* non-zero wall NEE contributions */
   DTS_CTR_SAMPLES,         /* path samples: non-zero connection / NEE contributions before W */
   DTS_CTR_REJECTED,        /* path samples whose recorded time has W = 0 (Fig. 6) */
+  DTS_CTR_WALK_VERTICES,   /* of DTS_CTR_VERTICES: walk-only MEDIUM vertices of the two-stage render
+                              (their connection provably could not reach the bin, so it was not sampled) */
+  DTS_CTR_CAMERA_VERTICES, /* of DTS_CTR_VERTICES: camera / detector vertices (one per walk started) */
+  DTS_CTR_WALL_VERTICES,   /* of DTS_CTR_VERTICES: wall and triangle-surface vertices (DARTS kernels) */
   DTS_NUM_COUNTERS
 };
 

@@ -802,13 +802,21 @@ __device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_
 // ----------------------------------------------------------------- one DARTS vertex
 // Returns true if the walk continues.  contrib receives the vertex's
 // connection (+ wall NEE) contribution; end_reason the DTS_CTR_* of a stop.
-template <bool DBG, bool SMEM, int SH, int FL, bool DEFER = false>
+// WALK (the walk stage of the two-stage render, SPLIT scenes): a vertex whose
+// connection provably cannot land in its bin (conn_bound) runs only the walk:
+// the mixture direction, the connection's intersection and S range, and the
+// wall NEE are skipped -- they would contribute exactly 0 -- and the walk's
+// random numbers, directions and distances are the full vertex's, bit for bit.
+// *walk_step receives the distance moved.
+template <bool DBG, bool SMEM, int SH, int FL, bool DEFER = false, bool WALK = false>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason,
                                              const Defer* df = nullptr, bool* pushed = nullptr,
                                              RisReq* rq = nullptr, uint32_t* nsamp = nullptr,
-                                             bool* pushed1 = nullptr) {
+                                             bool* pushed1 = nullptr, float* walk_step = nullptr) {
+  static_assert(!WALK || ((FL & FL_SPLIT) && !(FL & FL_MESH) && !DEFER && !DBG),
+                "the walk stage serves SPLIT scenes without meshes");
   contrib = 0.0f;
   conn_nonempty = false;
   wall_nee = false;
@@ -828,7 +836,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   // warp's stage-1 queue; the warp later runs up to 32 of them at once (mixture
   // direction, intersection, S range) and forwards the non-empty ones to the
   // sampling queue.  A lane that finds the queue full connects inline.
-  bool skip_conn = false;
+  bool skip_conn = WALK;
   if (SPLIT && DEFER && kStage1Build && !DBG) {
     const bool cand = ps.kind == KIND_MEDIUM && may_connect_bound<SH>(S, ps.x, d2f(ps.resM - S.dt));
     const unsigned m1 = __ballot_sync(df->act, cand);
@@ -867,7 +875,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     const float cw = dot(n, we);
     const float resm = d2f(ps.resM - S.dt);
     float nee = 0.0f;
-    if (cw > 0.0f && resm - C <= 0.0f && resM - C > 0.0f) {  // E + C in [Rm, RM)
+    if (!WALK && cw > 0.0f && resm - C <= 0.0f && resM - C > 0.0f) {  // E + C in [Rm, RM)
       // R14: time-checked direct NEE at a wall vertex
       nee = ps.beta * (alb * (1.0f / kPi)) * cw * ek * segment_tr<SH, WALLS, MESH>(S, ps.x, xe, C, we) *
             __fdividef(1.0f, C * C);
@@ -977,7 +985,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   bool want_job = false;
   float job_dlo = 0.0f, job_width = 0.0f;
   float clo = lo, chi = hi;
-  int hitc = hit;
+  int hitc = WALK ? HIT_MISS : hit;
   if (SPLIT && ps.kind == KIND_MEDIUM) {
     if (skip_conn) {
       hitc = HIT_MISS;  // the connection stage runs from the stage-1 queue (or cannot land)
@@ -1132,6 +1140,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     ps.beta *= S.albedo;
     ps.x = fma3(ww, d, ps.x);
     ps.resM -= f2d(counts * d);
+    if (WALK) *walk_step = d;
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
     if (DBG) { dbg->event = 1; dbg->istar = 0; dbg->d = d; dbg->beta_ris = S.albedo; }
@@ -1240,6 +1249,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     ps.resM -= f2d(counts * dsel);
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
+    if (WALK) *walk_step = dsel;
     if (DBG) { dbg->event = 1; dbg->istar = (int)is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
   } else {
     if (WALLS && hit == HIT_WALL) {
@@ -1250,6 +1260,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       ps.x = xn;
       ps.resM -= f2d(counts * hi);
       ps.kind = KIND_WALL;
+      if (WALK) *walk_step = hi;
       ps.face = face;
       ps.w = ww;
       if (DBG) { dbg->event = 2; dbg->d = hi; dbg->beta_ris = 1.0f; }

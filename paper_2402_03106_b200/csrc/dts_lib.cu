@@ -57,6 +57,11 @@ struct dts_scene {
   cudaStream_t band_stream[2] = {nullptr, nullptr};  // dts_render_host row bands
   cudaEvent_t band_ev[kHostBands + 1] = {};
   unsigned long long* d_work_band = nullptr;
+  // two-stage render: hand-off buffer and 3 counters (walk work, connect work,
+  // slots) per launch slot: 0 = dts_render, 1 + band = row-band launches
+  struct HandOff* d_ho[1 + kHostBands] = {};
+  size_t ho_cap[1 + kHostBands] = {};
+  unsigned long long* d_wf = nullptr;
   float4* d_bvh = nullptr;         // mesh BVH nodes (R32)
   float4* d_tri4 = nullptr;        // mesh triangles in leaf order
   int32_t* d_tri_map = nullptr;    // caller -> leaf order, then leaf -> caller order (2 n_tris)
@@ -221,6 +226,9 @@ struct RenderParams {
   uint32_t one_cell_warps;        // 1: per-cell order with >= 32 samples per cell (splat fast path)
   uint32_t div32;                 // 1: work indices, sample indices + B fit 32 bits (fast divisions)
   uint32_t cells;                 // histogram cells of this launch (< 2^32; bounds checks of the check build)
+  uint64_t w_base;                // first work index of this launch (two-stage render: the chunk's)
+  struct HandOff* ho;             // two-stage render: the chunk's hand-off records
+  unsigned long long* ho_count;   // two-stage render: hand-off slots allocated (the connect stage's work count)
   FastDiv fd_ns, fd_npix, fd_cw, fd_b;  // division by n_s, npix, cw, n_bins (fastdiv.h)
 };
 
@@ -488,9 +496,90 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
 #ifndef DTS_TABLE_SMEM
 #define DTS_TABLE_SMEM 1
 #endif
-template <bool SMEM, int SH, int FL, bool DEFER>
+// ---------------------------------------------------------------- two-stage render (SPLIT scenes)
+// In SPLIT scenes (R29) the walk direction does not depend on the connection,
+// so while a path's connections provably cannot reach its bin (conn_margin >
+// 0: R_m - E exceeds every S a connection could have) its vertices need only
+// the walk.  For config 5 that holds for ~70 % of all vertices, for config 3
+// for ~78 %.  The walk stage (walk_kernel) runs those vertices with the walk-
+// only darts_vertex<WALK> -- every lane of a warp in the same, cheaper code --
+// and hands each surviving path over, at the first vertex that might connect,
+// through a 64-byte record in HBM; the connect stage (render_darts_kernel
+// <RESUME>) continues the path with full vertices.  Same path ids, same random
+// numbers, same vertices: the histogram equals the one-stage render's.
+struct __align__(16) HandOff {
+  float x[3], beta;
+  float w[3];
+  uint32_t k;                // next bounce index; 0xFFFFFFFF marks an unused slot
+  double resM;
+  uint32_t id_lo, id_hi;
+  uint32_t cell;
+  float inv_n;
+  int32_t kind_face_e;       // kind | (face + 1) << 8 | e << 16
+  uint32_t pad_;
+};
+static_assert(sizeof(HandOff) == 64, "hand-off records are 64 bytes");
+constexpr uint32_t kHoEmpty = 0xFFFFFFFFu;
+constexpr uint32_t kHoBlock = 32;  // hand-off slots a warp reserves at a time
+
+// Lower bound of (R_m - E) - max S of any connection from x: every point y of a
+// chord from x satisfies S = |y - x| + |y - x_e| <= (farthest medium point from
+// x) + (farthest medium point from any emitter) (may_connect_bound).  A
+// connection lands in the bin only if S >= R_m - E, so a positive margin means
+// it cannot (nor can the wall NEE: C <= that bound).  fp32 safety: 1e-4
+// relative + 1e-3 absolute.
+template <int SH>
+__device__ __forceinline__ float conn_margin(const DevScene& S, f3 x, double resM) {
+  const float resm = d2f(resM - S.dt);
+  float far_x;
+  if (SH == DTS_MEDIUM_BOX) {
+    const float fx = fmaxf(x.x - S.bmin[0], S.bmax[0] - x.x);
+    const float fy = fmaxf(x.y - S.bmin[1], S.bmax[1] - x.y);
+    const float fz = fmaxf(x.z - S.bmin[2], S.bmax[2] - x.z);
+    far_x = sqrtf(fmaf(fx, fx, fmaf(fy, fy, fz * fz)));
+  } else {
+    const f3 d = x - ld3(S.center);
+    far_x = sqrtf(dot(d, d)) + sqrtf(S.radius2);
+  }
+  return resm - fmaf(far_x + S.far_e, 1.0001f, 1e-3f);
+}
+
+__device__ __forceinline__ void store_handoff(HandOff* ho, const PathCtx& pc) {
+  const PathState& ps = pc.ps;
+  uint4* d = reinterpret_cast<uint4*>(ho);
+  d[0] = make_uint4(__float_as_uint(ps.x.x), __float_as_uint(ps.x.y), __float_as_uint(ps.x.z), __float_as_uint(ps.beta));
+  d[1] = make_uint4(__float_as_uint(ps.w.x), __float_as_uint(ps.w.y), __float_as_uint(ps.w.z), pc.k);
+  d[2] = make_uint4((uint32_t)__double2loint(ps.resM), (uint32_t)__double2hiint(ps.resM), pc.id_lo, pc.id_hi);
+  d[3] = make_uint4(pc.cell, __float_as_uint(pc.inv_n), (uint32_t)(ps.kind | ((ps.face + 1) << 8) | (ps.e << 16)), 0u);
+}
+
+__device__ __forceinline__ bool load_handoff(const RenderParams& P, uint64_t slot, PathCtx& pc) {
+  const uint4* s = reinterpret_cast<const uint4*>(P.ho + slot);
+  const uint4 a = __ldcs(s + 1);
+  if (a.w == kHoEmpty) return false;
+  const uint4 b = __ldcs(s), c = __ldcs(s + 2), d = __ldcs(s + 3);
+  PathState& ps = pc.ps;
+  ps.x = mk(__uint_as_float(b.x), __uint_as_float(b.y), __uint_as_float(b.z));
+  ps.beta = __uint_as_float(b.w);
+  ps.w = mk(__uint_as_float(a.x), __uint_as_float(a.y), __uint_as_float(a.z));
+  pc.k = a.w;
+  ps.resM = __hiloint2double((int)c.y, (int)c.x);
+  pc.id_lo = c.z;
+  pc.id_hi = c.w;
+  pc.cell = d.x;
+  pc.inv_n = __uint_as_float(d.y);
+  ps.kind = (int)(d.z & 0xFFu);
+  ps.face = (int)((d.z >> 8) & 0xFFu) - 1;
+  ps.e = (int)(d.z >> 16);
+  pc.acc = 0.0f;
+  return true;
+}
+
+template <bool SMEM, int SH, int FL, bool DEFER, bool RESUME = false>
 __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_MINB) render_darts_kernel(const RenderParams P) {
   constexpr bool WALLS = (FL & FL_WALLS) != 0;
+  // RESUME (connect stage): the work items are the walk stage's hand-off slots
+  const uint64_t ntotal = RESUME ? (uint64_t)*(volatile unsigned long long*)P.ho_count : P.total;
   extern __shared__ __align__(16) uint16_t s_dyn[];
   __shared__ uint64_t s_bar;
   // rare events (path starts and ends) are counted per CTA in shared memory;
@@ -547,11 +636,8 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
   PathCtx pc;
   // per-lane event counters, summed over the warp at the end
   uint32_t c_vert = 0, c_conn = 0, c_nee = 0;
+  uint32_t c_wall = 0;  // wall / surface vertices (scenes with walls or meshes)
   uint32_t c_samp = 0;  // non-zero contributions (path samples); DARTS never rejects one (its bin has W > 0)
-#ifndef DTS_COUNT_SKIP
-#define DTS_COUNT_SKIP 0
-#endif
-  uint32_t c_skip1 = 0, c_skip2 = 0;  // DTS_COUNT_SKIP builds: medium vertices whose connection provably cannot land
   uint32_t waste = 0;                // idle lane-iterations since the last refill
   // runs up to kQueue queued sampling jobs, one per lane, and splats them;
   // jobs left in the global overflow slots move down into the shared slots
@@ -653,8 +739,8 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
         unsigned long long nb = 0;
         if (lane == 0) nb = atomicAdd(P.work, (unsigned long long)kChunk);
         nb = __shfl_sync(FULL, nb, 0);
-        uint64_t ne = nb + kChunk < P.total ? nb + kChunk : P.total;
-        if (nb >= P.total) {
+        uint64_t ne = nb + kChunk < ntotal ? nb + kChunk : ntotal;
+        if (nb >= ntotal) {
           exhausted = true;
           ne = nb;
         }
@@ -668,10 +754,10 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
         wn = nq < ne ? nq : ne;
         we = ne;
       }
-      const bool starts = !active && my != ~0ull && my < P.total;
+      const bool starts = !active && my != ~0ull && my < ntotal;
       const unsigned sm = __ballot_sync(FULL, starts);
-      if (lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
-      if (starts) active = start_path<SH, FL>(P, my, pc, s_ctr);
+      if (!RESUME && lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
+      if (starts) active = RESUME ? load_handoff(P, my, pc) : start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
     }
     const unsigned act = __ballot_sync(FULL, active);
     // queue batches; once the work is exhausted and every lane idle, drain them
@@ -702,20 +788,6 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
       const unsigned act_r = rep == 0 ? act : __ballot_sync(FULL, active && !done);
       if (act_r == 0u) break;
       const bool run = active && !done;
-      if (DTS_COUNT_SKIP && run && pc.ps.kind == KIND_MEDIUM && SH == DTS_MEDIUM_BOX) {
-        const float resm = d2f(pc.ps.resM - S.dt);
-        if (!may_connect_bound<SH>(S, pc.ps.x, resm)) ++c_skip1;
-        // tighter: max over the box corners y of |y - x| + |y - x_e| bounds S(t) on any chord
-        const f3 xe = ld3(S.em_pos[0]);
-        float mx = 0.0f;
-        for (int cidx = 0; cidx < 8; ++cidx) {
-          const f3 y = mk((cidx & 1) ? S.bmax[0] : S.bmin[0], (cidx & 2) ? S.bmax[1] : S.bmin[1],
-                          (cidx & 4) ? S.bmax[2] : S.bmin[2]);
-          const f3 a1 = y - pc.ps.x, a2 = y - xe;
-          mx = fmaxf(mx, sqrtf(dot(a1, a1)) + sqrtf(dot(a2, a2)));
-        }
-        if (resm > mx * 1.001f) ++c_skip2;
-      }
       bool pushed = false, pushed1 = false;
       bool cn = false, wnee = false, alive = false;
       int reason = 0;
@@ -724,6 +796,10 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
       RisReq rq;
       rq.need = false;
       if (run) {
+        // vertex mix of the roofline basis (bench/opcounts.json): camera vertices
+        // (once per walk, shared-memory counter), wall / surface vertices
+        if (pc.ps.kind == KIND_CAMERA) atomicAdd(s_ctr + DTS_CTR_CAMERA_VERTICES, 1u);
+        if (WALLS || (FL & FL_MESH)) c_wall += (pc.ps.kind == KIND_WALL || pc.ps.kind == KIND_SURF) ? 1u : 0u;
         const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
         const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
         r[0] = a.a; r[1] = a.b; r[2] = a.c; r[3] = a.d;
@@ -779,20 +855,14 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     c_conn += __shfl_xor_sync(FULL, c_conn, o);
     c_nee += __shfl_xor_sync(FULL, c_nee, o);
     c_samp += __shfl_xor_sync(FULL, c_samp, o);
-    if (DTS_COUNT_SKIP) {
-      c_skip1 += __shfl_xor_sync(FULL, c_skip1, o);
-      c_skip2 += __shfl_xor_sync(FULL, c_skip2, o);
-    }
+    if (WALLS || (FL & FL_MESH)) c_wall += __shfl_xor_sync(FULL, c_wall, o);
   }
   if (lane == 0 && P.counters) {  // per-vertex counters: 64-bit, straight to global
     atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
     atomicAdd(P.counters + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
     atomicAdd(P.counters + DTS_CTR_WALL_NEE, (unsigned long long)c_nee);
     atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
-    if (DTS_COUNT_SKIP) {  // (diagnostic build: reuses two counters DARTS leaves at 0)
-      atomicAdd(P.counters + DTS_CTR_REJECTED, (unsigned long long)c_skip1);
-      atomicAdd(P.counters + DTS_CTR_NONFINITE, (unsigned long long)c_skip2);
-    }
+    if (WALLS || (FL & FL_MESH)) atomicAdd(P.counters + DTS_CTR_WALL_VERTICES, (unsigned long long)c_wall);
   }
   __syncthreads();
   if (P.priv_cells) {  // flush the CTA's private histogram (coalesced REDs of its non-zero cells)
@@ -801,6 +871,142 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
       if (s_sq && s_sq[i] != 0.0f) atomicAdd(P.hist_sq + i, s_sq[i]);
     }
   }
+  if (P.counters && threadIdx.x < DTS_NUM_COUNTERS && s_ctr[threadIdx.x])
+    atomicAdd(P.counters + threadIdx.x, (unsigned long long)s_ctr[threadIdx.x]);
+}
+
+// Walk stage of the two-stage render (see HandOff): persistent, one lane per
+// path, no EDA table (so no shared-memory staging), walk-only vertices while
+// conn_margin > 0.  The margin is tracked without re-evaluating the bound at
+// every vertex: a step of length d lowers R_m - E by (counts d) and can raise
+// the bound by at most d (|y - x| is 1-Lipschitz in x), so margin - (1 +
+// counts) d is a lower bound; the exact margin is recomputed only when that
+// lower bound reaches 0.  A path whose margin is <= 0 is written to the next
+// hand-off slot (warp-level reservation of kHoBlock slots from a global
+// counter); a path that ends in the walk stage contributed nothing.
+#ifndef DTS_BLOCK_WALK
+#define DTS_BLOCK_WALK 896
+#endif
+constexpr int kBlockWalk = DTS_BLOCK_WALK;
+template <int SH, int FL>
+__global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams P) {
+  static_assert((FL & FL_SPLIT) && !(FL & FL_MESH), "walk stage: SPLIT scenes without meshes");
+  __shared__ uint32_t s_ctr[DTS_NUM_COUNTERS];
+  if (threadIdx.x < DTS_NUM_COUNTERS) s_ctr[threadIdx.x] = 0u;
+  __syncthreads();
+  const DevScene& S = P.S;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint64_t wn = 0, we = 0;   // warp-uniform work queue [wn, we)
+  uint64_t hn = 0, he = 0;   // warp-uniform reserved hand-off slots [hn, he)
+  bool exhausted = false, active = false;
+  PathCtx pc;
+  float margin = 0.0f;
+  uint32_t c_vert = 0, c_walkm = 0, c_wall = 0, waste = 0;
+  while (true) {
+    const unsigned idle = __ballot_sync(FULL, !active);
+    waste += __popc(idle);
+    if (idle && !exhausted && (waste >= P.refill_k || idle == FULL)) {
+      waste = 0;
+      const uint32_t nidle = __popc(idle);
+      const uint32_t rank = __popc(idle & lt_mask);
+      const uint64_t avail = we - wn;
+      uint64_t my = ~0ull;
+      if (avail >= nidle) {
+        my = wn + rank;
+        wn += nidle;
+      } else {
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(P.work, (unsigned long long)kChunk);
+        nb = __shfl_sync(FULL, nb, 0);
+        uint64_t ne = nb + kChunk < P.total ? nb + kChunk : P.total;
+        if (nb >= P.total) {
+          exhausted = true;
+          ne = nb;
+        }
+        if (rank < avail) {
+          my = wn + rank;
+        } else {
+          const uint64_t cand = nb + (rank - avail);
+          my = cand < ne ? cand : ~0ull;
+        }
+        const uint64_t nq = nb + (nidle - avail);
+        wn = nq < ne ? nq : ne;
+        we = ne;
+      }
+      const bool starts = !active && my != ~0ull && my < P.total;
+      const unsigned sm = __ballot_sync(FULL, starts);
+      if (lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
+      if (starts) {
+        active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
+        margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
+      }
+    }
+    const unsigned act = __ballot_sync(FULL, active);
+    if (act == 0u) {
+      if (exhausted) break;
+      continue;
+    }
+    bool hand = false, done = false;
+    if (active) {
+      if (margin <= 0.0f) margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
+      hand = margin <= 0.0f;
+    }
+    if (active && !hand) {
+      const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
+      const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
+      const uint32_t r[8] = {a.a, a.b, a.c, a.d, b.a, b.b, b.c, b.d};
+      const float counts = (S.warped || pc.ps.kind != KIND_CAMERA) ? 1.0f : 0.0f;
+      if (pc.ps.kind == KIND_CAMERA) atomicAdd(s_ctr + DTS_CTR_CAMERA_VERTICES, 1u);
+      c_walkm += pc.ps.kind == KIND_MEDIUM ? 1u : 0u;
+      c_wall += pc.ps.kind == KIND_WALL ? 1u : 0u;
+      float contrib = 0.0f, step = 0.0f;
+      bool cn = false, wnee = false;
+      int reason = 0;
+      const bool alive = darts_vertex<false, false, SH, FL, false, true>(S, nullptr, pc.ps, r, contrib, nullptr, cn,
+                                                                         wnee, reason, nullptr, nullptr, nullptr,
+                                                                         nullptr, nullptr, &step);
+      ++pc.k;
+      ++c_vert;
+      const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
+      done = !alive || cap;
+      if (done) atomicAdd(s_ctr + (cap ? (int)DTS_CTR_CAP_HITS : reason), 1u);
+      margin -= (1.0f + counts) * step * 1.00001f;
+    }
+    const unsigned hm = __ballot_sync(FULL, hand);
+    if (hm) {
+      const uint32_t nh = __popc(hm), rank = __popc(hm & lt_mask);
+      const uint64_t avail = he - hn;
+      uint64_t slot;
+      if (avail >= nh) {
+        slot = hn + rank;
+        hn += nh;
+      } else {
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(P.ho_count, (unsigned long long)kHoBlock);
+        nb = __shfl_sync(FULL, nb, 0);
+        slot = rank < avail ? hn + rank : nb + (rank - avail);
+        hn = nb + (nh - avail);
+        he = nb + kHoBlock;
+      }
+      if (hand) store_handoff(P.ho + slot, pc);
+    }
+    if (hand || done) active = false;
+  }
+  // this warp's unused reserved slots are marked empty for the connect stage
+  if ((uint64_t)lane < he - hn) reinterpret_cast<uint4*>(P.ho + hn + lane)[1].w = kHoEmpty;
+  for (int o = 16; o > 0; o >>= 1) {
+    c_vert += __shfl_xor_sync(FULL, c_vert, o);
+    c_walkm += __shfl_xor_sync(FULL, c_walkm, o);
+    c_wall += __shfl_xor_sync(FULL, c_wall, o);
+  }
+  if (lane == 0 && P.counters) {
+    atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
+    atomicAdd(P.counters + DTS_CTR_WALK_VERTICES, (unsigned long long)c_walkm);
+    if (c_wall) atomicAdd(P.counters + DTS_CTR_WALL_VERTICES, (unsigned long long)c_wall);
+  }
+  __syncthreads();
   if (P.counters && threadIdx.x < DTS_NUM_COUNTERS && s_ctr[threadIdx.x])
     atomicAdd(P.counters + threadIdx.x, (unsigned long long)s_ctr[threadIdx.x]);
 }
@@ -1059,6 +1265,36 @@ struct PickMesh {
   static const void* inf() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_INFINITE, FL | FL_MESH, false>; }
   static const void* sph() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_SPHERE, FL | FL_MESH, false>; }
 };
+// two-stage render (SPLIT scenes without meshes, BOX or SPHERE media)
+template <bool SMEM>
+struct PickResume {
+  template <int FL>
+  struct F {
+    static const void* box() {
+      if constexpr ((FL & FL_SPLIT) != 0) return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, FL, false, true>;
+      return nullptr;
+    }
+    static const void* inf() { return nullptr; }
+    static const void* sph() {
+      if constexpr ((FL & FL_SPLIT) != 0 && (FL & FL_WALLS) == 0)
+        return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, FL, false, true>;
+      return nullptr;
+    }
+  };
+};
+template <int FL>
+struct PickWalk {
+  static const void* box() {
+    if constexpr ((FL & FL_SPLIT) != 0) return (const void*)walk_kernel<DTS_MEDIUM_BOX, FL>;
+    return nullptr;
+  }
+  static const void* inf() { return nullptr; }
+  static const void* sph() {
+    if constexpr ((FL & FL_SPLIT) != 0 && (FL & FL_WALLS) == 0) return (const void*)walk_kernel<DTS_MEDIUM_SPHERE, FL>;
+    return nullptr;
+  }
+};
+
 static const void* darts_kernel_ptr(bool smem, bool defer, const dts_scene_desc& d) {
   const int sh = d.medium_shape, fl = scene_flags(d);
   if (d.n_tris > 0) return (smem && !defer) ? pick_fl<PickMesh>(sh, fl) : nullptr;
@@ -1426,6 +1662,8 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   for (int i = 0; i <= kHostBands; ++i)
     if (s->band_ev[i]) cudaEventDestroy(s->band_ev[i]);
   cudaFree(s->d_work_band);
+  for (int i = 0; i <= kHostBands; ++i) cudaFree(s->d_ho[i]);
+  cudaFree(s->d_wf);
   cudaFree(s->d_bvh);
   cudaFree(s->d_tri4);
   cudaFree(s->d_tri_map);
@@ -1539,7 +1777,7 @@ size_t dts_hist_cells(dts_scene_t s) {
 // device->host copy overlaps the next band's render.
 static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* d_hist,
                               float* d_hist_sq, uint64_t* d_counters, void* stream, int row0, int row1,
-                              unsigned long long* work, bool allow_defer) {
+                              unsigned long long* work, bool allow_defer, int slot) {
   g_last_launches = 0;
   if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
   if (!d_hist) return fail(DTS_E_INVALID_ARG, "d_hist is NULL");
@@ -1654,11 +1892,68 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       }
       P.qover = s->d_qover;
     }
-    CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
-    void* args[] = {&P};
-    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(blk), args, dyn, st));
-    CUDA_TRY(cudaGetLastError());
-    g_last_launches = 1;
+    // two-stage render (walk stage + connect stage, see HandOff) for SPLIT
+    // scenes without meshes in BOX / SPHERE media; DTS_WAVEFRONT=0 forces the
+    // one-stage kernel (A/B)
+    bool wave = !defer && d.direction_mode == DTS_DIR_SPLIT && d.n_tris == 0 && d.medium_shape != DTS_MEDIUM_INFINITE;
+    const char* wv = getenv("DTS_WAVEFRONT");
+    if (wv && wv[0] == '0') wave = false;
+    const void* kwalk = wave ? pick_fl<PickWalk>(d.medium_shape, scene_flags(d)) : nullptr;
+    const void* kres = wave ? (smem ? pick_fl<PickResume<true>::F>(d.medium_shape, scene_flags(d))
+                                    : pick_fl<PickResume<false>::F>(d.medium_shape, scene_flags(d)))
+                            : nullptr;
+    if (!kwalk || !kres) {
+      CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
+      void* args[] = {&P};
+      CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(blk), args, dyn, st));
+      CUDA_TRY(cudaGetLastError());
+      g_last_launches = 1;
+    } else {
+      int bw = 1;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bw, kwalk, kBlockWalk, 0));
+      if (bw < 1) bw = 1;
+      const uint64_t gw = (uint64_t)s->num_sms * bw;
+      // paths per chunk: the hand-off buffer holds one chunk (64 B per path)
+      uint64_t chunk = (uint64_t)1 << 27;
+      const char* ch = getenv("DTS_WF_CHUNK");
+      if (ch && atoll(ch) >= 1024) chunk = (uint64_t)atoll(ch);
+      if (chunk > P.total) chunk = P.total;
+      const size_t cap = (size_t)chunk + (size_t)gw * (kBlockWalk / 32) * kHoBlock;
+      if (s->ho_cap[slot] < cap) {
+        cudaFree(s->d_ho[slot]);
+        s->d_ho[slot] = nullptr;
+        s->ho_cap[slot] = 0;
+        if (cudaMalloc(&s->d_ho[slot], cap * sizeof(HandOff)) != cudaSuccess)
+          return fail(DTS_E_OOM, "cudaMalloc(hand-off buffer) failed");
+        s->ho_cap[slot] = cap;
+      }
+      if (!s->d_wf && cudaMalloc(&s->d_wf, 3 * (1 + kHostBands) * sizeof(unsigned long long)) != cudaSuccess)
+        return fail(DTS_E_OOM, "cudaMalloc(two-stage counters) failed");
+      unsigned long long* wf = s->d_wf + 3 * slot;
+      const uint64_t gc = std::min<uint64_t>(grid, (cap + 31) / 32 / (blk / 32) + 1);
+      int launches = 0;
+      for (uint64_t w0 = 0; w0 < P.total; w0 += chunk) {
+        RenderParams PW = P;
+        PW.w_base = w0;
+        PW.total = std::min<uint64_t>(chunk, P.total - w0);
+        PW.work = wf;
+        PW.ho = s->d_ho[slot];
+        PW.ho_count = wf + 2;
+        RenderParams PC = PW;
+        PC.w_base = 0;
+        PC.work = wf + 1;
+        CUDA_TRY(cudaMemsetAsync(wf, 0, 3 * sizeof(unsigned long long), st));
+        void* aw[] = {&PW};
+        CUDA_TRY(cudaLaunchKernel(kwalk, dim3((unsigned)std::min<uint64_t>(gw, (PW.total + kBlockWalk - 1) / kBlockWalk)),
+                                  dim3(kBlockWalk), aw, 0, st));
+        void* ac[] = {&PC};
+        CUDA_TRY(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        CUDA_TRY(cudaLaunchKernel(kres, dim3((unsigned)gc), dim3(blk), ac, dyn, st));
+        CUDA_TRY(cudaGetLastError());
+        launches += 2;
+      }
+      g_last_launches = launches;
+    }
     g_last_grid = (int)grid;
     g_last_block = blk;
     g_last_smem = (int)dyn;
@@ -1688,7 +1983,7 @@ dts_status dts_render(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, u
                       float* d_hist_sq, uint64_t* d_counters, void* stream) {
   if (!s) return fail(DTS_E_INVALID_ARG, "scene is NULL");
   return render_impl(s, spp, seed, sb, se, d_hist, d_hist_sq, d_counters, stream, 0,
-                     s->desc.crop[3] - s->desc.crop[1], s->d_work, true);
+                     s->desc.crop[3] - s->desc.crop[1], s->d_work, true, 0);
 }
 
 static dts_status ensure_bands(dts_scene_t s) {
@@ -1709,7 +2004,7 @@ dts_status dts_render_rows(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
   dts_status r = ensure_bands(s);
   if (r != DTS_OK) return r;
   return render_impl(s, spp, seed, sb, se, d_hist_band, nullptr, d_counters, stream, row0, row1, s->d_work_band + band,
-                     false);
+                     false, 1 + band);
 }
 
 dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t sb, uint64_t se, float* h_hist,
@@ -1748,7 +2043,7 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
       const int r0 = rows * k / kHostBands, r1 = rows * (k + 1) / kHostBands;
       cudaStream_t bs = s->band_stream[k & 1];
       dts_status r = render_impl(s, spp, seed, sb, se, s->d_hist_host + (size_t)r0 * row_cells, nullptr,
-                                 s->d_ctr_host, bs, r0, r1, s->d_work_band + k, false);
+                                 s->d_ctr_host, bs, r0, r1, s->d_work_band + k, false, 1 + k);
       if (r != DTS_OK) return r;
       CUDA_TRY(cudaEventRecord(s->band_ev[k], bs));
       CUDA_TRY(cudaStreamWaitEvent(st, s->band_ev[k], 0));

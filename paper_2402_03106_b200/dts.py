@@ -23,9 +23,10 @@ _lib = ctypes.CDLL(LIB_PATH)
 # ----------------------------------------------------------------- ABI structs
 F3 = ctypes.c_float * 3
 MAX_EMITTERS = 8
-NUM_COUNTERS = 12
+NUM_COUNTERS = 15
 COUNTER_NAMES = ("paths", "camera_miss", "vertices", "conn_nonempty", "ris_invalid", "early_exit", "escapes",
-                 "cap_hits", "nonfinite", "wall_nee", "samples", "rejected")
+                 "cap_hits", "nonfinite", "wall_nee", "samples", "rejected", "walk_vertices",
+                 "camera_vertices", "wall_vertices")
 
 
 class SceneDesc(ctypes.Structure):

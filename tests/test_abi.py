@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(dts.EXPORTED)
-    assert dts.abi_version() == 1
+    assert dts.abi_version() == 2
     assert dts.status_string(2) == "DTS_E_STATE"
 
 
