@@ -429,7 +429,8 @@ def mse_equal_time(cfg_idx, seeds=16, crop=8):
       1. the fp64 oracle renders the crop at the config's spp with ``seeds``
          seeds on all host cores; T_cpu = the median wall time of one render;
       2. the GPU renders the same crop at the sample count spp_eq it finishes
-         in T_cpu (from a timed probe launch), DIRECTLY, with ``seeds`` seeds;
+         in T_cpu (from a timed probe launch, refined once at the estimated
+         count), DIRECTLY, with ``seeds`` seeds;
          each launch is timed (CUDA events) to show it took ~T_cpu;
       3. the reference for GPU seed k is the mean of the other seeds' renders
          (leave-one-out: (seeds - 1) x spp_eq samples, independent of render k);
@@ -472,6 +473,8 @@ def mse_equal_time(cfg_idx, seeds=16, crop=8):
     probe = 64 * spp
     _, t_probe = gpu(probe, 2)
     spp_eq = max(spp, int(probe * t_cpu / t_probe))
+    _, t_1 = gpu(spp_eq, 3)                             # one refinement at the estimated count
+    spp_eq = max(spp, int(spp_eq * t_cpu / t_1))
     h_g, t_g = [], []
     for k in range(seeds):
         h, t = gpu(spp_eq, 9000 + k)

@@ -59,9 +59,14 @@ struct dts_scene {
   unsigned long long* d_work_band = nullptr;
   // two-stage render: hand-off buffer and 3 counters (walk work, connect work,
   // slots) per launch slot: 0 = dts_render, 1 + band = row-band launches
+  // (dts_render's slot 0 holds two halves: consecutive chunks alternate between
+  // them and between the caller's stream and wf_stream, so each chunk's connect-
+  // stage tail overlaps the next chunk's walk stage)
   struct HandOff* d_ho[1 + kHostBands] = {};
   size_t ho_cap[1 + kHostBands] = {};
   unsigned long long* d_wf = nullptr;
+  cudaStream_t wf_stream = nullptr;
+  cudaEvent_t wf_ev[2] = {};
   float4* d_bvh = nullptr;         // mesh BVH nodes (R32)
   float4* d_tri4 = nullptr;        // mesh triangles in leaf order
   int32_t* d_tri_map = nullptr;    // caller -> leaf order, then leaf -> caller order (2 n_tris)
@@ -1664,6 +1669,9 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaFree(s->d_work_band);
   for (int i = 0; i <= kHostBands; ++i) cudaFree(s->d_ho[i]);
   cudaFree(s->d_wf);
+  if (s->wf_stream) cudaStreamDestroy(s->wf_stream);
+  for (int i = 0; i < 2; ++i)
+    if (s->wf_ev[i]) cudaEventDestroy(s->wf_ev[i]);
   cudaFree(s->d_bvh);
   cudaFree(s->d_tri4);
   cudaFree(s->d_tri_map);
@@ -1918,39 +1926,60 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       const char* ch = getenv("DTS_WF_CHUNK");
       if (ch && atoll(ch) >= 1024) chunk = (uint64_t)atoll(ch);
       if (chunk > P.total) chunk = P.total;
+      // dts_render (slot 0) with more than one chunk: two halves, two streams
+      const bool overlap = slot == 0 && chunk < P.total;
+      const int halves = overlap ? 2 : 1;
       const size_t cap = (size_t)chunk + (size_t)gw * (kBlockWalk / 32) * kHoBlock;
-      if (s->ho_cap[slot] < cap) {
+      if (s->ho_cap[slot] < cap * halves) {
         cudaFree(s->d_ho[slot]);
         s->d_ho[slot] = nullptr;
         s->ho_cap[slot] = 0;
-        if (cudaMalloc(&s->d_ho[slot], cap * sizeof(HandOff)) != cudaSuccess)
+        if (cudaMalloc(&s->d_ho[slot], cap * halves * sizeof(HandOff)) != cudaSuccess)
           return fail(DTS_E_OOM, "cudaMalloc(hand-off buffer) failed");
-        s->ho_cap[slot] = cap;
+        s->ho_cap[slot] = cap * halves;
       }
-      if (!s->d_wf && cudaMalloc(&s->d_wf, 3 * (1 + kHostBands) * sizeof(unsigned long long)) != cudaSuccess)
+      if (!s->d_wf && cudaMalloc(&s->d_wf, 3 * (2 + kHostBands) * sizeof(unsigned long long)) != cudaSuccess)
         return fail(DTS_E_OOM, "cudaMalloc(two-stage counters) failed");
-      unsigned long long* wf = s->d_wf + 3 * slot;
+      cudaStream_t xs[2] = {st, st};
+      if (overlap) {
+        if (!s->wf_stream) {
+          CUDA_TRY(cudaStreamCreateWithFlags(&s->wf_stream, cudaStreamNonBlocking));
+          for (int i = 0; i < 2; ++i) CUDA_TRY(cudaEventCreateWithFlags(&s->wf_ev[i], cudaEventDisableTiming));
+        }
+        xs[1] = s->wf_stream;
+        CUDA_TRY(cudaEventRecord(s->wf_ev[0], st));  // fork: the aux stream starts after the caller's prior work
+        CUDA_TRY(cudaStreamWaitEvent(xs[1], s->wf_ev[0], 0));
+      }
       const uint64_t gc = std::min<uint64_t>(grid, (cap + 31) / 32 / (blk / 32) + 1);
+      CUDA_TRY(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
       int launches = 0;
-      for (uint64_t w0 = 0; w0 < P.total; w0 += chunk) {
+      int i = 0;
+      for (uint64_t w0 = 0; w0 < P.total; w0 += chunk, ++i) {
+        const int h = overlap ? (i & 1) : 0;
+        cudaStream_t xst = xs[h];
+        // counters: slot 0 uses pairs 0 and 1 (halves), slot k >= 1 uses pair k + 1
+        unsigned long long* wf = s->d_wf + 3 * (slot == 0 ? h : slot + 1);
         RenderParams PW = P;
         PW.w_base = w0;
         PW.total = std::min<uint64_t>(chunk, P.total - w0);
         PW.work = wf;
-        PW.ho = s->d_ho[slot];
+        PW.ho = s->d_ho[slot] + (size_t)h * cap;
         PW.ho_count = wf + 2;
         RenderParams PC = PW;
         PC.w_base = 0;
         PC.work = wf + 1;
-        CUDA_TRY(cudaMemsetAsync(wf, 0, 3 * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMemsetAsync(wf, 0, 3 * sizeof(unsigned long long), xst));
         void* aw[] = {&PW};
         CUDA_TRY(cudaLaunchKernel(kwalk, dim3((unsigned)std::min<uint64_t>(gw, (PW.total + kBlockWalk - 1) / kBlockWalk)),
-                                  dim3(kBlockWalk), aw, 0, st));
+                                  dim3(kBlockWalk), aw, 0, xst));
         void* ac[] = {&PC};
-        CUDA_TRY(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        CUDA_TRY(cudaLaunchKernel(kres, dim3((unsigned)gc), dim3(blk), ac, dyn, st));
+        CUDA_TRY(cudaLaunchKernel(kres, dim3((unsigned)gc), dim3(blk), ac, dyn, xst));
         CUDA_TRY(cudaGetLastError());
         launches += 2;
+      }
+      if (overlap) {  // join: the caller's stream waits for the aux stream's chunks
+        CUDA_TRY(cudaEventRecord(s->wf_ev[1], xs[1]));
+        CUDA_TRY(cudaStreamWaitEvent(st, s->wf_ev[1], 0));
       }
       g_last_launches = launches;
     }

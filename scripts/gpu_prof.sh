@@ -1,10 +1,17 @@
-# ncu --set full captures of the render kernel, config 5 at spp 16 and config 3 at spp 4 (tag = $1)
+# ncu evidence of a round (run through gpurun, one GPU): the launch list of the
+# default bench command (per-launch time + DRAM bytes), then `ncu --set full` of
+# the render kernels -- config 5 at spp 128 and config 3 at spp 4 (one chunk of
+# the two-stage render each: the walk kernel and the connect kernel).
 TAG=${1:-dev}
 mkdir -p gpurun_out
-for spec in "5 16" "3 4"; do
+CMD="python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-mse"
+$CMD > gpurun_out/plain_launch_${TAG}.log 2>&1 && \
+  timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file gpurun_out/launches_c5_${TAG}.csv $CMD > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "ncu-launch rc=$?"
+for spec in "5 128" "3 4"; do
   set -- $spec
-  PCMD="python bench.py --config $1 --spp $2 --steps 1 --warmup 3 --no-cpu-baseline"
-  $PCMD > gpurun_out/plain_prof_c$1.log 2>&1 && \
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_darts -s 3 -c 1 \
-      -o gpurun_out/prof_${TAG}_c$1 $PCMD > gpurun_out/ncu_full_c$1.log 2>&1; echo "ncu c$1 rc=$?"
+  PCMD="python bench.py --config $1 --spp $2 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-mse"
+  $PCMD > gpurun_out/plain_prof_c$1_${TAG}.log 2>&1 && \
+    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"walk_kernel|render_darts" -s 6 -c 2 \
+      -o gpurun_out/prof_${TAG}_c$1 $PCMD > gpurun_out/ncu_full_c$1_${TAG}.log 2>&1; echo "ncu c$1 rc=$?"
 done
