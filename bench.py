@@ -153,6 +153,10 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # communicator lines (rank count, NVLS / channels) for the driver, on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = I.as_f32(I.config(args.config, **({"ico_subdiv": args.mesh_subdiv} if args.config == 6 and
                                           args.mesh_subdiv is not None else {})))
@@ -219,8 +223,14 @@ def run_gpu(args):
     kms = [a.elapsed_time(b) for a, b in kern_ms]
     kern_avg = sum(kms) / len(kms)
     launch = dts.last_launch()
-    # max over ranks of the step time; sum of counters over ranks
+    # per-rank step and render times (the rest of a step is the table build and,
+    # at N > 1, the reduce); max over ranks of the step time; counters summed
+    per_rank = {"step_ms": [ms / args.steps], "render_ms": [kern_avg]}
     if world > 1:
+        mine = torch.tensor([ms / args.steps, kern_avg], dtype=torch.float64, device="cuda")
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = {"step_ms": [float(t[0]) for t in allr], "render_ms": [float(t[1]) for t in allr]}
         tt = torch.tensor([ms, kern_avg], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, kern_avg = float(tt[0]), float(tt[1])
@@ -284,6 +294,7 @@ def run_gpu(args):
                 "launches_per_step": launch.get("n_launches"),
             },
             "clocks": clocks,
+            "per_rank": per_rank,
             "e2e": e2e,
             # per step and rank: the table build + the render's launches (two-stage: 2 per chunk)
             "gpu_launches": (1 + launch.get("n_launches", 1)) * args.steps * world,
@@ -305,12 +316,14 @@ def run_gpu(args):
 
 
 def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts, step_ms=1e9):
+    from paper_2402_03106_b200.shard import pipeline_bands
     """Same metric through the public API with host buffers: per step the host
     scene description goes in (dts_scene_create + dts_table_build), the
     histogram comes back to pinned host memory."""
     cells = sc.hist_cells()
-    host = torch.empty(cells, dtype=torch.float32, pin_memory=True)
-    hnp = host.numpy()
+    # only rank 0 receives the histogram: only it pins a host buffer (4.2 GB for config 5)
+    host = torch.empty(cells, dtype=torch.float32, pin_memory=True) if rank == 0 else None
+    hnp = host.numpy() if host is not None else None
     hctr = np.zeros(dts.NUM_COUNTERS, np.uint64)
     spp = c["spp"]
     sb, se = _shard(spp, rank, world)
@@ -350,19 +363,22 @@ def run_e2e(args, c, sc, world, rank, stream, torch, dist, dts, step_ms=1e9):
             dev_hist.zero_()
             ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
             flat = dev_hist.view(-1)
-            for k in range(nbands):
-                r0, r1 = rows * k // nbands, rows * (k + 1) // nbands
-                band = flat[r0 * rowsz:r1 * rowsz]
+
+            def render_band(k, r0, r1, i=i, s2=s2, ctr=ctr):
+                s2.render_rows(spp, c["seed"] + 7 * i, sb, se, r0, r1, k % 4, flat[r0 * rowsz:r1 * rowsz], ctr, stream)
+
+            def reduce_band(k, r0, r1):
                 # every collective stays on the main stream, in the same order on every rank
-                s2.render_rows(spp, c["seed"] + 7 * i, sb, se, r0, r1, k % 4, band, ctr, stream)
-                if world > 1:
-                    dist.reduce(band, dst=0)
-                if rank == 0:
-                    ev = torch.cuda.Event()
-                    ev.record(stream)
-                    copy_stream.wait_event(ev)
-                    with torch.cuda.stream(copy_stream):
-                        host[r0 * rowsz:r1 * rowsz].copy_(band, non_blocking=True)
+                dist.reduce(flat[r0 * rowsz:r1 * rowsz], dst=0)
+
+            def copy_band(k, r0, r1):
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                copy_stream.wait_event(ev)
+                with torch.cuda.stream(copy_stream):
+                    host[r0 * rowsz:r1 * rowsz].copy_(flat[r0 * rowsz:r1 * rowsz], non_blocking=True)
+
+            pipeline_bands(rows, nbands, render_band, reduce_band, copy_band, world, rank)
             if world > 1:
                 dist.all_reduce(ctr)
             torch.cuda.synchronize()

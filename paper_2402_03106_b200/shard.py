@@ -40,6 +40,30 @@ def render_sharded(render_range: Callable[[int, int], None], spp: int, hist, cou
     return b, e
 
 
+def band_rows(rows: int, nbands: int) -> list[tuple[int, int]]:
+    """Row bands [r0, r1) of a crop of ``rows`` rows: contiguous, covering, sizes within one."""
+    if nbands < 1 or rows < nbands:
+        raise ValueError(f"need 1 <= nbands <= rows, got {nbands} bands of {rows} rows")
+    return [(rows * k // nbands, rows * (k + 1) // nbands) for k in range(nbands)]
+
+
+def pipeline_bands(rows: int, nbands: int, render_rows: Callable[[int, int, int], None],
+                   reduce_band: Callable[[int, int, int], None], to_host: Callable[[int, int, int], None],
+                   world: int, rank: int, dst: int = 0) -> None:
+    """The end-to-end pipeline of a large histogram at N ranks:
+    band by band, every rank renders its sample range of the band
+    (``render_rows(k, r0, r1)``), the band is reduced onto rank ``dst``
+    (``reduce_band``: a collective, issued in the same band order on every rank),
+    and rank ``dst`` starts the band's copy to the host (``to_host``, e.g. on a
+    copy stream) while the next band renders.  No arithmetic of the method here."""
+    for k, (r0, r1) in enumerate(band_rows(rows, nbands)):
+        render_rows(k, r0, r1)
+        if world > 1:
+            reduce_band(k, r0, r1)
+        if rank == dst:
+            to_host(k, r0, r1)
+
+
 _PEER_CACHE: dict = {}
 
 
