@@ -401,6 +401,46 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   return true;
 }
 
+// ---------------------------------------------------------------- persistent work distribution
+// Hands the lanes of `need` (warp-uniform mask) consecutive work items from the
+// warp's private queue [wn, we), refilled with kChunk items from the global
+// counter `work` (one atomicAdd per chunk); returns this lane's item, ~0 if it
+// gets none (then `exhausted` is set: the global range is used up).
+__device__ __forceinline__ uint64_t take_work(unsigned need, int lane, unsigned lt_mask, uint64_t& wn, uint64_t& we,
+                                              bool& exhausted, unsigned long long* work, uint64_t ntotal) {
+  const uint32_t nidle = __popc(need);
+  const uint32_t rank = __popc(need & lt_mask);
+  const uint64_t avail = we - wn;
+  uint64_t my = ~0ull;
+  if (avail >= nidle) {
+    my = wn + rank;
+    wn += nidle;
+  } else {
+    unsigned long long nb = 0;
+    if (lane == 0) nb = atomicAdd(work, (unsigned long long)kChunk);
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+    uint64_t ne = nb + kChunk < ntotal ? nb + kChunk : ntotal;
+    if (nb >= ntotal) {
+      exhausted = true;
+      ne = nb;
+    }
+    if (rank < avail) {
+      my = wn + rank;
+    } else {
+      const uint64_t cand = nb + (rank - avail);
+      my = cand < ne ? cand : ~0ull;
+    }
+    const uint64_t nq = nb + (nidle - avail);
+    wn = nq < ne ? nq : ne;
+    we = ne;
+  }
+  return ((need >> lane) & 1u) ? my : ~0ull;
+}
+#ifndef DTS_START_TRIES
+#define DTS_START_TRIES 8
+#endif
+constexpr int kStartTries = DTS_START_TRIES;  // start attempts per refill for a lane whose path retires at its start
+
 // ---------------------------------------------------------------- TMA 1-D bulk staging
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -733,36 +773,19 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     waste += __popc(idle);
     if (idle && !exhausted && (waste >= P.refill_k || idle == FULL)) {
       waste = 0;
-      const uint32_t nidle = __popc(idle);
-      const uint32_t rank = __popc(idle & lt_mask);
-      const uint64_t avail = we - wn;
-      uint64_t my = ~0ull;
-      if (avail >= nidle) {
-        my = wn + rank;
-        wn += nidle;
-      } else {
-        unsigned long long nb = 0;
-        if (lane == 0) nb = atomicAdd(P.work, (unsigned long long)kChunk);
-        nb = __shfl_sync(FULL, nb, 0);
-        uint64_t ne = nb + kChunk < ntotal ? nb + kChunk : ntotal;
-        if (nb >= ntotal) {
-          exhausted = true;
-          ne = nb;
-        }
-        if (rank < avail) {
-          my = wn + rank;
-        } else {
-          const uint64_t cand = nb + (rank - avail);
-          my = cand < ne ? cand : ~0ull;
-        }
-        const uint64_t nq = nb + (nidle - avail);
-        wn = nq < ne ? nq : ne;
-        we = ne;
+      // a lane whose new path retires at its start (camera miss, early exit, an
+      // empty hand-off slot) takes the next one in the same refill: refilled
+      // lanes enter the vertex loop with a live path (configs 2 and 4 miss the
+      // medium with 60 % / 35 % of their primary rays)
+      unsigned need = idle;
+      for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
+        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal);
+        const bool starts = my != ~0ull && my < ntotal;
+        const unsigned sm = __ballot_sync(FULL, starts);
+        if (!RESUME && lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
+        if (starts) active = RESUME ? load_handoff(P, my, pc) : start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
+        need = __ballot_sync(FULL, ((need >> lane) & 1u) && !active);
       }
-      const bool starts = !active && my != ~0ull && my < ntotal;
-      const unsigned sm = __ballot_sync(FULL, starts);
-      if (!RESUME && lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
-      if (starts) active = RESUME ? load_handoff(P, my, pc) : start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
     }
     const unsigned act = __ballot_sync(FULL, active);
     // queue batches; once the work is exhausted and every lane idle, drain them
@@ -914,38 +937,17 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
     waste += __popc(idle);
     if (idle && !exhausted && (waste >= P.refill_k || idle == FULL)) {
       waste = 0;
-      const uint32_t nidle = __popc(idle);
-      const uint32_t rank = __popc(idle & lt_mask);
-      const uint64_t avail = we - wn;
-      uint64_t my = ~0ull;
-      if (avail >= nidle) {
-        my = wn + rank;
-        wn += nidle;
-      } else {
-        unsigned long long nb = 0;
-        if (lane == 0) nb = atomicAdd(P.work, (unsigned long long)kChunk);
-        nb = __shfl_sync(FULL, nb, 0);
-        uint64_t ne = nb + kChunk < P.total ? nb + kChunk : P.total;
-        if (nb >= P.total) {
-          exhausted = true;
-          ne = nb;
+      unsigned need = idle;  // (retry paths that retire at their start, as in render_darts_kernel)
+      for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
+        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, P.total);
+        const bool starts = my != ~0ull && my < P.total;
+        const unsigned sm = __ballot_sync(FULL, starts);
+        if (lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
+        if (starts) {
+          active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
+          margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
         }
-        if (rank < avail) {
-          my = wn + rank;
-        } else {
-          const uint64_t cand = nb + (rank - avail);
-          my = cand < ne ? cand : ~0ull;
-        }
-        const uint64_t nq = nb + (nidle - avail);
-        wn = nq < ne ? nq : ne;
-        we = ne;
-      }
-      const bool starts = !active && my != ~0ull && my < P.total;
-      const unsigned sm = __ballot_sync(FULL, starts);
-      if (lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
-      if (starts) {
-        active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
-        margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
+        need = __ballot_sync(FULL, ((need >> lane) & 1u) && !active);
       }
     }
     const unsigned act = __ballot_sync(FULL, active);

@@ -218,3 +218,36 @@ def test_box_wall_single_bounce_quadrature(oracle, strategy):
     assert ref.sum() > 0 and (ref > 0).sum() >= 20
     assert ok.mean() >= 0.95, np.c_[m, ref, se]
     assert m.sum() == pytest.approx(ref.sum(), rel=0.02)
+
+
+# ---------------------------------------------------------------- config 5: DARTS == vanilla at a mid window
+def test_cfg5_darts_equals_vanilla_mid_window(oracle):
+    """PAPER.md:340 ("verified to converge to the same results") at config 5's
+    mid window t in [40, 50): DARTS (RIS distance, EDA + HG in SPLIT mode,
+    elliptical connections) and the vanilla estimator on a 2 x 2-pixel crop,
+    5 bins of 2 time units.  Per-path contributions are heavy-tailed there (a
+    cell's effective sample size n_eff = (sum x)^2 / sum x^2 is ~2 per 2000
+    DARTS paths), so the comparison pools: the window total and each bin summed
+    over the 4 pixels, at 20 000 DARTS paths per cell and 200 000 vanilla paths
+    per pixel, each within 3 SE, with n_eff reported."""
+    c = I.small(I.config(5, parity_s_excess=0.05, spp_mode="cell"), 2, 2, n_bins=5, t1=50.0)
+    c["t0"] = 40.0
+    c = I.as_f32(c)
+    q, _ = oracle.build_table(c)
+    nd, nv = 20000, 200000
+    d = oracle.render(c, q, nd, 51)
+    v = oracle.render(dict(c, strategy="vanilla"), None, nv, 52)
+    # per-cell variances of the cell means, pooled by summation (independent cells)
+    vd = np.maximum(d["hist_sq"] - d["hist"] ** 2, 0) / (nd - 1)
+    vv = np.maximum(v["hist_sq"] - v["hist"] ** 2, 0) / (nv - 1)
+    hd, hv = d["hist"].sum(axis=(0, 1)), v["hist"].sum(axis=(0, 1))
+    sd, sv = vd.sum(axis=(0, 1)), vv.sum(axis=(0, 1))
+    z_bins = (hd - hv) / np.sqrt(sd + sv)
+    z_tot = (hd.sum() - hv.sum()) / math.sqrt(sd.sum() + sv.sum())
+    neff_d = float(np.mean(nd * d["hist"] ** 2 / np.maximum(d["hist_sq"], 1e-300)))
+    neff_v = float(np.mean(nv * v["hist"] ** 2 / np.maximum(v["hist_sq"], 1e-300)))
+    print(f"cfg5 [40,50): DARTS {hd.sum():.4e} vanilla {hv.sum():.4e}, z total {z_tot:+.2f}, z bins {np.round(z_bins, 2)}; "
+          f"mean n_eff per cell DARTS {neff_d:.1f} vanilla {neff_v:.1f}")
+    assert hd.sum() > 0 and hv.sum() > 0
+    assert abs(z_tot) < 3
+    assert (np.abs(z_bins) < 3).all()
