@@ -166,6 +166,8 @@ def run_gpu(args):
         c["strategy"] = args.strategy
     if args.spp:
         c["spp"] = args.spp
+    if args.crop:
+        c = I.crop_center(c, min(args.crop, c["width"]), min(args.crop, c["height"]))
     spp = c["spp"]
     sb, se = _shard(spp, rank, world)
     sc = dts.Scene(c)
@@ -253,7 +255,7 @@ def run_gpu(args):
         # per-rank algorithmic instructions / their CUDA-event time on the stream
         achieved = (verts_per_step / world) * alg / (kern_avg * 1e-3) / 1e12
         value = verts_per_step / (ms / args.steps * 1e-3)
-        traffic = None if (args.spp or args.strategy or args.direction_mode) else _profile_traffic(args.config)
+        traffic = None if (args.spp or args.crop or args.strategy or args.direction_mode) else _profile_traffic(args.config)
         clocks = clk.summary()
         line = {
             "metric": METRIC,
@@ -570,6 +572,7 @@ def main():
     ap.add_argument("--mse-crop", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--spp", type=int, default=None, help="override spp (profiling runs only; not a bench line)")
+    ap.add_argument("--crop", type=int, default=None, help="centre crop W x W (profiling runs only; not a bench line)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

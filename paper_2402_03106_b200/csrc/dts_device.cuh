@@ -803,11 +803,13 @@ __device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_
 // Returns true if the walk continues.  contrib receives the vertex's
 // connection (+ wall NEE) contribution; end_reason the DTS_CTR_* of a stop.
 // WALK (the walk stage of the two-stage render, SPLIT scenes): a vertex whose
-// connection provably cannot land in its bin (conn_bound) runs only the walk:
-// the mixture direction, the connection's intersection and S range, and the
-// wall NEE are skipped -- they would contribute exactly 0 -- and the walk's
+// connection provably cannot land in its bin (conn_margin > 0) runs only the
+// walk: the mixture direction, the connection's intersection and S range, and
+// the wall NEE are skipped -- they would contribute exactly 0 -- and the walk's
 // random numbers, directions and distances are the full vertex's, bit for bit.
-// *walk_step receives the distance moved.
+// *walk_step carries the margin in and its lower bound after the step out
+// (margin - (1 + counts) d: see walk_kernel); while it stays positive the early
+// exit test is skipped (R_M - E - C >= R_m - E - S_max > 0).
 template <bool DBG, bool SMEM, int SH, int FL, bool DEFER = false, bool WALK = false>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
@@ -1140,7 +1142,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     ps.beta *= S.albedo;
     ps.x = fma3(ww, d, ps.x);
     ps.resM -= f2d(counts * d);
-    if (WALK) *walk_step = d;
+    if (WALK) *walk_step -= (1.0f + counts) * d * 1.00001f;
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
     if (DBG) { dbg->event = 1; dbg->istar = 0; dbg->d = d; dbg->beta_ris = S.albedo; }
@@ -1224,19 +1226,19 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     }
     // resample: smallest i with sum_{j<=i} w_j > u3 W (CDF inversion in candidate order)
     const float thr = unif(r[3]) * W;
-    // the partial sums are monotone, so candidate i is taken iff it is the
-    // first whose partial sum exceeds thr
-    float cum = 0.0f, wsel = e2[7];
-    uint32_t is = 7;
-    bool gt_prev = false;
+    // the partial sums are monotone: scanning them from the last to the first,
+    // the last one found above thr is the first in candidate order
+    float cum[7];
+    cum[0] = e2[0];
 #pragma unroll
-    for (int i = 0; i < 7; ++i) {
-      cum += e2[i];
-      const bool gt = cum > thr;
-      const bool take = gt && !gt_prev;
-      wsel = take ? e2[i] : wsel;
-      is = take ? (uint32_t)i : is;
-      gt_prev = gt;
+    for (int i = 1; i < 7; ++i) cum[i] = cum[i - 1] + e2[i];
+    float wsel = e2[7];
+    uint32_t is = 7;
+#pragma unroll
+    for (int i = 6; i >= 0; --i) {
+      const bool gt = cum[i] > thr;
+      wsel = gt ? e2[i] : wsel;
+      is = gt ? (uint32_t)i : is;
     }
     // regenerate the selected candidate's distance (cheaper than keeping all 8)
     const uint32_t brs = __brev(is) >> 29;
@@ -1249,7 +1251,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     ps.resM -= f2d(counts * dsel);
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
-    if (WALK) *walk_step = dsel;
+    if (WALK) *walk_step -= (1.0f + counts) * dsel * 1.00001f;
     if (DBG) { dbg->event = 1; dbg->istar = (int)is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
   } else {
     if (WALLS && hit == HIT_WALL) {
@@ -1260,7 +1262,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       ps.x = xn;
       ps.resM -= f2d(counts * hi);
       ps.kind = KIND_WALL;
-      if (WALK) *walk_step = hi;
+      if (WALK) *walk_step -= (1.0f + counts) * hi * 1.00001f;
       ps.face = face;
       ps.w = ww;
       if (DBG) { dbg->event = 2; dbg->d = hi; dbg->beta_ris = 1.0f; }
@@ -1283,6 +1285,15 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   if (DBG) {
     dbg->x_next[0] = ps.x.x; dbg->x_next[1] = ps.x.y; dbg->x_next[2] = ps.x.z;
     dbg->beta_out = ps.beta;
+  }
+  if (WALK && *walk_step > 0.0f) {
+    // walk stage: the connection margin still bounds R_M - E - C from below, so
+    // the early exit provably does not fire; only the non-finite test remains
+    if (!isfinite(ps.beta)) {
+      end_reason = DTS_CTR_NONFINITE;
+      return false;
+    }
+    return true;
   }
   const bool alive = vertex_tail(ps, xe, end_reason);
   if (DBG && !alive) dbg->terminate = 1;

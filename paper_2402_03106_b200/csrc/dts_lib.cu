@@ -927,11 +927,11 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   uint64_t wn = 0, we = 0;   // warp-uniform work queue [wn, we)
-  uint64_t hn = 0, he = 0;   // warp-uniform reserved hand-off slots [hn, he)
+  uint32_t hn = 0, he = 0;   // warp-uniform reserved hand-off slots [hn, he) (a chunk holds < 2^31)
   bool exhausted = false, active = false;
   PathCtx pc;
   float margin = 0.0f;
-  uint32_t c_vert = 0, c_walkm = 0, c_wall = 0, waste = 0;
+  uint32_t c_vert = 0, c_camw = 0, c_wall = 0, waste = 0;
   while (true) {
     const unsigned idle = __ballot_sync(FULL, !active);
     waste += __popc(idle);
@@ -946,6 +946,7 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
         if (starts) {
           active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
           margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
+          c_camw += (active && margin > 0.0f) ? 1u : 0u;  // its camera vertex runs in the walk stage
         }
         need = __ballot_sync(FULL, ((need >> lane) & 1u) && !active);
       }
@@ -964,53 +965,51 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
       const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
       const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
       const uint32_t r[8] = {a.a, a.b, a.c, a.d, b.a, b.b, b.c, b.d};
-      const float counts = (S.warped || pc.ps.kind != KIND_CAMERA) ? 1.0f : 0.0f;
-      if (pc.ps.kind == KIND_CAMERA) atomicAdd(s_ctr + DTS_CTR_CAMERA_VERTICES, 1u);
-      c_walkm += pc.ps.kind == KIND_MEDIUM ? 1u : 0u;
-      c_wall += pc.ps.kind == KIND_WALL ? 1u : 0u;
-      float contrib = 0.0f, step = 0.0f;
+      if (FL & FL_WALLS) c_wall += pc.ps.kind == KIND_WALL ? 1u : 0u;
+      float contrib = 0.0f;
       bool cn = false, wnee = false;
       int reason = 0;
       const bool alive = darts_vertex<false, false, SH, FL, false, true>(S, nullptr, pc.ps, r, contrib, nullptr, cn,
                                                                          wnee, reason, nullptr, nullptr, nullptr,
-                                                                         nullptr, nullptr, &step);
+                                                                         nullptr, nullptr, &margin);
       ++pc.k;
       ++c_vert;
       const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
       done = !alive || cap;
       if (done) atomicAdd(s_ctr + (cap ? (int)DTS_CTR_CAP_HITS : reason), 1u);
-      margin -= (1.0f + counts) * step * 1.00001f;
     }
     const unsigned hm = __ballot_sync(FULL, hand);
     if (hm) {
       const uint32_t nh = __popc(hm), rank = __popc(hm & lt_mask);
-      const uint64_t avail = he - hn;
-      uint64_t slot;
+      const uint32_t avail = he - hn;
+      uint32_t slot;
       if (avail >= nh) {
         slot = hn + rank;
         hn += nh;
       } else {
         unsigned long long nb = 0;
         if (lane == 0) nb = atomicAdd(P.ho_count, (unsigned long long)kHoBlock);
-        nb = __shfl_sync(FULL, nb, 0);
-        slot = rank < avail ? hn + rank : nb + (rank - avail);
-        hn = nb + (nh - avail);
-        he = nb + kHoBlock;
+        const uint32_t nb32 = (uint32_t)__shfl_sync(FULL, nb, 0);
+        slot = rank < avail ? hn + rank : nb32 + (rank - avail);
+        hn = nb32 + (nh - avail);
+        he = nb32 + kHoBlock;
       }
       if (hand) store_handoff(P.ho + slot, pc);
     }
     if (hand || done) active = false;
   }
   // this warp's unused reserved slots are marked empty for the connect stage
-  if ((uint64_t)lane < he - hn) reinterpret_cast<uint4*>(P.ho + hn + lane)[1].w = kHoEmpty;
+  if ((uint32_t)lane < he - hn) reinterpret_cast<uint4*>(P.ho + hn + lane)[1].w = kHoEmpty;
   for (int o = 16; o > 0; o >>= 1) {
     c_vert += __shfl_xor_sync(FULL, c_vert, o);
-    c_walkm += __shfl_xor_sync(FULL, c_walkm, o);
+    c_camw += __shfl_xor_sync(FULL, c_camw, o);
     c_wall += __shfl_xor_sync(FULL, c_wall, o);
   }
   if (lane == 0 && P.counters) {
     atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
-    atomicAdd(P.counters + DTS_CTR_WALK_VERTICES, (unsigned long long)c_walkm);
+    // walk-only medium vertices: every walk-stage vertex but the camera and wall ones
+    atomicAdd(P.counters + DTS_CTR_WALK_VERTICES, (unsigned long long)(c_vert - c_camw - c_wall));
+    if (c_camw) atomicAdd(P.counters + DTS_CTR_CAMERA_VERTICES, (unsigned long long)c_camw);
     if (c_wall) atomicAdd(P.counters + DTS_CTR_WALL_VERTICES, (unsigned long long)c_wall);
   }
   __syncthreads();
@@ -1926,7 +1925,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       // paths per chunk: the hand-off buffer holds one chunk (64 B per path)
       uint64_t chunk = (uint64_t)1 << 27;
       const char* ch = getenv("DTS_WF_CHUNK");
-      if (ch && atoll(ch) >= 1024) chunk = (uint64_t)atoll(ch);
+      if (ch && atoll(ch) >= 1024) chunk = std::min<uint64_t>((uint64_t)atoll(ch), (uint64_t)1 << 31);
       if (chunk > P.total) chunk = P.total;
       // dts_render (slot 0) with more than one chunk: two halves, two streams
       const bool overlap = slot == 0 && chunk < P.total;

@@ -14,7 +14,7 @@ if [ "${LAUNCH:-0}" = "1" ]; then
 fi
 for spec in "$@"; do
   set -- $spec
-  PCMD="python bench.py --config $1 --spp $2 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-mse"
+  PCMD="python bench.py --config $1 --spp $2 ${CROP:+--crop $CROP} --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-mse"
   $PCMD > gpurun_out/plain_prof_c$1_${TAG}.log 2>&1 && \
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"walk_kernel|render_darts" -s 6 -c 2 \
       -o gpurun_out/prof_${TAG}_c$1 $PCMD > gpurun_out/ncu_full_c$1_${TAG}.log 2>&1; echo "ncu c$1 rc=$?"

@@ -1,14 +1,20 @@
 #!/usr/bin/env python
 """Per-source-region instruction accounting of an ncu --set full capture
 (`ncu -i REP --page source --csv --print-source cuda,sass`): warp-instructions
-per vertex and SIMT efficiency by source line / region of darts_vertex."""
+per vertex and SIMT efficiency by source line / region of darts_vertex.
+
+    python scripts/ncu_lines.py REP VERTICES [kernel=REGEX] [name:file:lo:hi ...]"""
 import collections
 import csv
 import subprocess
 import sys
 
 rep, verts = sys.argv[1], float(sys.argv[2])
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kern = []
+if len(sys.argv) > 3 and sys.argv[3].startswith("kernel="):   # e.g. kernel=walk_kernel (a regex)
+    kern = ["-k", "regex:" + sys.argv[3].split("=", 1)[1]]
+    del sys.argv[3]
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", *kern],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 cur = None
