@@ -437,9 +437,11 @@ __device__ __forceinline__ uint64_t take_work(unsigned need, int lane, unsigned 
   return ((need >> lane) & 1u) ? my : ~0ull;
 }
 #ifndef DTS_START_TRIES
-#define DTS_START_TRIES 8
+#define DTS_START_TRIES 1
 #endif
-constexpr int kStartTries = DTS_START_TRIES;  // start attempts per refill for a lane whose path retires at its start
+// start attempts per refill for a lane whose path retires at its start: 1 (A/B,
+// profiles/ab_r02_start_tries.log: 8 tries cost 0.5-5 % on configs 1, 2, 4, 6)
+constexpr int kStartTries = DTS_START_TRIES;
 
 // ---------------------------------------------------------------- TMA 1-D bulk staging
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -773,10 +775,9 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     waste += __popc(idle);
     if (idle && !exhausted && (waste >= P.refill_k || idle == FULL)) {
       waste = 0;
-      // a lane whose new path retires at its start (camera miss, early exit, an
-      // empty hand-off slot) takes the next one in the same refill: refilled
-      // lanes enter the vertex loop with a live path (configs 2 and 4 miss the
-      // medium with 60 % / 35 % of their primary rays)
+      // (kStartTries > 1: a lane whose new path retires at its start -- camera
+      // miss, early exit, empty hand-off slot -- takes the next one in the same
+      // refill; measured slower, off by default)
       unsigned need = idle;
       for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
         const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal);
