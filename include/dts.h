@@ -154,7 +154,8 @@ typedef struct {
  * is returned with terminate = 1 and nothing else set).
  * u_i = (r_i >> 9) * 2^-23 (R24): u0 event, u1 Sobol row, u2 CP shift, u3 RIS
  * select, u4 technique, u5 cos/bin, u6 phi, u7 connection; the SPLIT walk's
- * u8/u9 come from the low bits of r0..r2 / r3..r5; r8..r11 are reserved. */
+ * u8 = bits 0..22 of r1 and u9 = bits 0..8 of r0 | 0..8 of r2 | 0..4 of r3
+ * (23-bit fractions); r8..r11 are reserved. */
 typedef struct {
   int32_t kind, face, bin, emitter;
   float x[3], w[3];

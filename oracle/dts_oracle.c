@@ -507,12 +507,15 @@ typedef struct {
 
 static double uu(const uint32_t r[12], int i) { return or_uniform(r[i]); }
 
-/* R24, SPLIT walk direction: u8 and u9 are the 23-bit integers formed by the
- * low bits (left unused by u0..u7) of r0, r1, r2 and of r3, r4, r5:
- * (r_a & 0x7F) << 16 | (r_b & 0xFF) << 8 | (r_c & 0xFF). */
+/* R24, SPLIT walk direction: u8 and u9 are 23-bit integers made of bits of the
+ * first Philox block that u0..u3 leave unused (u0, u2, u3 take the top 23 bits
+ * of r0, r2, r3; the Sobol row of u1 only the top 5 bits of r1):
+ *   u8: bits 0..22 of r1;
+ *   u9: bits 0..8 of r0, then bits 0..8 of r2, then bits 0..4 of r3
+ *       ((r0 & 0x1FF) << 14 | (r2 & 0x1FF) << 5 | (r3 & 0x1F)). */
 static double u_split(const uint32_t r[12], int which) {
-  const uint32_t* a = r + 3 * which;
-  uint32_t m = ((a[0] & 0x7Fu) << 16) | ((a[1] & 0xFFu) << 8) | (a[2] & 0xFFu);
+  uint32_t m = which == 0 ? (r[1] & 0x7FFFFFu)
+                          : (((r[0] & 0x1FFu) << 14) | ((r[2] & 0x1FFu) << 5) | (r[3] & 0x1Fu));
   return (double)m * (1.0 / 8388608.0);
 }
 

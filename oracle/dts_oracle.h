@@ -85,7 +85,7 @@ typedef struct {
   int32_t kind, face, bin, emitter;
   double x[3], w[3];
   double E, beta;
-  uint32_t r[12]; /* raw Philox words: u_i = (r_i >> 9) * 2^-23; SPLIT u8/u9 from the low bits of r0..r5; r8..r11 reserved (R24) */
+  uint32_t r[12]; /* raw Philox words: u_i = (r_i >> 9) * 2^-23; SPLIT u8/u9 from the low bits of r0..r3; r8..r11 reserved (R24) */
 } or_debug_in;
 
 typedef struct {

@@ -495,10 +495,14 @@ __device__ __forceinline__ uint32_t gload(const uint8_t* g, int i) {
   return __ldg(g + i);
 }
 
-// R24: the SPLIT walk direction uses u8, u9 = the 23-bit integers formed by the
-// low bits (unused by u0..u7) of r0, r1, r2 and of r3, r4, r5.
-__device__ __forceinline__ float u_split(uint32_t a, uint32_t b, uint32_t c) {
-  return mant01(((a & 0x7Fu) << 16) | ((b & 0xFFu) << 8) | (c & 0xFFu));
+// R24: the SPLIT walk direction uses u8, u9, made of bits of the first Philox
+// block that u0..u3 leave unused (u0, u2, u3: top 23 bits of r0, r2, r3; the
+// Sobol row of u1: top 5 bits of r1): u8 = bits 0..22 of r1; u9 = bits 0..8 of
+// r0 | bits 0..8 of r2 | bits 0..4 of r3.  So a walk-only vertex (two-stage
+// render) needs one Philox call.
+__device__ __forceinline__ float u8_split(const uint32_t (&r)[8]) { return mant01(r[1] & 0x7FFFFFu); }
+__device__ __forceinline__ float u9_split(const uint32_t (&r)[8]) {
+  return mant01(((r[0] & 0x1FFu) << 14) | ((r[2] & 0x1FFu) << 5) | (r[3] & 0x1Fu));
 }
 
 // ----------------------------------------------------------------- elliptical connection (E20-E22)
@@ -935,8 +939,8 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       // R29 SPLIT, connection queued (or unreachable): only the walk's
       // independent HG direction is drawn here
       float o2, m2;
-      hg_sample(S, u_split(r[0], r[1], r[2]), o2, m2);
-      wc = ww = from_frame(ps.w, o2, m2, kPi * (2.0f * u_split(r[3], r[4], r[5]) - 1.0f));
+      hg_sample(S, u8_split(r), o2, m2);
+      wc = ww = from_frame(ps.w, o2, m2, kPi * (2.0f * u9_split(r) - 1.0f));
     } else {
     const MixDir md = mix_direction<SMEM, !(SPLIT && kStage1Build)>(S, tab, ps.x, ps.w, resM, xe, r[4], r[5], r[6]);
     const f3 om = md.om;
@@ -948,8 +952,8 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       // R29 SPLIT: MIS weight on the connection only; independent HG walk direction
       wconn = ratio_w;
       float o2, m2;
-      hg_sample(S, u_split(r[0], r[1], r[2]), o2, m2);
-      ww = from_frame(ps.w, o2, m2, kPi * (2.0f * u_split(r[3], r[4], r[5]) - 1.0f));
+      hg_sample(S, u8_split(r), o2, m2);
+      ww = from_frame(ps.w, o2, m2, kPi * (2.0f * u9_split(r) - 1.0f));
       if (DBG) dbg->beta_dir = 1.0f;
     } else {
       ww = om;

@@ -231,6 +231,7 @@ struct RenderParams {
   uint32_t one_cell_warps;        // 1: per-cell order with >= 32 samples per cell (splat fast path)
   uint32_t div32;                 // 1: work indices, sample indices + B fit 32 bits (fast divisions)
   uint32_t cells;                 // histogram cells of this launch (< 2^32; bounds checks of the check build)
+  uint32_t van_rows;              // vanilla: 1 = pixel-major batches splat into per-warp shared-memory rows
   uint64_t w_base;                // first work index of this launch (two-stage render: the chunk's)
   struct HandOff* ho;             // two-stage render: the chunk's hand-off records
   unsigned long long* ho_count;   // two-stage render: hand-off slots allocated (the connect stage's work count)
@@ -917,6 +918,10 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
 #define DTS_BLOCK_WALK 896
 #endif
 constexpr int kBlockWalk = DTS_BLOCK_WALK;
+#ifndef DTS_WALK_INNER
+#define DTS_WALK_INNER 4
+#endif
+constexpr int kWalkInner = DTS_WALK_INNER;
 template <int SH, int FL>
 __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams P) {
   static_assert((FL & FL_SPLIT) && !(FL & FL_MESH), "walk stage: SPLIT scenes without meshes");
@@ -958,26 +963,35 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
       continue;
     }
     bool hand = false, done = false;
-    if (active) {
-      if (margin <= 0.0f) margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
-      hand = margin <= 0.0f;
-    }
-    if (active && !hand) {
-      const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
-      const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
-      const uint32_t r[8] = {a.a, a.b, a.c, a.d, b.a, b.b, b.c, b.d};
-      if (FL & FL_WALLS) c_wall += pc.ps.kind == KIND_WALL ? 1u : 0u;
-      float contrib = 0.0f;
-      bool cn = false, wnee = false;
-      int reason = 0;
-      const bool alive = darts_vertex<false, false, SH, FL, false, true>(S, nullptr, pc.ps, r, contrib, nullptr, cn,
-                                                                         wnee, reason, nullptr, nullptr, nullptr,
-                                                                         nullptr, nullptr, &margin);
-      ++pc.k;
-      ++c_vert;
-      const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
-      done = !alive || cap;
-      if (done) atomicAdd(s_ctr + (cap ? (int)DTS_CTR_CAP_HITS : reason), 1u);
+    // kWalkInner vertices per lane between refills and hand-offs (the warp's
+    // refill / hand-off bookkeeping is paid once per kWalkInner vertices; a lane
+    // that stops in an earlier one waits; walk phases last ~10^2 vertices)
+    for (int rep = 0; rep < kWalkInner; ++rep) {
+      if (rep > 0 && !__any_sync(FULL, active && !hand && !done)) break;
+      if (active && !hand && !done) {
+        if (margin <= 0.0f) margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
+        hand = margin <= 0.0f;
+      }
+      if (active && !hand && !done) {
+        // a walk-only vertex reads u0..u3 and the SPLIT walk's u8, u9, all from
+        // the first Philox block (R24); only a wall's cosine bounce needs u5, u6
+        const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
+        u4 b = u4{0u, 0u, 0u, 0u};
+        if (FL & FL_WALLS) b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
+        const uint32_t r[8] = {a.a, a.b, a.c, a.d, b.a, b.b, b.c, b.d};
+        if (FL & FL_WALLS) c_wall += pc.ps.kind == KIND_WALL ? 1u : 0u;
+        float contrib = 0.0f;
+        bool cn = false, wnee = false;
+        int reason = 0;
+        const bool alive = darts_vertex<false, false, SH, FL, false, true>(S, nullptr, pc.ps, r, contrib, nullptr, cn,
+                                                                           wnee, reason, nullptr, nullptr, nullptr,
+                                                                           nullptr, nullptr, &margin);
+        ++pc.k;
+        ++c_vert;
+        const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
+        done = !alive || cap;
+        if (done) atomicAdd(s_ctr + (cap ? (int)DTS_CTR_CAP_HITS : reason), 1u);
+      }
     }
     const unsigned hm = __ballot_sync(FULL, hand);
     if (hm) {
@@ -1022,192 +1036,252 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
 // splats a vanilla connection into the bin of its arrival time, weighted by
 // the sensor response W there (RESPONSE scenes); returns 1 for a path sample
 // rejected by W = 0 (outside the bins, or a zero of W), 0 if splatted
-__device__ __forceinline__ int vanilla_splat(const RenderParams& P, uint32_t pl, double arrive, float c) {
+// splats a vanilla connection into the bin of its arrival time, weighted by
+// the sensor response W there (RESPONSE scenes); returns 1 for a path sample
+// rejected by W = 0 (outside the bins, or a zero of W), 0 if splatted.  row:
+// the warp's shared-memory copy of this pixel's histogram row (privatised
+// launches), else null (RED to the histogram in global memory)
+__device__ __forceinline__ int vanilla_splat(const RenderParams& P, uint32_t pl, double arrive, float c, float* row) {
   const DevScene& S = P.S;
   const int bin = arrive >= S.t0 ? (int)floor((arrive - S.t0) / S.dt) : -1;
   if (bin < 0 || bin >= S.n_bins) return 1;
   DTS_CHECK((size_t)pl * S.n_bins + bin < P.cells);
   const float w = P.resp_w ? __ldg(P.resp_w + bin) : 1.0f;
   if (w == 0.0f) return 1;
-  atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, __fdividef(w * c, (float)P.spp));
+  const float v = __fdividef(w * c, (float)P.spp);
+  if (row) atomicAdd(row + bin, v);
+  else atomicAdd(P.hist + (size_t)pl * S.n_bins + bin, v);
   return 0;
 }
 
+struct VanCtr {
+  uint32_t paths = 0, miss = 0, vert = 0, early = 0, esc = 0, cap = 0, samp = 0, rej = 0;
+};
+
+// One vanilla path: work item (pixel pl of the crop, sample s).
+template <int SH, bool WALLS, bool MESH>
+__device__ __forceinline__ void vanilla_path(const RenderParams& P, uint32_t pl, uint64_t s, float* row, VanCtr& c) {
+  const DevScene& S = P.S;
+  uint32_t cx;
+  const uint32_t cy = fastdiv_divmod(pl, P.fd_cw, cx);
+  const uint32_t px = (uint32_t)S.crop[0] + cx, py = (uint32_t)S.crop[1] + cy;
+  const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
+  const uint64_t id = s * ((uint64_t)S.width * (uint64_t)S.height) + p;
+  const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
+  ++c.paths;
+  const u4 a = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 0u, S.rk);
+  const int e = (int)unif_index((uint32_t)S.n_emitters, a.c);
+  const f3 xe = ld3(S.em_pos[e]);
+  const double te = (double)S.em_t[e];
+  const float ek = S.em_k[e];
+  f3 x, w;
+  float beta;
+  if (S.camera_kind == DTS_CAMERA_PINHOLE) {
+    const float sx = (__fdividef(2.0f * ((float)px + unif(a.a)), (float)S.width) - 1.0f) * S.tan_half * S.aspect;
+    const float sy = (1.0f - __fdividef(2.0f * ((float)py + unif(a.b)), (float)S.height)) * S.tan_half;
+    w = mk(S.fwd[0] + sx * S.right[0] + sy * S.upc[0], S.fwd[1] + sx * S.right[1] + sy * S.upc[1],
+           S.fwd[2] + sx * S.right[2] + sy * S.upc[2]);
+    w = w * rsqrtf(dot(w, w));
+    x = ld3(S.cam_pos);
+    beta = 1.0f;
+  } else {
+    const u4 bb = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 1u, S.rk);
+    const u4 cc = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 2u, S.rk);
+    const float rad = S.det_radius * cbrtf(unif(bb.a));
+    const float z = 1.0f - 2.0f * unif(bb.b);
+    const float sz = sqrtf(fmaxf(0.0f, 1.0f - z * z));
+    float sp, cp;
+    __sincosf(2.0f * kPi * unif(bb.c), &sp, &cp);
+    x = mk(S.cam_pos[0] + rad * sz * cp, S.cam_pos[1] + rad * sz * sp, S.cam_pos[2] + rad * z);
+    const float z2 = 1.0f - 2.0f * unif(bb.d);
+    const float s2 = sqrtf(fmaxf(0.0f, 1.0f - z2 * z2));
+    __sincosf(2.0f * kPi * unif(cc.a), &sp, &cp);
+    w = mk(s2 * cp, s2 * sp, z2);
+    beta = 4.0f * kPi;
+  }
+  {
+    float lo, hi;
+    int f;
+    if (intersect<SH, WALLS>(S, x, w, lo, hi, f) == HIT_MISS) {
+      ++c.miss;
+      return;
+    }
+  }
+  int kind = KIND_CAMERA, face = -1;
+  double E = 0.0;
+  bool alive = true;
+  int k;
+  for (k = 0; k < S.max_bounces && alive; ++k) {
+    const u4 r = philox_rk(id_lo, id_hi, (uint32_t)k, 0u, S.rk);
+    ++c.vert;
+    if (kind == KIND_MEDIUM) {
+      float opc, omc;
+      hg_sample(S, unif(r.b), opc, omc);
+      w = from_frame(w, opc, omc, kPi * (2.0f * unif(r.c) - 1.0f));
+    } else if (kind == KIND_WALL) {
+      const f3 n = inward_normal(face);
+      const float u5 = unif(r.b), u6 = unif(r.c);
+      const float rr = sqrtf(u5);
+      float sp, cp;
+      __sincosf(2.0f * kPi * u6, &sp, &cp);
+      const float sign = n.z >= -1e-6f ? 1.0f : -1.0f;  // R12 tie-break (from_frame)
+      const float aa = __fdividef(-1.0f, sign + n.z);
+      const float bq = n.x * n.y * aa;
+      const f3 b1 = mk(1.0f + sign * n.x * n.x * aa, sign * bq, -sign * n.x);
+      const f3 b2 = mk(bq, sign + n.y * n.y * aa, -n.y);
+      const float lx = rr * cp, ly = rr * sp, lz = sqrtf(fmaxf(0.0f, 1.0f - u5));
+      w = mk(b1.x * lx + b2.x * ly + n.x * lz, b1.y * lx + b2.y * ly + n.y * lz, b1.z * lx + b2.z * ly + n.z * lz);
+      beta *= S.wall_albedo[face];
+    } else if (MESH && kind == KIND_SURF) {
+      // R32 sampling (lobe u3, direction u1 u2; the oracle's vanilla order)
+      int mat;
+      const f3 n = tri_side_normal(S, face, w, mat);
+      f3 wo;
+      const float wgt = bsdf_sample(S, mat, n, w, unif(r.d), unif(r.b), unif(r.c), wo);
+      if (!(wgt > 0.0f)) { ++c.esc; alive = false; break; }
+      beta *= wgt;
+      w = wo;
+    }
+    float lo, hi;
+    int hf;
+    int hit = intersect<SH, WALLS>(S, x, w, lo, hi, hf);
+    if (MESH && hit != HIT_MISS) {
+      float tm;
+      const int tri = mesh_trace<false>(S, x, w, hi, tm);
+      if (tri >= 0) { hi = tm; hit = HIT_SURF; hf = tri; }
+    }
+    if (hit == HIT_MISS) { ++c.esc; alive = false; break; }
+    const float counts = (S.warped || kind != KIND_CAMERA) ? 1.0f : 0.0f;
+    const f3 d0 = x - xe;
+    const float Cprev = sqrtf(dot(d0, d0));
+    float d = lo + neg_log1m(unif(r.a)) * S.inv_sigma_t;
+    if (d < hi) {
+      x = fma3(w, d, x);
+      E += (double)(counts * d);
+      beta *= S.albedo;
+      kind = KIND_MEDIUM;
+    } else if (WALLS && hit == HIT_WALL) {
+      d = hi;
+      f3 xn = fma3(w, hi, x);
+      const int ax = hf >> 1;
+      const float pl2 = (hf & 1) ? S.bmax[ax] : S.bmin[ax];
+      if (ax == 0) xn.x = pl2; else if (ax == 1) xn.y = pl2; else xn.z = pl2;
+      x = xn;
+      E += (double)(counts * hi);
+      kind = KIND_WALL;
+      face = hf;
+    } else if (MESH && hit == HIT_SURF) {
+      d = hi;
+      int mat;
+      const f3 n = tri_side_normal(S, hf, w, mat);
+      x = fma3(n, kSurfEps, fma3(w, hi, x));
+      E += (double)(counts * hi);
+      kind = KIND_SURF;
+      face = hf;
+    } else { ++c.esc; alive = false; break; }
+    const f3 cv = xe - x;
+    const float C = sqrtf(dot(cv, cv));
+    const double arrive = te + E + (double)C;
+    if (arrive >= S.t0 + S.dt * S.n_bins) { ++c.early; alive = false; break; }
+    const f3 we = cv * (1.0f / C);
+    float cc;
+    if (kind == KIND_MEDIUM) {
+      cc = beta * hg_eval(S, dot(w, we));
+      if (S.s_excess > 0.0f && d + C - Cprev < S.s_excess) cc = 0.0f;
+    } else if (MESH && kind == KIND_SURF) {
+      int mat;
+      const f3 n = tri_side_normal(S, face, w, mat);
+      cc = beta * bsdf_eval(S, mat, n, w, we) * fmaxf(0.0f, dot(n, we));
+    } else {
+      cc = beta * (S.wall_albedo[face] * (1.0f / kPi)) * fmaxf(0.0f, dot(inward_normal(face), we));
+    }
+    cc *= segment_tr<SH, WALLS, MESH>(S, x, xe, C, we) * __fdividef(ek, C * C);
+    if (S.r_excl > 0.0f && C < S.r_excl) cc = 0.0f;
+    if (cc != 0.0f && isfinite(cc)) {
+      ++c.samp;
+      c.rej += vanilla_splat(P, pl, arrive, cc, row);
+    }
+  }
+  if (alive && k >= S.max_bounces) ++c.cap;
+}
+
+// Vanilla estimator: one lane per path.  Privatised launches (P.van_rows:
+// vanilla paths splat into every bin along their walk, ~1 RED per vertex) take
+// the work in pixel-major order, so a warp's 32 lanes are consecutive samples
+// of one pixel; their connections go to the warp's shared-memory copy of that
+// pixel's row of n_bins floats (shared-memory atomics), flushed to HBM with
+// coalesced REDs of the non-zero bins after each batch of 32 paths.  Lanes of a
+// batch that crosses into the next pixel RED straight to HBM.
 template <int SH, bool WALLS, bool MESH = false>
 __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderParams P) {
+  extern __shared__ float s_rows[];
   const DevScene& S = P.S;
+  const uint32_t B = (uint32_t)S.n_bins;
+  const int lane = threadIdx.x & 31;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint32_t c_paths = 0, c_miss = 0, c_vert = 0, c_early = 0, c_esc = 0, c_cap = 0, c_samp = 0, c_rej = 0;
-  for (uint64_t widx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; widx < P.total; widx += stride) {
-    uint32_t pl, cx;
-    uint64_t s;
-    if (P.div32) {
-      s = P.s_begin + fastdiv_divmod((uint32_t)widx, P.fd_npix, pl);
-    } else {
-      pl = (uint32_t)(widx % P.npix);
-      s = P.s_begin + widx / P.npix;
-    }
-    const uint32_t cy = fastdiv_divmod(pl, P.fd_cw, cx);
-    const uint32_t px = (uint32_t)S.crop[0] + cx, py = (uint32_t)S.crop[1] + cy;
-    const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
-    const uint64_t id = s * ((uint64_t)S.width * (uint64_t)S.height) + p;
-    const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
-    ++c_paths;
-    const u4 a = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 0u, S.rk);
-    const int e = (int)unif_index((uint32_t)S.n_emitters, a.c);
-    const f3 xe = ld3(S.em_pos[e]);
-    const double te = (double)S.em_t[e];
-    const float ek = S.em_k[e];
-    f3 x, w;
-    float beta;
-    if (S.camera_kind == DTS_CAMERA_PINHOLE) {
-      const float sx = (__fdividef(2.0f * ((float)px + unif(a.a)), (float)S.width) - 1.0f) * S.tan_half * S.aspect;
-      const float sy = (1.0f - __fdividef(2.0f * ((float)py + unif(a.b)), (float)S.height)) * S.tan_half;
-      w = mk(S.fwd[0] + sx * S.right[0] + sy * S.upc[0], S.fwd[1] + sx * S.right[1] + sy * S.upc[1],
-             S.fwd[2] + sx * S.right[2] + sy * S.upc[2]);
-      w = w * rsqrtf(dot(w, w));
-      x = ld3(S.cam_pos);
-      beta = 1.0f;
-    } else {
-      const u4 bb = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 1u, S.rk);
-      const u4 cc = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 2u, S.rk);
-      const float rad = S.det_radius * cbrtf(unif(bb.a));
-      const float z = 1.0f - 2.0f * unif(bb.b);
-      const float sz = sqrtf(fmaxf(0.0f, 1.0f - z * z));
-      float sp, cp;
-      __sincosf(2.0f * kPi * unif(bb.c), &sp, &cp);
-      x = mk(S.cam_pos[0] + rad * sz * cp, S.cam_pos[1] + rad * sz * sp, S.cam_pos[2] + rad * z);
-      const float z2 = 1.0f - 2.0f * unif(bb.d);
-      const float s2 = sqrtf(fmaxf(0.0f, 1.0f - z2 * z2));
-      __sincosf(2.0f * kPi * unif(cc.a), &sp, &cp);
-      w = mk(s2 * cp, s2 * sp, z2);
-      beta = 4.0f * kPi;
-    }
-    {
-      float lo, hi;
-      int f;
-      if (intersect<SH, WALLS>(S, x, w, lo, hi, f) == HIT_MISS) {
-        ++c_miss;
-        continue;
-      }
-    }
-    int kind = KIND_CAMERA, face = -1;
-    double E = 0.0;
-    bool alive = true;
-    int k;
-    for (k = 0; k < S.max_bounces && alive; ++k) {
-      const u4 r = philox_rk(id_lo, id_hi, (uint32_t)k, 0u, S.rk);
-      ++c_vert;
-      if (kind == KIND_MEDIUM) {
-        float opc, omc;
-        hg_sample(S, unif(r.b), opc, omc);
-        w = from_frame(w, opc, omc, kPi * (2.0f * unif(r.c) - 1.0f));
-      } else if (kind == KIND_WALL) {
-        const f3 n = inward_normal(face);
-        const float u5 = unif(r.b), u6 = unif(r.c);
-        const float rr = sqrtf(u5);
-        float sp, cp;
-        __sincosf(2.0f * kPi * u6, &sp, &cp);
-        const float sign = n.z >= -1e-6f ? 1.0f : -1.0f;  // R12 tie-break (from_frame)
-        const float aa = __fdividef(-1.0f, sign + n.z);
-        const float bq = n.x * n.y * aa;
-        const f3 b1 = mk(1.0f + sign * n.x * n.x * aa, sign * bq, -sign * n.x);
-        const f3 b2 = mk(bq, sign + n.y * n.y * aa, -n.y);
-        const float lx = rr * cp, ly = rr * sp, lz = sqrtf(fmaxf(0.0f, 1.0f - u5));
-        w = mk(b1.x * lx + b2.x * ly + n.x * lz, b1.y * lx + b2.y * ly + n.y * lz, b1.z * lx + b2.z * ly + n.z * lz);
-        beta *= S.wall_albedo[face];
-      } else if (MESH && kind == KIND_SURF) {
-        // R32 sampling (lobe u3, direction u1 u2; the oracle's vanilla order)
-        int mat;
-        const f3 n = tri_side_normal(S, face, w, mat);
-        f3 wo;
-        const float wgt = bsdf_sample(S, mat, n, w, unif(r.d), unif(r.b), unif(r.c), wo);
-        if (!(wgt > 0.0f)) { ++c_esc; alive = false; break; }
-        beta *= wgt;
-        w = wo;
-      }
-      float lo, hi;
-      int hf;
-      int hit = intersect<SH, WALLS>(S, x, w, lo, hi, hf);
-      if (MESH && hit != HIT_MISS) {
-        float tm;
-        const int tri = mesh_trace<false>(S, x, w, hi, tm);
-        if (tri >= 0) { hi = tm; hit = HIT_SURF; hf = tri; }
-      }
-      if (hit == HIT_MISS) { ++c_esc; alive = false; break; }
-      const float counts = (S.warped || kind != KIND_CAMERA) ? 1.0f : 0.0f;
-      const f3 d0 = x - xe;
-      const float Cprev = sqrtf(dot(d0, d0));
-      float d = lo + neg_log1m(unif(r.a)) * S.inv_sigma_t;
-      if (d < hi) {
-        x = fma3(w, d, x);
-        E += (double)(counts * d);
-        beta *= S.albedo;
-        kind = KIND_MEDIUM;
-      } else if (WALLS && hit == HIT_WALL) {
-        d = hi;
-        f3 xn = fma3(w, hi, x);
-        const int ax = hf >> 1;
-        const float pl2 = (hf & 1) ? S.bmax[ax] : S.bmin[ax];
-        if (ax == 0) xn.x = pl2; else if (ax == 1) xn.y = pl2; else xn.z = pl2;
-        x = xn;
-        E += (double)(counts * hi);
-        kind = KIND_WALL;
-        face = hf;
-      } else if (MESH && hit == HIT_SURF) {
-        d = hi;
-        int mat;
-        const f3 n = tri_side_normal(S, hf, w, mat);
-        x = fma3(n, kSurfEps, fma3(w, hi, x));
-        E += (double)(counts * hi);
-        kind = KIND_SURF;
-        face = hf;
-      } else { ++c_esc; alive = false; break; }
-      const f3 cv = xe - x;
-      const float C = sqrtf(dot(cv, cv));
-      const double arrive = te + E + (double)C;
-      if (arrive >= S.t0 + S.dt * S.n_bins) { ++c_early; alive = false; break; }
-      const f3 we = cv * (1.0f / C);
-      float c;
-      if (kind == KIND_MEDIUM) {
-        c = beta * hg_eval(S, dot(w, we));
-        if (S.s_excess > 0.0f && d + C - Cprev < S.s_excess) c = 0.0f;
-      } else if (MESH && kind == KIND_SURF) {
-        int mat;
-        const f3 n = tri_side_normal(S, face, w, mat);
-        c = beta * bsdf_eval(S, mat, n, w, we) * fmaxf(0.0f, dot(n, we));
+  float* row = P.van_rows ? s_rows + (size_t)(threadIdx.x >> 5) * B : nullptr;
+  if (row)
+    for (uint32_t b = lane; b < B; b += 32) row[b] = 0.0f;
+  __syncwarp();
+  VanCtr c;
+  // warp-uniform batches of 32 consecutive work items
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < P.total; base += stride) {
+    const uint64_t widx = base + (uint64_t)lane;
+    const bool valid = widx < P.total;
+    uint32_t pl = 0;
+    uint64_t s = 0;
+    if (valid) {
+      if (P.van_rows) {  // pixel-major: samples of a pixel are consecutive
+        if (P.div32) {
+          uint32_t sl;
+          pl = fastdiv_divmod((uint32_t)widx, P.fd_ns, sl);
+          s = P.s_begin + sl;
+        } else {
+          s = P.s_begin + widx % P.n_s;
+          pl = (uint32_t)(widx / P.n_s);
+        }
+      } else if (P.div32) {
+        s = P.s_begin + fastdiv_divmod((uint32_t)widx, P.fd_npix, pl);
       } else {
-        c = beta * (S.wall_albedo[face] * (1.0f / kPi)) * fmaxf(0.0f, dot(inward_normal(face), we));
-      }
-      c *= segment_tr<SH, WALLS, MESH>(S, x, xe, C, we) * __fdividef(ek, C * C);
-      if (S.r_excl > 0.0f && C < S.r_excl) c = 0.0f;
-      if (c != 0.0f && isfinite(c)) {
-        ++c_samp;
-        c_rej += vanilla_splat(P, pl, arrive, c);
+        pl = (uint32_t)(widx % P.npix);
+        s = P.s_begin + widx / P.npix;
       }
     }
-    if (alive && k >= S.max_bounces) ++c_cap;
+    const uint32_t pw = __shfl_sync(0xffffffffu, pl, 0);   // the batch's pixel (lane 0 is always valid)
+    if (valid) vanilla_path<SH, WALLS, MESH>(P, pl, s, (row && pl == pw) ? row : nullptr, c);
+    if (row) {  // flush the batch's row: coalesced REDs of its non-zero bins
+      __syncwarp();
+      float* g = P.hist + (size_t)pw * B;
+      for (uint32_t b = lane; b < B; b += 32) {
+        const float v = row[b];
+        if (v != 0.0f) {
+          atomicAdd(g + b, v);
+          row[b] = 0.0f;
+        }
+      }
+      __syncwarp();
+    }
   }
   // warp-reduce and flush counters
   for (int o = 16; o > 0; o >>= 1) {
-    c_paths += __shfl_xor_sync(0xffffffffu, c_paths, o);
-    c_miss += __shfl_xor_sync(0xffffffffu, c_miss, o);
-    c_vert += __shfl_xor_sync(0xffffffffu, c_vert, o);
-    c_early += __shfl_xor_sync(0xffffffffu, c_early, o);
-    c_esc += __shfl_xor_sync(0xffffffffu, c_esc, o);
-    c_cap += __shfl_xor_sync(0xffffffffu, c_cap, o);
-    c_samp += __shfl_xor_sync(0xffffffffu, c_samp, o);
-    c_rej += __shfl_xor_sync(0xffffffffu, c_rej, o);
+    c.paths += __shfl_xor_sync(0xffffffffu, c.paths, o);
+    c.miss += __shfl_xor_sync(0xffffffffu, c.miss, o);
+    c.vert += __shfl_xor_sync(0xffffffffu, c.vert, o);
+    c.early += __shfl_xor_sync(0xffffffffu, c.early, o);
+    c.esc += __shfl_xor_sync(0xffffffffu, c.esc, o);
+    c.cap += __shfl_xor_sync(0xffffffffu, c.cap, o);
+    c.samp += __shfl_xor_sync(0xffffffffu, c.samp, o);
+    c.rej += __shfl_xor_sync(0xffffffffu, c.rej, o);
   }
-  if ((threadIdx.x & 31) == 0 && P.counters) {
-    atomicAdd(P.counters + DTS_CTR_PATHS, (unsigned long long)c_paths);
-    atomicAdd(P.counters + DTS_CTR_CAMERA_MISS, (unsigned long long)c_miss);
-    atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
-    atomicAdd(P.counters + DTS_CTR_EARLY_EXIT, (unsigned long long)c_early);
-    atomicAdd(P.counters + DTS_CTR_ESCAPES, (unsigned long long)c_esc);
-    atomicAdd(P.counters + DTS_CTR_CAP_HITS, (unsigned long long)c_cap);
-    atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
-    atomicAdd(P.counters + DTS_CTR_REJECTED, (unsigned long long)c_rej);
+  if (lane == 0 && P.counters) {
+    atomicAdd(P.counters + DTS_CTR_PATHS, (unsigned long long)c.paths);
+    atomicAdd(P.counters + DTS_CTR_CAMERA_MISS, (unsigned long long)c.miss);
+    atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c.vert);
+    atomicAdd(P.counters + DTS_CTR_EARLY_EXIT, (unsigned long long)c.early);
+    atomicAdd(P.counters + DTS_CTR_ESCAPES, (unsigned long long)c.esc);
+    atomicAdd(P.counters + DTS_CTR_CAP_HITS, (unsigned long long)c.cap);
+    atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c.samp);
+    atomicAdd(P.counters + DTS_CTR_REJECTED, (unsigned long long)c.rej);
   }
 }
 
@@ -1923,8 +1997,12 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bw, kwalk, kBlockWalk, 0));
       if (bw < 1) bw = 1;
       const uint64_t gw = (uint64_t)s->num_sms * bw;
-      // paths per chunk: the hand-off buffer holds one chunk (64 B per path)
+      // paths per chunk: the hand-off buffer holds one chunk (64 B per path);
+      // 2^27, but at least two chunks for launches of >= 2^21 paths (an 8-GPU
+      // rank's share of config 5 is 2^27 paths) so that the second chunk's walk
+      // stage fills the first one's tail
       uint64_t chunk = (uint64_t)1 << 27;
+      if (P.total >= ((uint64_t)1 << 21)) chunk = std::min<uint64_t>(chunk, (P.total + 1) / 2);
       const char* ch = getenv("DTS_WF_CHUNK");
       if (ch && atoll(ch) >= 1024) chunk = std::min<uint64_t>((uint64_t)atoll(ch), (uint64_t)1 << 31);
       if (chunk > P.total) chunk = P.total;
@@ -1993,17 +2071,24 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     int bps = 1;
     const void* kfn = vanilla_kernel_ptr(d.medium_shape, d.wall_mask != 0u, d.n_tris > 0);
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, kBlock, 0));
+    // per-warp shared-memory histogram rows when a warp's 32 paths share a pixel
+    // (>= 32 samples per pixel) and a row fits (n_bins <= 2048: 24 warps x 8 KB);
+    // DTS_VANILLA_ROWS=0 forces the direct REDs (A/B)
+    const char* vr = getenv("DTS_VANILLA_ROWS");
+    P.van_rows = (ns >= 32 && d.n_bins <= 2048 && !(vr && vr[0] == '0')) ? 1u : 0u;
+    const size_t vdyn = P.van_rows ? (size_t)(kBlock / 32) * d.n_bins * sizeof(float) : 0;
+    CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vdyn));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, kBlock, vdyn));
     uint64_t grid = (uint64_t)s->num_sms * (bps < 1 ? 1 : bps) * 4;
     const uint64_t need = (P.total + kBlock - 1) / kBlock;
     if (grid > need) grid = need;
     void* args[] = {&P};
-    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(kBlock), args, 0, st));
+    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(kBlock), args, vdyn, st));
     CUDA_TRY(cudaGetLastError());
     g_last_launches = 1;
     g_last_grid = (int)grid;
     g_last_block = kBlock;
-    g_last_smem = 0;
+    g_last_smem = (int)vdyn;
   }
   return DTS_OK;
 }
