@@ -2072,10 +2072,12 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     const void* kfn = vanilla_kernel_ptr(d.medium_shape, d.wall_mask != 0u, d.n_tris > 0);
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
     // per-warp shared-memory histogram rows when a warp's 32 paths share a pixel
-    // (>= 32 samples per pixel) and a row fits (n_bins <= 2048: 24 warps x 8 KB);
-    // DTS_VANILLA_ROWS=0 forces the direct REDs (A/B)
+    // (>= 32 samples per pixel) and the row is short against the batch's
+    // contributions (n_bins <= 128; A/B, profiles/ab_r02_vanilla_rows.log: config 4
+    // (1 bin) +23 %, config 1 (128) even, config 3 (512 bins, ~19 vertices per
+    // path) -5 %, config 5 (1000) even); DTS_VANILLA_ROWS=0/1 forces off / on
     const char* vr = getenv("DTS_VANILLA_ROWS");
-    P.van_rows = (ns >= 32 && d.n_bins <= 2048 && !(vr && vr[0] == '0')) ? 1u : 0u;
+    P.van_rows = (ns >= 32 && d.n_bins <= (vr && vr[0] == '1' ? 2048 : 128) && !(vr && vr[0] == '0')) ? 1u : 0u;
     const size_t vdyn = P.van_rows ? (size_t)(kBlock / 32) * d.n_bins * sizeof(float) : 0;
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vdyn));
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, kBlock, vdyn));
