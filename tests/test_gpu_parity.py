@@ -781,3 +781,39 @@ def test_mesh_debug_surface_records(dts, oracle):
     gb = dts.debug(sc, bad)
     assert (gb["terminate"] == 1).all() and (gb["tech"] == 0).all()
     sc.close()
+
+
+# ------------------------------------------------------------------ two-stage render
+TWO_STAGE = [
+    ("cfg5_pixelmode", lambda: I.small(I.config(5), 24, 20, n_bins=200, t1=40.0), 64),
+    ("cfg3_cell", lambda: I.small(I.config(3), 16, 16, n_bins=64), 16),
+    ("cfg5_full_width_rows", lambda: I.config(5, crop=(0, 500, 1024, 506)), 8),
+]
+
+
+@pytest.mark.parametrize("name,mk,spp", TWO_STAGE, ids=[t[0] for t in TWO_STAGE])
+def test_two_stage_render_equals_one_stage(dts, monkeypatch, name, mk, spp):
+    """The walk stage only skips connections that provably cannot land in the
+    bin: the two-stage render (walk kernel + hand-off + connect kernel) traces
+    the same paths as the one-stage kernel -- every counter equal, vertices
+    included -- and the same histogram up to fp32 summation order.  Small
+    chunks (DTS_WF_CHUNK) exercise the chunk loop and its two-stream overlap."""
+    c = I.as_f32(mk())
+    sc = _scene(dts, c)
+    monkeypatch.setenv("DTS_WAVEFRONT", "0")
+    h1, _, c1 = dts.render_to_tensor(sc, spp, c["seed"])
+    monkeypatch.setenv("DTS_WAVEFRONT", "1")
+    monkeypatch.setenv("DTS_WF_CHUNK", "8192")
+    h2, _, c2 = dts.render_to_tensor(sc, spp, c["seed"])
+    torch.cuda.synchronize()
+    launches = dts.last_launch()["n_launches"]
+    d1, d2 = dts.counters_dict(c1), dts.counters_dict(c2)
+    print(f"{name}: one-stage {d1['vertices']} vertices, two-stage {d2['vertices']} ({d2['walk_vertices']} walk-only), "
+          f"{launches} launches")
+    assert launches >= 4
+    assert d2["walk_vertices"] > 0 and d1["walk_vertices"] == 0
+    for k in d1:
+        if k not in ("walk_vertices",):
+            assert d1[k] == d2[k], (k, d1[k], d2[k])
+    a, b = h1.double(), h2.double()
+    assert float((a - b).norm() / a.norm()) < 1e-5
