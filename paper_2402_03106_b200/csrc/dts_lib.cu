@@ -1347,18 +1347,18 @@ struct PickMesh {
   static const void* sph() { return (const void*)render_darts_kernel<true, DTS_MEDIUM_SPHERE, FL | FL_MESH, false>; }
 };
 // two-stage render (SPLIT scenes without meshes, BOX or SPHERE media)
-template <bool SMEM>
+template <bool SMEM, bool DEFER = false>
 struct PickResume {
   template <int FL>
   struct F {
     static const void* box() {
-      if constexpr ((FL & FL_SPLIT) != 0) return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, FL, false, true>;
+      if constexpr ((FL & FL_SPLIT) != 0) return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_BOX, FL, DEFER, true>;
       return nullptr;
     }
     static const void* inf() { return nullptr; }
     static const void* sph() {
       if constexpr ((FL & FL_SPLIT) != 0 && (FL & FL_WALLS) == 0)
-        return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, FL, false, true>;
+        return (const void*)render_darts_kernel<SMEM, DTS_MEDIUM_SPHERE, FL, DEFER, true>;
       return nullptr;
     }
   };
@@ -1965,8 +1965,11 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     uint64_t grid = (uint64_t)s->num_sms * blocks_per_sm;
     const uint64_t need = (P.total + 31) / 32 / (blk / 32) + 1;
     if (grid > need) grid = need;
-    if (defer) {  // global overflow queue slots: kQueue x (kJobWords + kJob1Words) floats per warp
-      const size_t ov = (size_t)grid * (kBlock / 32) * kQueue * (kJobWords + kJob1Words);
+    // global overflow queue slots: kQueue x (kJobWords + kJob1Words) floats per
+    // warp, twice (the two-stage render's overlapped chunks run two connect kernels)
+    const size_t ov1 = (size_t)grid * (kBlock / 32) * kQueue * (kJobWords + kJob1Words);
+    if (defer) {
+      const size_t ov = 2 * ov1;
       if (ov > s->qover_n) {
         cudaFree(s->d_qover);
         s->d_qover = nullptr;
@@ -1979,13 +1982,16 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     // two-stage render (walk stage + connect stage, see HandOff) for SPLIT
     // scenes without meshes in BOX / SPHERE media; DTS_WAVEFRONT=0 forces the
     // one-stage kernel (A/B)
-    bool wave = !defer && d.direction_mode == DTS_DIR_SPLIT && d.n_tris == 0 && d.medium_shape != DTS_MEDIUM_INFINITE;
+    // (DTS_DEFER=1: the connect stage runs the deferred-connection kernel)
+    bool wave = d.direction_mode == DTS_DIR_SPLIT && d.n_tris == 0 && d.medium_shape != DTS_MEDIUM_INFINITE;
     const char* wv = getenv("DTS_WAVEFRONT");
     if (wv && wv[0] == '0') wave = false;
     const void* kwalk = wave ? pick_fl<PickWalk>(d.medium_shape, scene_flags(d)) : nullptr;
-    const void* kres = wave ? (smem ? pick_fl<PickResume<true>::F>(d.medium_shape, scene_flags(d))
-                                    : pick_fl<PickResume<false>::F>(d.medium_shape, scene_flags(d)))
-                            : nullptr;
+    const void* kres = !wave ? nullptr
+                       : defer ? (smem ? pick_fl<PickResume<true, true>::F>(d.medium_shape, scene_flags(d))
+                                       : pick_fl<PickResume<false, true>::F>(d.medium_shape, scene_flags(d)))
+                               : (smem ? pick_fl<PickResume<true>::F>(d.medium_shape, scene_flags(d))
+                                       : pick_fl<PickResume<false>::F>(d.medium_shape, scene_flags(d)));
     if (!kwalk || !kres) {
       CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
       void* args[] = {&P};
@@ -2048,6 +2054,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         RenderParams PC = PW;
         PC.w_base = 0;
         PC.work = wf + 1;
+        if (defer) PC.qover = s->d_qover + (size_t)h * ov1;
         CUDA_TRY(cudaMemsetAsync(wf, 0, 3 * sizeof(unsigned long long), xst));
         void* aw[] = {&PW};
         CUDA_TRY(cudaLaunchKernel(kwalk, dim3((unsigned)std::min<uint64_t>(gw, (PW.total + kBlockWalk - 1) / kBlockWalk)),
