@@ -253,7 +253,17 @@ size_t dts_hist_cells(dts_scene_t scene);
  * lane-iterations that trigger a lane refill.  None changes any result
  * beyond fp32 summation order.  DTS_DEFER applies to dts_render only: row-band
  * launches (dts_render_rows, dts_render_host's bands), which may run
- * concurrently on one scene, always take the immediate kernels. */
+ * concurrently on one scene, always take the immediate kernels.
+ * SPLIT scenes (R29) without meshes in BOX or SPHERE media render in two stages
+ * (DESIGN.md 5.2b): a walk kernel runs the vertices whose connection provably
+ * cannot reach the bin, then hands each path to a connect kernel through a
+ * library-owned HBM buffer of 64 bytes per path of a chunk (chunks of at most
+ * 2^27 paths, and at least two for launches of >= 2^21 paths; DTS_WF_CHUNK
+ * overrides; dts_render holds two chunks' worth -- 17 GB for config 5 -- and
+ * overlaps consecutive chunks on an internal stream ordered after `stream`;
+ * each row band holds one chunk's worth and runs its chunks in order).  The paths, counters and histogram are those of the one-stage
+ * kernel (DTS_WAVEFRONT=0 selects it); failing to allocate the buffer is
+ * DTS_E_OOM. */
 dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
                       uint64_t sample_end, float* d_hist, float* d_hist_sq, uint64_t* d_counters,
                       void* stream);
