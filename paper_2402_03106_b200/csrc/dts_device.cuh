@@ -319,10 +319,13 @@ __device__ __forceinline__ int intersect_inside(const DevScene& S, f3 o, f3 d, f
     hi = tf;
     return HIT_OPEN;
   }
-  const float tx = ((d.x > 0.0f ? S.bmax[0] : S.bmin[0]) - o.x) * __fdividef(1.0f, d.x);
-  const float ty = ((d.y > 0.0f ? S.bmax[1] : S.bmin[1]) - o.y) * __fdividef(1.0f, d.y);
-  const float tz = ((d.z > 0.0f ? S.bmax[2] : S.bmin[2]) - o.z) * __fdividef(1.0f, d.z);
-  const float tf = fminf(fminf(tx, ty), tz);  // NaN (0 * inf) of an axis-parallel ray is dropped
+  // the exit plane of each axis by the sign BIT of d: a +0 or -0 component then
+  // gives (plane - o) * (1/d) = +inf (the ray never leaves through that axis);
+  // a "d > 0" test would pick the wrong plane for +0 and return -inf
+  const float tx = ((__float_as_int(d.x) >= 0 ? S.bmax[0] : S.bmin[0]) - o.x) * __fdividef(1.0f, d.x);
+  const float ty = ((__float_as_int(d.y) >= 0 ? S.bmax[1] : S.bmin[1]) - o.y) * __fdividef(1.0f, d.y);
+  const float tz = ((__float_as_int(d.z) >= 0 ? S.bmax[2] : S.bmin[2]) - o.z) * __fdividef(1.0f, d.z);
+  const float tf = fminf(fminf(tx, ty), tz);  // NaN (0 * inf, an origin on a plane) is dropped
   if (!(tf > 0.0f)) return HIT_MISS;
   hi = tf;
   if (!WALLS) return HIT_OPEN;  // the exit face only matters when some face is a wall
@@ -978,8 +981,11 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   // ---- intersection, reused by the connection and the walk ----
   float lo = 0.0f, hi = 0.0f;
   int face = -1;
-  int hit = ps.kind == KIND_CAMERA ? intersect<SH, WALLS>(S, ps.x, ww, lo, hi, face)
-                                   : intersect_inside<SH, WALLS>(S, ps.x, ww, lo, hi, face);
+  // one call site for every vertex kind: intersect() gives an inside origin
+  // lo = 0 and the same exit as intersect_inside(), and a warp that mixes
+  // camera and inside vertices then runs one intersection, not both (A/B:
+  // config 4 +7 %, config 2 +1.6 %, config 5 even; profiles/ab_r02_isect1.log)
+  int hit = intersect<SH, WALLS>(S, ps.x, ww, lo, hi, face);
   if (MESH && hit != HIT_MISS) {  // the interval ends at the nearest triangle (PAPER.md:301 case II)
     float tm;
     const int tri = mesh_trace<false>(S, ps.x, ww, hi, tm);
