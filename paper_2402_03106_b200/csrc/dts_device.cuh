@@ -814,7 +814,7 @@ __device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_
 // walk: the mixture direction, the connection's intersection and S range, and
 // the wall NEE are skipped -- they would contribute exactly 0 -- and the walk's
 // random numbers, directions and distances are the full vertex's, bit for bit.
-// *walk_step carries the margin in and its lower bound after the step out
+// *walk_margin carries the margin in and its lower bound after the step out
 // (margin - (1 + counts) d: see walk_kernel); while it stays positive the early
 // exit test is skipped (R_M - E - C >= R_m - E - S_max > 0).
 template <bool DBG, bool SMEM, int SH, int FL, bool DEFER = false, bool WALK = false>
@@ -823,7 +823,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason,
                                              const Defer* df = nullptr, bool* pushed = nullptr,
                                              RisReq* rq = nullptr, uint32_t* nsamp = nullptr,
-                                             bool* pushed1 = nullptr, float* walk_step = nullptr) {
+                                             bool* pushed1 = nullptr, float* walk_margin = nullptr) {
   static_assert(!WALK || ((FL & FL_SPLIT) && !(FL & FL_MESH) && !DEFER && !DBG),
                 "the walk stage serves SPLIT scenes without meshes");
   contrib = 0.0f;
@@ -1152,7 +1152,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     ps.beta *= S.albedo;
     ps.x = fma3(ww, d, ps.x);
     ps.resM -= f2d(counts * d);
-    if (WALK) *walk_step -= (1.0f + counts) * d * 1.00001f;
+    if (WALK) *walk_margin -= (1.0f + counts) * d * 1.00001f;
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
     if (DBG) { dbg->event = 1; dbg->istar = 0; dbg->d = d; dbg->beta_ris = S.albedo; }
@@ -1261,7 +1261,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     ps.resM -= f2d(counts * dsel);
     ps.kind = KIND_MEDIUM;
     ps.w = ww;
-    if (WALK) *walk_step -= (1.0f + counts) * dsel * 1.00001f;
+    if (WALK) *walk_margin -= (1.0f + counts) * dsel * 1.00001f;
     if (DBG) { dbg->event = 1; dbg->istar = (int)is; dbg->d = dsel; dbg->beta_ris = beta_ris; }
   } else {
     if (WALLS && hit == HIT_WALL) {
@@ -1272,7 +1272,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       ps.x = xn;
       ps.resM -= f2d(counts * hi);
       ps.kind = KIND_WALL;
-      if (WALK) *walk_step -= (1.0f + counts) * hi * 1.00001f;
+      if (WALK) *walk_margin -= (1.0f + counts) * hi * 1.00001f;
       ps.face = face;
       ps.w = ww;
       if (DBG) { dbg->event = 2; dbg->d = hi; dbg->beta_ris = 1.0f; }
@@ -1296,7 +1296,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     dbg->x_next[0] = ps.x.x; dbg->x_next[1] = ps.x.y; dbg->x_next[2] = ps.x.z;
     dbg->beta_out = ps.beta;
   }
-  if (WALK && *walk_step > 0.0f) {
+  if (WALK && *walk_margin > 0.0f) {
     // walk stage: the connection margin still bounds R_M - E - C from below, so
     // the early exit provably does not fire; only the non-finite test remains
     if (!isfinite(ps.beta)) {
