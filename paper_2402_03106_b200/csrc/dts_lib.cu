@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
 // hand-off slot (warp-level reservation of kHoBlock slots from a global
 // counter); a path that ends in the walk stage contributed nothing.
 #ifndef DTS_BLOCK_WALK
-#define DTS_BLOCK_WALK 896
+#define DTS_BLOCK_WALK 1024
 #endif
 constexpr int kBlockWalk = DTS_BLOCK_WALK;
 #ifndef DTS_WALK_INNER
