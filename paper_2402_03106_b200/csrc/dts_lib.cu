@@ -2151,9 +2151,10 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
   const dts_scene_desc& d = s->desc;
   const int rows = d.crop[3] - d.crop[1];
   const size_t row_cells = (size_t)(d.crop[2] - d.crop[0]) * (size_t)d.n_bins;
-  // large histograms (config 5: 4.2 GB, ~80 ms over PCIe): kHostBands row bands
+  // large histograms (config 5: 4.2 GB, ~170 ms over PCIe): kHostBands row bands
   // on two streams; band k's copy to the host overlaps band k+1's render (and
-  // band k's tail overlaps band k+1's start).  Same paths, same ids.
+  // band k's tail overlaps band k+1's start), the last band is 1/32 of the rows.
+  // Same paths, same ids.
   const bool banded = n * sizeof(float) >= ((size_t)256 << 20) && rows >= 2 * kHostBands && sb < se;
   if (!banded) {
     dts_status r = dts_render(s, spp, seed, sb, se, s->d_hist_host, nullptr, s->d_ctr_host, stream);
@@ -2164,8 +2165,12 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
     if (eb != DTS_OK) return eb;
     CUDA_TRY(cudaEventRecord(s->band_ev[kHostBands], st));
     for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamWaitEvent(s->band_stream[i], s->band_ev[kHostBands], 0));
+    // the last band is short (1/32 of the rows): only its copy is not hidden
+    // behind a later band's render
+    const int cut = rows - std::max(1, rows / 32);
     for (int k = 0; k < kHostBands; ++k) {
-      const int r0 = rows * k / kHostBands, r1 = rows * (k + 1) / kHostBands;
+      const int r0 = k < kHostBands - 1 ? cut * k / (kHostBands - 1) : cut;
+      const int r1 = k < kHostBands - 1 ? cut * (k + 1) / (kHostBands - 1) : rows;
       cudaStream_t bs = s->band_stream[k & 1];
       dts_status r = render_impl(s, spp, seed, sb, se, s->d_hist_host + (size_t)r0 * row_cells, nullptr,
                                  s->d_ctr_host, bs, r0, r1, s->d_work_band + k, false, 1 + k);

@@ -41,10 +41,17 @@ def render_sharded(render_range: Callable[[int, int], None], spp: int, hist, cou
 
 
 def band_rows(rows: int, nbands: int) -> list[tuple[int, int]]:
-    """Row bands [r0, r1) of a crop of ``rows`` rows: contiguous, covering, sizes within one."""
-    if nbands < 1 or rows < nbands:
-        raise ValueError(f"need 1 <= nbands <= rows, got {nbands} bands of {rows} rows")
-    return [(rows * k // nbands, rows * (k + 1) // nbands) for k in range(nbands)]
+    """Row bands [r0, r1) of a crop of ``rows`` rows: contiguous and covering;
+    with more than one band the last is short (1/32 of the rows, at least one
+    row) -- only its host copy is not hidden behind a later band's render -- and
+    the others split the rest within one row (dts_render_host does the same)."""
+    if nbands < 1 or rows < 2 * nbands:
+        raise ValueError(f"need 1 <= nbands <= rows / 2, got {nbands} bands of {rows} rows")
+    if nbands == 1:
+        return [(0, rows)]
+    cut = rows - max(1, rows // 32)
+    m = nbands - 1
+    return [(cut * k // m, cut * (k + 1) // m) for k in range(m)] + [(cut, rows)]
 
 
 def pipeline_bands(rows: int, nbands: int, render_rows: Callable[[int, int, int], None],

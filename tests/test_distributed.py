@@ -145,6 +145,7 @@ def test_two_rank_banded_e2e_pipeline_equals_single_render(tmp_path):
     ref = O.render(c, O.build_table(c)[0], spp, seed, sq=False)["hist"].ravel()
     assert np.count_nonzero(ref) > 0
     assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
-    assert band_rows(9, 4) == [(0, 2), (2, 4), (4, 6), (6, 9)]
+    assert band_rows(9, 4) == [(0, 2), (2, 5), (5, 8), (8, 9)]
+    assert band_rows(1024, 4)[-1] == (992, 1024) and band_rows(10, 1) == [(0, 10)]
     with pytest.raises(ValueError):
         band_rows(3, 4)
