@@ -302,6 +302,12 @@ dts_status dts_sample_debug(dts_scene_t scene, int32_t n, const dts_debug_in* d_
  * Synchronizes the device. */
 dts_status dts_check_failures(uint64_t* out);
 
+/* The large library-owned buffers (the two-stage render's hand-off records,
+ * dts_render_host's device histogram) go to a process-wide per-device pool when
+ * their scene is destroyed (up to 96 GB per device) and are reused by later
+ * scenes.  This frees every pooled buffer.  Thread-safe; synchronous. */
+dts_status dts_pool_release(void);
+
 /* Enables peer access from the current device to device `peer` (a no-op when
  * it is the current device or already enabled), so that a render kernel on
  * this device can accumulate into a histogram that lives on `peer` and was

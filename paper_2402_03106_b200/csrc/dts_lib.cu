@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -39,6 +40,57 @@ static dts_status fail(dts_status s, const std::string& msg) {
 
 constexpr int kHostBands = 4;  // dts_render_host row bands for large histograms
 
+// ============================================================== device buffer pool
+// The large library-owned buffers (hand-off records, dts_render_host's device
+// histogram: gigabytes for config 5) are returned here when a scene is destroyed
+// and handed to the next scene of the same device that needs as much, so an
+// application that creates a scene per frame (bench.py's e2e leg) does not pay
+// a cudaMalloc / cudaFree of tens of GB per frame.  Pooled bytes per device are
+// capped (kPoolCap); the rest is freed.
+namespace {
+struct PoolBuf {
+  int dev;
+  void* p;
+  size_t bytes;
+};
+std::mutex g_pool_mu;
+std::vector<PoolBuf> g_pool;
+constexpr size_t kPoolCap = (size_t)96 << 30;
+
+// a buffer of >= bytes on device dev (the smallest pooled one that fits, else cudaMalloc)
+cudaError_t pool_get(int dev, size_t bytes, void** out, size_t* got) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_pool.size(); ++i)
+      if (g_pool[i].dev == dev && g_pool[i].bytes >= bytes && (best < 0 || g_pool[i].bytes < g_pool[best].bytes))
+        best = i;
+    if (best >= 0) {
+      *out = g_pool[best].p;
+      *got = g_pool[best].bytes;
+      g_pool.erase(g_pool.begin() + best);
+      return cudaSuccess;
+    }
+  }
+  *got = bytes;
+  return cudaMalloc(out, bytes);
+}
+
+// returns a buffer to the pool (the caller has synchronised its last use)
+void pool_put(int dev, void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  size_t held = 0;
+  for (const PoolBuf& b : g_pool)
+    if (b.dev == dev) held += b.bytes;
+  if (held + bytes > kPoolCap) {
+    cudaFree(p);
+    return;
+  }
+  g_pool.push_back(PoolBuf{dev, p, bytes});
+}
+}  // namespace
+
 struct dts_scene {
   dts_scene_desc desc;
   DevScene S;
@@ -46,7 +98,7 @@ struct dts_scene {
   size_t table_n = 0;
   unsigned long long* d_work = nullptr;  // global work counter
   float* d_hist_host = nullptr;          // dts_render_host scratch
-  size_t d_hist_host_n = 0;
+  size_t d_hist_host_n = 0;              // its capacity in floats
   uint64_t* d_ctr_host = nullptr;
   uint32_t* d_resp_cdf = nullptr;  // R31 bin CDF (n_bins + 1)
   float* d_resp_wgt = nullptr;     // W_b / pi_b
@@ -1731,7 +1783,7 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaDeviceSynchronize();
   cudaFree(s->d_table);
   cudaFree(s->d_work);
-  cudaFree(s->d_hist_host);
+  pool_put(s->device, s->d_hist_host, s->d_hist_host_n * sizeof(float));
   cudaFree(s->d_ctr_host);
   cudaFree(s->d_resp_cdf);
   cudaFree(s->d_resp_wgt);
@@ -1743,7 +1795,7 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   for (int i = 0; i <= kHostBands; ++i)
     if (s->band_ev[i]) cudaEventDestroy(s->band_ev[i]);
   cudaFree(s->d_work_band);
-  for (int i = 0; i <= kHostBands; ++i) cudaFree(s->d_ho[i]);
+  for (int i = 0; i <= kHostBands; ++i) pool_put(s->device, s->d_ho[i], s->ho_cap[i] * sizeof(HandOff));
   cudaFree(s->d_wf);
   if (s->wf_stream) cudaStreamDestroy(s->wf_stream);
   for (int i = 0; i < 2; ++i)
@@ -2017,12 +2069,18 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       const int halves = overlap ? 2 : 1;
       const size_t cap = (size_t)chunk + (size_t)gw * (kBlockWalk / 32) * kHoBlock;
       if (s->ho_cap[slot] < cap * halves) {
-        cudaFree(s->d_ho[slot]);
+        if (s->d_ho[slot]) {  // (a smaller one: its last use must be over before it is pooled)
+          CUDA_TRY(cudaStreamSynchronize(st));
+          pool_put(s->device, s->d_ho[slot], s->ho_cap[slot] * sizeof(HandOff));
+        }
         s->d_ho[slot] = nullptr;
         s->ho_cap[slot] = 0;
-        if (cudaMalloc(&s->d_ho[slot], cap * halves * sizeof(HandOff)) != cudaSuccess)
+        void* p = nullptr;
+        size_t got = 0;
+        if (pool_get(s->device, cap * halves * sizeof(HandOff), &p, &got) != cudaSuccess)
           return fail(DTS_E_OOM, "cudaMalloc(hand-off buffer) failed");
-        s->ho_cap[slot] = cap * halves;
+        s->d_ho[slot] = static_cast<HandOff*>(p);
+        s->ho_cap[slot] = got / sizeof(HandOff);
       }
       if (!s->d_wf && cudaMalloc(&s->d_wf, 3 * (2 + kHostBands) * sizeof(unsigned long long)) != cudaSuccess)
         return fail(DTS_E_OOM, "cudaMalloc(two-stage counters) failed");
@@ -2137,12 +2195,15 @@ dts_status dts_render_host(dts_scene_t s, uint64_t spp, uint64_t seed, uint64_t 
   if (!s || !h_hist) return fail(DTS_E_INVALID_ARG, "NULL argument");
   const size_t n = dts_hist_cells(s);
   cudaStream_t st = (cudaStream_t)stream;
-  if (s->d_hist_host_n != n) {
-    cudaFree(s->d_hist_host);
+  if (s->d_hist_host_n < n) {  // (capacity in floats; the previous call synchronised its stream)
+    pool_put(s->device, s->d_hist_host, s->d_hist_host_n * sizeof(float));
     s->d_hist_host = nullptr;
     s->d_hist_host_n = 0;
-    if (cudaMalloc(&s->d_hist_host, n * sizeof(float)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(hist) failed");
-    s->d_hist_host_n = n;
+    void* p = nullptr;
+    size_t got = 0;
+    if (pool_get(s->device, n * sizeof(float), &p, &got) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(hist) failed");
+    s->d_hist_host = static_cast<float*>(p);
+    s->d_hist_host_n = got / sizeof(float);
   }
   if (!s->d_ctr_host && cudaMalloc(&s->d_ctr_host, DTS_NUM_COUNTERS * sizeof(uint64_t)) != cudaSuccess)
     return fail(DTS_E_OOM, "cudaMalloc(counters) failed");
@@ -2217,6 +2278,13 @@ dts_status dts_check_failures(uint64_t* out) {
   CUDA_TRY(cudaMemcpyFromSymbol(&v, dts::g_dts_check_fail, sizeof v));
   CUDA_TRY(cudaMemcpyToSymbol(dts::g_dts_check_fail, &z, sizeof z));
   *out = (uint64_t)v;
+  return DTS_OK;
+}
+
+dts_status dts_pool_release(void) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (const PoolBuf& b : g_pool) cudaFree(b.p);
+  g_pool.clear();
   return DTS_OK;
 }
 

@@ -96,13 +96,14 @@ _lib.dts_last_launch.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 4
 _lib.dts_set_response.argtypes = [_VP, _VP, ctypes.c_int32]
 _lib.dts_check_failures.argtypes = [ctypes.POINTER(ctypes.c_uint64)]
 _lib.dts_enable_peer.argtypes = [ctypes.c_int32]
+_lib.dts_pool_release.argtypes = []
 _lib.dts_status_string.restype = ctypes.c_char_p
 _lib.dts_status_string.argtypes = [ctypes.c_int]
 _lib.dts_last_error.restype = ctypes.c_char_p
 _lib.dts_abi_version.restype = ctypes.c_int32
 
 EXPORTED = ("dts_scene_create", "dts_scene_destroy", "dts_set_response", "dts_table_build", "dts_table_export",
-            "dts_table_size", "dts_check_failures", "dts_enable_peer",
+            "dts_table_size", "dts_check_failures", "dts_enable_peer", "dts_pool_release",
             "dts_hist_cells", "dts_render", "dts_render_rows", "dts_render_host", "dts_sample_debug", "dts_last_launch",
             "dts_status_string", "dts_last_error", "dts_abi_version")
 
@@ -289,6 +290,11 @@ def check_failures() -> int:
     v = ctypes.c_uint64()
     _check(_lib.dts_check_failures(ctypes.byref(v)), "dts_check_failures")
     return int(v.value)
+
+
+def pool_release() -> None:
+    """dts_pool_release: frees the library's pooled device buffers."""
+    _check(_lib.dts_pool_release(), "dts_pool_release")
 
 
 def enable_peer(peer: int) -> None:

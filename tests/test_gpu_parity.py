@@ -211,6 +211,10 @@ SAME_KEY = [
     ("cfg5_global_table_pixelmode",
      lambda: I.small(I.config(5, table_nr=32, table_ns=32), 7, 9, n_bins=120, t1=12.0), 150),
     ("cfg4_global_table", lambda: I.small(I.config(4, table_nr=32, table_ns=32), 24, 24), 64),
+    # the two-stage render with walls and two emitters (the walk stage's wall
+    # bounce draws the second Philox block) and in a sphere with the unwarped camera
+    ("cfg4_split_two_stage", lambda: I.small(I.config(4, direction_mode="split"), 24, 24), 64),
+    ("cfg2_split_two_stage", lambda: I.small(I.config(2, direction_mode="split"), 16, 16, n_bins=64, t1=10.0), 8),
     ("plate_plastic_vanilla", lambda: I.plate_config([(0.7, 0.5, 10.0)], strategy="vanilla"), 100000),
 ]
 
@@ -550,6 +554,8 @@ def test_edge_cases(dts):
     with pytest.raises(dts.DtsError, match="DTS_E_RANGE"):
         dts.Scene(I.as_f32(I.config(5, width=2048, height=2048, n_bins=1024)))
     dts.Scene(I.as_f32(I.config(5, width=2048, height=2048, n_bins=1023))).close()
+    # pooled library buffers can be released at any time (later scenes allocate anew)
+    dts.pool_release()
     # peer access: the current device is a no-op, a device out of range an error
     dts.enable_peer(torch.cuda.current_device())
     with pytest.raises(dts.DtsError, match="DTS_E_INVALID_ARG"):
@@ -788,6 +794,10 @@ TWO_STAGE = [
     ("cfg5_pixelmode", lambda: I.small(I.config(5), 24, 20, n_bins=200, t1=40.0), 64),
     ("cfg3_cell", lambda: I.small(I.config(3), 16, 16, n_bins=64), 16),
     ("cfg5_full_width_rows", lambda: I.config(5, crop=(0, 500, 1024, 506)), 8),
+    ("cfg4_split_walls_two_emitters", lambda: I.small(I.config(4, direction_mode="split", t1=9.0, n_bins=30), 24, 24),
+     64),
+    ("cfg2_split_sphere_unwarped", lambda: I.small(I.config(2, direction_mode="split"), 16, 16, n_bins=64, t1=10.0),
+     8),
 ]
 
 
