@@ -1202,14 +1202,19 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       const float2 Delta = fma2(d, negc, resM2);
       const float2 dq = add2(d, negqd);
       const float2 r2 = fma2(dq, dq, p2);
-      const float2 sv = f2(rsqrtf(fmaxf(Delta.x, 1e-20f)), rsqrtf(fmaxf(Delta.y, 1e-20f)));
+      // (walk stage: every candidate is valid -- it lies on a chord from x, so
+      // d + r <= S_max(x) < R_m - E by the positive connection margin (with its
+      // 1e-3 safety), i.e. r < Delta with Delta >= 1e-3 -- so neither the clamp
+      // nor the mask can change a value there and both are skipped)
+      const float2 sv = WALK ? f2(rsqrtf(Delta.x), rsqrtf(Delta.y))
+                             : f2(rsqrtf(fmaxf(Delta.x, 1e-20f)), rsqrtf(fmaxf(Delta.y, 1e-20f)));
       const float2 ss = mul2(sv, sv);
       const float2 q = mul2(r2, ss);                        // r^2 / Delta
       const float2 ex = fma2(q, k1, mul2(Delta, k2));
       const float2 cube = mul2(ss, sv);                     // s^3 (finite for invalid candidates)
       if (DBG) { dbg->cand_d[2 * j] = d.x; dbg->cand_d[2 * j + 1] = d.y; }
-      e2[2 * j] = q.x < Delta.x ? ex.x : -__int_as_float(0x7f800000);
-      e2[2 * j + 1] = q.y < Delta.y ? ex.y : -__int_as_float(0x7f800000);
+      e2[2 * j] = (WALK || q.x < Delta.x) ? ex.x : -__int_as_float(0x7f800000);
+      e2[2 * j + 1] = (WALK || q.y < Delta.y) ? ex.y : -__int_as_float(0x7f800000);
       s3[2 * j] = cube.x;
       s3[2 * j + 1] = cube.y;
       emax = fmaxf(emax, fmaxf(e2[2 * j], e2[2 * j + 1]));
