@@ -1219,7 +1219,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       s3[2 * j + 1] = cube.y;
       emax = fmaxf(emax, fmaxf(e2[2 * j], e2[2 * j + 1]));
     }
-    if (emax == -__int_as_float(0x7f800000)) emax = 0.0f;  // all invalid: exp2(-inf) = 0, not NaN
+    if (!WALK && emax == -__int_as_float(0x7f800000)) emax = 0.0f;  // all invalid: exp2(-inf) = 0, not NaN
     // R7: weights relative to the largest exponent, w_i = s_i^3 2^(e_i - emax)
     float2 W2 = f2s(0.0f);
 #pragma unroll
@@ -1234,7 +1234,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     if (DBG) {
       for (int i = 0; i < 8; ++i) dbg->cand_wn[i] = W > 0.0f ? e2[i] / W : 0.0f;
     }
-    if (!(W > 0.0f)) {
+    if (!WALK && !(W > 0.0f)) {  // (walk stage: every candidate is valid, W > 0)
       if (DBG) { dbg->event = 4; dbg->terminate = 1; dbg->beta_out = ps.beta; }
       end_reason = DTS_CTR_RIS_INVALID;  // R5
       return false;
