@@ -124,6 +124,7 @@ struct dts_scene {
   int32_t* d_tri_map = nullptr;    // caller -> leaf order, then leaf -> caller order (2 n_tris)
   int num_sms = 0;
   int device = 0;
+  int live[4] = {0, 0, 0, 0};  // pixels [x0, x1) x [y0, y1) outside which every camera ray misses (live_rect)
 };
 
 // ============================================================== EDA table build (fp64, R9/R10)
@@ -267,8 +268,10 @@ struct RenderParams {
   uint64_t s_begin;  // first sample index
   uint64_t n_s;      // samples per cell/pixel in this launch
   uint64_t spp;      // samples per cell (PER_CELL) or per pixel
-  uint32_t npix;     // crop pixels
-  uint32_t cw;       // crop width
+  uint32_t npix;     // pixels of the launch's live rectangle (S.crop[0..1]: its origin; live_rect)
+  uint32_t cw;       // its width
+  uint32_t hw;       // histogram rows' width in pixels (the launch's crop / band)
+  uint32_t ph_base;  // histogram pixel of the live rectangle's first pixel
   uint32_t table_u4; // table size in 16-byte words
   uint32_t spp_div_b, spp_mod_b;  // SPP_PER_PIXEL cell counts (R21)
   const uint32_t* resp_cdf;       // SPP_RESPONSE: bin CDF c_0..c_B (R31)
@@ -370,6 +373,7 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
   cy = fastdiv_divmod(pl, P.fd_cw, cx);
   const uint32_t px = (uint32_t)S.crop[0] + cx, py = (uint32_t)S.crop[1] + cy;
   const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
+  pl = P.ph_base + cy * P.hw + cx;  // the histogram's pixel
   float scale = 1.0f;
   if (S.spp_mode == DTS_SPP_PER_CELL) {
     id = (s * Npix + p) * (uint64_t)B + b;
@@ -616,7 +620,7 @@ struct __align__(16) HandOff {
   uint32_t cell;
   float inv_n;
   int32_t kind_face_e;       // kind | (face + 1) << 8 | e << 16
-  uint32_t pad_;
+  float acc;                 // contribution so far (the start stage's camera vertex; 0 after walk-only vertices)
 };
 static_assert(sizeof(HandOff) == 64, "hand-off records are 64 bytes");
 constexpr uint32_t kHoEmpty = 0xFFFFFFFFu;
@@ -650,7 +654,8 @@ __device__ __forceinline__ void store_handoff(HandOff* ho, const PathCtx& pc) {
   d[0] = make_uint4(__float_as_uint(ps.x.x), __float_as_uint(ps.x.y), __float_as_uint(ps.x.z), __float_as_uint(ps.beta));
   d[1] = make_uint4(__float_as_uint(ps.w.x), __float_as_uint(ps.w.y), __float_as_uint(ps.w.z), pc.k);
   d[2] = make_uint4((uint32_t)__double2loint(ps.resM), (uint32_t)__double2hiint(ps.resM), pc.id_lo, pc.id_hi);
-  d[3] = make_uint4(pc.cell, __float_as_uint(pc.inv_n), (uint32_t)(ps.kind | ((ps.face + 1) << 8) | (ps.e << 16)), 0u);
+  d[3] = make_uint4(pc.cell, __float_as_uint(pc.inv_n), (uint32_t)(ps.kind | ((ps.face + 1) << 8) | (ps.e << 16)),
+                   __float_as_uint(pc.acc));
 }
 
 __device__ __forceinline__ bool load_handoff(const RenderParams& P, uint64_t slot, PathCtx& pc) {
@@ -671,7 +676,7 @@ __device__ __forceinline__ bool load_handoff(const RenderParams& P, uint64_t slo
   ps.kind = (int)(d.z & 0xFFu);
   ps.face = (int)((d.z >> 8) & 0xFFu) - 1;
   ps.e = (int)(d.z >> 16);
-  pc.acc = 0.0f;
+  pc.acc = __uint_as_float(d.w);
   return true;
 }
 
@@ -1084,6 +1089,91 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
     atomicAdd(P.counters + threadIdx.x, (unsigned long long)s_ctr[threadIdx.x]);
 }
 
+// Start stage of the two-stage render of REUSE scenes:
+// every work item's path start (decode, camera ray, R18 miss, start early
+// exit) and its camera vertex (the camera-ray connection and RIS distance; no
+// mixture direction, so no EDA table) run here, one work item per lane and
+// every lane in the same code, instead of one start at a time inside the
+// persistent loop's refills next to medium and wall vertices.  A path that
+// ends at its camera vertex splats here; a surviving one is handed over,
+// with its contribution so far, through a 64-byte HBM record (one slot
+// reservation per warp) to the connect stage (render_darts_kernel<RESUME>),
+// which continues it from bounce 1.  Same path ids, random numbers, vertices
+// and per-path sums as the one-stage kernel.
+#ifndef DTS_BLOCK_START
+#define DTS_BLOCK_START 512
+#endif
+constexpr int kBlockStart = DTS_BLOCK_START;
+template <int SH, int FL>
+__global__ void __launch_bounds__(kBlockStart) start_kernel(const RenderParams P) {
+  static_assert(!(FL & FL_SPLIT), "start stage: REUSE scenes (SPLIT scenes run the walk stage)");
+  __shared__ uint32_t s_ctr[DTS_NUM_COUNTERS];
+  if (threadIdx.x < DTS_NUM_COUNTERS) s_ctr[threadIdx.x] = 0u;
+  __syncthreads();
+  const DevScene& S = P.S;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint32_t c_vert = 0, c_conn = 0, c_samp = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < P.total; base += stride) {
+    const uint64_t my = base + (uint64_t)lane;
+    PathCtx pc;
+    bool active = false;
+    if (my < P.total) active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
+    if (lane == 0) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)(P.total - base < 32u ? P.total - base : 32u));
+    bool done = false;
+    if (active) {
+      const u4 a = philox_rk(pc.id_lo, pc.id_hi, 0u, 0u, S.rk);
+      const u4 b = philox_rk(pc.id_lo, pc.id_hi, 0u, 1u, S.rk);
+      const uint32_t r[8] = {a.a, a.b, a.c, a.d, b.a, b.b, b.c, b.d};
+      float contrib = 0.0f;
+      bool cn = false, wnee = false;
+      int reason = 0;
+      pc.ps.kind = KIND_CAMERA;  // (constant: only the camera branches of the vertex are compiled in)
+      const bool alive = darts_vertex<false, false, SH, FL>(S, nullptr, pc.ps, r, contrib, nullptr, cn, wnee, reason,
+                                                            nullptr, nullptr, nullptr, &c_samp);
+      pc.acc += contrib;
+      ++pc.k;
+      ++c_vert;
+      c_conn += cn ? 1u : 0u;
+      const bool cap = alive && pc.k >= (uint32_t)S.max_bounces;
+      done = !alive || cap;
+      if (done) atomicAdd(s_ctr + (cap ? (int)DTS_CTR_CAP_HITS : reason), 1u);
+    }
+    const bool hand = active && !done;
+    const unsigned hm = __ballot_sync(FULL, hand);
+    if (hm) {
+      unsigned long long nb = 0;
+      if (lane == 0) nb = atomicAdd(P.ho_count, (unsigned long long)__popc(hm));
+      const uint32_t slot = (uint32_t)__shfl_sync(FULL, nb, 0) + __popc(hm & lt_mask);
+      if (hand) store_handoff(P.ho + slot, pc);
+    }
+    const unsigned dmask = __ballot_sync(FULL, done);
+    if (dmask) {
+      const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
+      if (!(P.one_cell_warps &&
+            splat_one_cell(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, nullptr, nullptr,
+                           lane, P.cells)))
+        splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, nullptr, nullptr, lane, P.cells);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c_vert += __shfl_xor_sync(FULL, c_vert, o);
+    c_conn += __shfl_xor_sync(FULL, c_conn, o);
+    c_samp += __shfl_xor_sync(FULL, c_samp, o);
+  }
+  if (lane == 0 && P.counters) {
+    atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
+    atomicAdd(P.counters + DTS_CTR_CAMERA_VERTICES, (unsigned long long)c_vert);  // every vertex here is one
+    atomicAdd(P.counters + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
+    atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c_samp);
+  }
+  __syncthreads();
+  if (P.counters && threadIdx.x < DTS_NUM_COUNTERS && s_ctr[threadIdx.x])
+    atomicAdd(P.counters + threadIdx.x, (unsigned long long)s_ctr[threadIdx.x]);
+}
+
 // ============================================================== vanilla
 // splats a vanilla connection into the bin of its arrival time, weighted by
 // the sensor response W there (RESPONSE scenes); returns 1 for a path sample
@@ -1119,6 +1209,7 @@ __device__ __forceinline__ void vanilla_path(const RenderParams& P, uint32_t pl,
   const uint32_t px = (uint32_t)S.crop[0] + cx, py = (uint32_t)S.crop[1] + cy;
   const uint64_t p = (uint64_t)py * (uint64_t)S.width + px;
   const uint64_t id = s * ((uint64_t)S.width * (uint64_t)S.height) + p;
+  pl = P.ph_base + cy * P.hw + cx;  // the histogram's pixel
   const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
   ++c.paths;
   const u4 a = philox_rk(id_lo, id_hi, 0xFFFFFFFFu, 0u, S.rk);
@@ -1300,10 +1391,12 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
       }
     }
     const uint32_t pw = __shfl_sync(0xffffffffu, pl, 0);   // the batch's pixel (lane 0 is always valid)
+    uint32_t pwx;
+    const uint32_t pwh = P.ph_base + fastdiv_divmod(pw, P.fd_cw, pwx) * P.hw + pwx;  // its histogram pixel
     if (valid) vanilla_path<SH, WALLS, MESH>(P, pl, s, (row && pl == pw) ? row : nullptr, c);
     if (row) {  // flush the batch's row: coalesced REDs of its non-zero bins
       __syncwarp();
-      float* g = P.hist + (size_t)pw * B;
+      float* g = P.hist + (size_t)pwh * B;
       for (uint32_t b = lane; b < B; b += 32) {
         const float v = row[b];
         if (v != 0.0f) {
@@ -1335,6 +1428,12 @@ __global__ void __launch_bounds__(kBlock) render_vanilla_kernel(const RenderPara
     atomicAdd(P.counters + DTS_CTR_SAMPLES, (unsigned long long)c.samp);
     atomicAdd(P.counters + DTS_CTR_REJECTED, (unsigned long long)c.rej);
   }
+}
+
+// culled camera rays (live_rect) are counted as started paths that missed
+__global__ void add_culled_kernel(unsigned long long* counters, unsigned long long n) {
+  atomicAdd(counters + DTS_CTR_PATHS, n);
+  atomicAdd(counters + DTS_CTR_CAMERA_MISS, n);
 }
 
 // ============================================================== kernel selection
@@ -1424,6 +1523,60 @@ struct PickWalk {
   static const void* inf() { return nullptr; }
   static const void* sph() {
     if constexpr ((FL & FL_SPLIT) != 0 && (FL & FL_WALLS) == 0) return (const void*)walk_kernel<DTS_MEDIUM_SPHERE, FL>;
+    return nullptr;
+  }
+};
+
+// start stage + connect stage of REUSE scenes in BOX / SPHERE media, EDA table
+// in shared memory (meshes included)
+template <int FL>
+struct PickStart {
+  static const void* box() {
+    if constexpr ((FL & FL_SPLIT) == 0) return (const void*)start_kernel<DTS_MEDIUM_BOX, FL>;
+    return nullptr;
+  }
+  static const void* inf() { return nullptr; }
+  static const void* sph() {
+    if constexpr ((FL & (FL_SPLIT | FL_WALLS)) == 0) return (const void*)start_kernel<DTS_MEDIUM_SPHERE, FL>;
+    return nullptr;
+  }
+};
+template <int FL>
+struct PickStartMesh {
+  static const void* box() {
+    if constexpr ((FL & FL_SPLIT) == 0) return (const void*)start_kernel<DTS_MEDIUM_BOX, FL | FL_MESH>;
+    return nullptr;
+  }
+  static const void* inf() { return nullptr; }
+  static const void* sph() {
+    if constexpr ((FL & (FL_SPLIT | FL_WALLS)) == 0) return (const void*)start_kernel<DTS_MEDIUM_SPHERE, FL | FL_MESH>;
+    return nullptr;
+  }
+};
+template <int FL>
+struct PickResumeReuse {
+  static const void* box() {
+    if constexpr ((FL & FL_SPLIT) == 0) return (const void*)render_darts_kernel<true, DTS_MEDIUM_BOX, FL, false, true>;
+    return nullptr;
+  }
+  static const void* inf() { return nullptr; }
+  static const void* sph() {
+    if constexpr ((FL & (FL_SPLIT | FL_WALLS)) == 0)
+      return (const void*)render_darts_kernel<true, DTS_MEDIUM_SPHERE, FL, false, true>;
+    return nullptr;
+  }
+};
+template <int FL>
+struct PickResumeMesh {
+  static const void* box() {
+    if constexpr ((FL & FL_SPLIT) == 0)
+      return (const void*)render_darts_kernel<true, DTS_MEDIUM_BOX, FL | FL_MESH, false, true>;
+    return nullptr;
+  }
+  static const void* inf() { return nullptr; }
+  static const void* sph() {
+    if constexpr ((FL & (FL_SPLIT | FL_WALLS)) == 0)
+      return (const void*)render_darts_kernel<true, DTS_MEDIUM_SPHERE, FL | FL_MESH, false, true>;
     return nullptr;
   }
 };
@@ -1637,6 +1790,89 @@ static dts_status upload_mesh(dts_scene* s) {
   return DTS_OK;
 }
 
+// Camera-ray culling: the pixels [x0, x1) x [y0, y1) (absolute image
+// coordinates) outside of which every pinhole ray -- whatever its sub-pixel
+// jitter -- misses the medium's bounds, so its path retires at its start with
+// nothing splatted (a "camera miss", R18).  The medium's image is bounded by
+// projecting a conservative outline: the 8 corners of the (slightly enlarged)
+// box -- the box's image is their convex hull -- or, for a sphere, a polygon of
+// 1024 directions circumscribing the cone of rays that touch the (enlarged)
+// ball.  A pixel is live when its footprint [p, p + 1) meets the outline's
+// bounding interval, widened by 2 pixels on every side (the GPU's fp32 ray and
+// slab test differ from this fp64 bound by ~1e-6 of a pixel's width).  When
+// some outline point lies behind or beside the camera (or the camera is inside
+// or near the medium) every pixel stays live.  Same paths, same random
+// numbers: culled work items are exactly the ones that would miss.
+static void live_rect(const dts_scene_desc& d, int out[4]) {
+  out[0] = 0;
+  out[1] = 0;
+  out[2] = d.width;
+  out[3] = d.height;
+  if (d.camera_kind != DTS_CAMERA_PINHOLE || d.medium_shape == DTS_MEDIUM_INFINITE) return;
+  double cam[3] = {d.cam_pos[0], d.cam_pos[1], d.cam_pos[2]}, la[3] = {d.look_at[0], d.look_at[1], d.look_at[2]},
+         up[3] = {d.up[0], d.up[1], d.up[2]};
+  double fwd[3], right[3], upc[3];
+  vsub(la, cam, fwd);
+  vnorm(fwd);
+  vcross(fwd, up, right);
+  vnorm(right);
+  vcross(right, fwd, upc);
+  const double th = std::tan(0.5 * (double)d.fov_y_deg * M_PI / 180.0), asp = (double)d.width / d.height;
+  double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+  // image-plane coordinates (sx, sy) of direction v; false if v is not well in front
+  auto project = [&](const double v[3]) {
+    const double z = v[0] * fwd[0] + v[1] * fwd[1] + v[2] * fwd[2];
+    const double n = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    if (!(z > 0.05 * n)) return false;
+    const double sx = (v[0] * right[0] + v[1] * right[1] + v[2] * right[2]) / z;
+    const double sy = (v[0] * upc[0] + v[1] * upc[1] + v[2] * upc[2]) / z;
+    xmin = std::min(xmin, sx); xmax = std::max(xmax, sx);
+    ymin = std::min(ymin, sy); ymax = std::max(ymax, sy);
+    return true;
+  };
+  if (d.medium_shape == DTS_MEDIUM_BOX) {
+    double ext = 0.0;
+    for (int i = 0; i < 3; ++i) ext = std::max(ext, (double)d.bmax[i] - (double)d.bmin[i]);
+    const double eps = 1e-4 * ext + 1e-4;
+    for (int c = 0; c < 8; ++c) {
+      double v[3];
+      for (int i = 0; i < 3; ++i) v[i] = (((c >> i) & 1) ? (double)d.bmax[i] + eps : (double)d.bmin[i] - eps) - cam[i];
+      if (!project(v)) return;
+    }
+  } else {
+    double a[3];
+    for (int i = 0; i < 3; ++i) a[i] = (double)d.center[i] - cam[i];
+    const double dist = std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    const double R = (double)d.radius * (1.0 + 1e-4) + 1e-4;
+    if (!(dist > 1.01 * R)) return;
+    for (int i = 0; i < 3; ++i) a[i] /= dist;
+    constexpr int kN = 1024;
+    // the cone's cross-section at unit distance along a is a circle of radius
+    // tan(alpha); the kN-gon of circumradius tan(alpha) / cos(pi / kN) contains it
+    const double ta = (R / std::sqrt(dist * dist - R * R)) / std::cos(M_PI / kN);
+    double b1[3], b2[3], t[3] = {1.0, 0.0, 0.0};
+    if (std::fabs(a[0]) > 0.9) { t[0] = 0.0; t[1] = 1.0; }
+    vcross(a, t, b1);
+    vnorm(b1);
+    vcross(a, b1, b2);
+    for (int k = 0; k < kN; ++k) {
+      const double ph = 2.0 * M_PI * k / kN, c = std::cos(ph) * ta, s = std::sin(ph) * ta;
+      double v[3];
+      for (int i = 0; i < 3; ++i) v[i] = a[i] + c * b1[i] + s * b2[i];
+      if (!project(v)) return;
+    }
+  }
+  // sx = (2 (px + u) / W - 1) tan_half aspect, sy = (1 - 2 (py + u) / H) tan_half
+  const double fx0 = (xmin / (th * asp) + 1.0) * 0.5 * d.width, fx1 = (xmax / (th * asp) + 1.0) * 0.5 * d.width;
+  const double fy0 = (1.0 - ymax / th) * 0.5 * d.height, fy1 = (1.0 - ymin / th) * 0.5 * d.height;
+  auto clampi = [](double v, int hi) { return (int)std::max(0.0, std::min((double)hi, v)); };
+  out[0] = clampi(std::floor(fx0) - 3.0, d.width);
+  out[2] = clampi(std::floor(fx1) + 3.0, d.width);
+  out[1] = clampi(std::floor(fy0) - 3.0, d.height);
+  out[3] = clampi(std::floor(fy1) + 3.0, d.height);
+  if (out[2] <= out[0] || out[3] <= out[1]) out[0] = out[1] = out[2] = out[3] = 0;  // the medium is out of view
+}
+
 static void derive(const dts_scene_desc& d, DevScene& S) {
   memset(&S, 0, sizeof S);
   const double ss = d.sigma_s, sa = d.sigma_a, g = d.g, st = ss + sa;
@@ -1761,6 +1997,7 @@ dts_status dts_scene_create(const dts_scene_desc* desc, dts_scene_t* out) {
   dts_scene* s = new dts_scene();
   s->desc = *desc;
   derive(*desc, s->S);
+  live_rect(*desc, s->live);
   s->num_sms = sms;
   s->device = dev;
   if (cudaMalloc(&s->d_work, sizeof(unsigned long long)) != cudaSuccess) {
@@ -1940,6 +2177,27 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
   P.S = s->S;
   P.S.crop[1] = d.crop[1] + row0;
   P.S.crop[3] = d.crop[1] + row1;
+  // camera-ray culling (live_rect): the launch renders the live part of its
+  // rows; the culled paths are camera misses, counted below (DTS_CULL=0: off)
+  const int hx0 = d.crop[0], hy0 = d.crop[1] + row0, hwid = d.crop[2] - d.crop[0];
+  int lx0 = hx0, ly0 = hy0, lx1 = d.crop[2], ly1 = d.crop[1] + row1;
+  {
+    const char* cu = getenv("DTS_CULL");
+    if (!(cu && cu[0] == '0')) {
+      lx0 = std::max(lx0, s->live[0]);
+      ly0 = std::max(ly0, s->live[1]);
+      lx1 = std::min(lx1, s->live[2]);
+      ly1 = std::min(ly1, s->live[3]);
+    }
+    if (lx1 <= lx0 || ly1 <= ly0) lx1 = lx0 = ly1 = ly0 = 0;
+  }
+  const uint64_t npix_live = (uint64_t)(lx1 - lx0) * (uint64_t)(ly1 - ly0);
+  P.S.crop[0] = lx0;
+  P.S.crop[1] = ly0;
+  P.S.crop[2] = lx1;
+  P.S.crop[3] = ly1;
+  P.hw = (uint32_t)hwid;
+  P.ph_base = npix_live ? (uint32_t)((uint64_t)(ly0 - hy0) * (uint64_t)hwid + (uint64_t)(lx0 - hx0)) : 0u;
   set_round_keys(P.S, seed);
   P.tab = s->d_table;
   P.hist = d_hist;
@@ -1949,14 +2207,14 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
   P.s_begin = sb;
   P.n_s = ns;
   P.spp = spp;
-  P.npix = (uint32_t)npix;
-  P.cw = (uint32_t)(d.crop[2] - d.crop[0]);
+  P.npix = (uint32_t)npix_live;
+  P.cw = (uint32_t)(lx1 - lx0);
   P.div32 = (sb + ns + (uint64_t)d.n_bins <= 0xFFFFFFFFull &&
              npix * ns * ((darts && d.spp_mode == DTS_SPP_PER_CELL) ? (uint64_t)d.n_bins : 1u) <= 0xFFFFFFFFull)
                 ? 1u : 0u;
   P.fd_ns = fastdiv_make((uint32_t)std::min<uint64_t>(ns, 0xFFFFFFFFull));
-  P.fd_npix = fastdiv_make((uint32_t)npix);
-  P.fd_cw = fastdiv_make(P.cw);
+  P.fd_npix = fastdiv_make(std::max<uint32_t>(P.npix, 1u));
+  P.fd_cw = fastdiv_make(std::max<uint32_t>(P.cw, 1u));
   P.fd_b = fastdiv_make((uint32_t)d.n_bins);
   P.one_cell_warps = (d.spp_mode == DTS_SPP_PER_CELL && ns >= 32u) ? 1u : 0u;
   P.spp_div_b = (uint32_t)(spp / (uint64_t)d.n_bins);
@@ -1965,8 +2223,20 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
   // histogram cell indices are 32-bit (dts_scene_create rejects larger crops)
   if (npix * (uint64_t)d.n_bins > 0xFFFFFFFFull) return fail(DTS_E_RANGE, "crop_w * crop_h * n_bins must be < 2^32");
   P.cells = (uint32_t)(npix * (uint64_t)d.n_bins);
+  {  // culled work items: paths started that miss at once (DTS_CTR_PATHS, DTS_CTR_CAMERA_MISS)
+    const uint64_t per_pix = ns * ((darts && d.spp_mode == DTS_SPP_PER_CELL) ? (uint64_t)d.n_bins : 1u);
+    const uint64_t culled = (npix - npix_live) * per_pix;
+    if (culled && P.counters) {
+      add_culled_kernel<<<1, 1, 0, st>>>(P.counters, (unsigned long long)culled);
+      g_last_launches = 1;
+      CUDA_TRY(cudaGetLastError());
+    }
+    if (npix_live == 0) {
+      return DTS_OK;
+    }
+  }
   if (darts) {
-    P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix * (uint64_t)d.n_bins * ns : npix * ns;
+    P.total = (d.spp_mode == DTS_SPP_PER_CELL) ? npix_live * (uint64_t)d.n_bins * ns : npix_live * ns;
     // kernels stage the 16-bit CDF rows and the 8-bit guide rows; stage-1 SPLIT
     // builds stage the CDF only (binary search) to leave room for the stage-1 queues
     const bool split = kStage1Build && d.direction_mode == DTS_DIR_SPLIT;
@@ -2038,21 +2308,38 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     bool wave = d.direction_mode == DTS_DIR_SPLIT && d.n_tris == 0 && d.medium_shape != DTS_MEDIUM_INFINITE;
     const char* wv = getenv("DTS_WAVEFRONT");
     if (wv && wv[0] == '0') wave = false;
-    const void* kwalk = wave ? pick_fl<PickWalk>(d.medium_shape, scene_flags(d)) : nullptr;
-    const void* kres = !wave ? nullptr
-                       : defer ? (smem ? pick_fl<PickResume<true, true>::F>(d.medium_shape, scene_flags(d))
-                                       : pick_fl<PickResume<false, true>::F>(d.medium_shape, scene_flags(d)))
-                               : (smem ? pick_fl<PickResume<true>::F>(d.medium_shape, scene_flags(d))
-                                       : pick_fl<PickResume<false>::F>(d.medium_shape, scene_flags(d)));
+    // REUSE scenes: start stage + connect stage (start_kernel) when the table
+    // is in shared memory and the medium is bounded; DTS_START_STAGE=0/1 forces
+    // the one-stage kernel / the start stage
+    bool start2 = d.direction_mode != DTS_DIR_SPLIT && d.medium_shape != DTS_MEDIUM_INFINITE && smem && !defer;
+    const char* ss = getenv("DTS_START_STAGE");
+    if (ss && ss[0] == '0') start2 = false;
+    const void* kwalk = nullptr;
+    const void* kres = nullptr;
+    int bwalk = kBlockWalk;
+    if (wave) {
+      kwalk = pick_fl<PickWalk>(d.medium_shape, scene_flags(d));
+      kres = defer ? (smem ? pick_fl<PickResume<true, true>::F>(d.medium_shape, scene_flags(d))
+                           : pick_fl<PickResume<false, true>::F>(d.medium_shape, scene_flags(d)))
+                   : (smem ? pick_fl<PickResume<true>::F>(d.medium_shape, scene_flags(d))
+                           : pick_fl<PickResume<false>::F>(d.medium_shape, scene_flags(d)));
+    } else if (start2) {
+      const bool mesh = d.n_tris > 0;
+      kwalk = mesh ? pick_fl<PickStartMesh>(d.medium_shape, scene_flags(d))
+                   : pick_fl<PickStart>(d.medium_shape, scene_flags(d));
+      kres = mesh ? pick_fl<PickResumeMesh>(d.medium_shape, scene_flags(d))
+                  : pick_fl<PickResumeReuse>(d.medium_shape, scene_flags(d));
+      bwalk = kBlockStart;
+    }
     if (!kwalk || !kres) {
       CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
       void* args[] = {&P};
       CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(blk), args, dyn, st));
       CUDA_TRY(cudaGetLastError());
-      g_last_launches = 1;
+      g_last_launches += 1;
     } else {
       int bw = 1;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bw, kwalk, kBlockWalk, 0));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bw, kwalk, bwalk, 0));
       if (bw < 1) bw = 1;
       const uint64_t gw = (uint64_t)s->num_sms * bw;
       // paths per chunk: the hand-off buffer holds one chunk (64 B per path);
@@ -2067,7 +2354,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       // dts_render (slot 0) with more than one chunk: two halves, two streams
       const bool overlap = slot == 0 && chunk < P.total;
       const int halves = overlap ? 2 : 1;
-      const size_t cap = (size_t)chunk + (size_t)gw * (kBlockWalk / 32) * kHoBlock;
+      const size_t cap = (size_t)chunk + (size_t)gw * (bwalk / 32) * kHoBlock;
       if (s->ho_cap[slot] < cap * halves) {
         if (s->d_ho[slot]) {  // (a smaller one: its last use must be over before it is pooled)
           CUDA_TRY(cudaStreamSynchronize(st));
@@ -2115,8 +2402,8 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         if (defer) PC.qover = s->d_qover + (size_t)h * ov1;
         CUDA_TRY(cudaMemsetAsync(wf, 0, 3 * sizeof(unsigned long long), xst));
         void* aw[] = {&PW};
-        CUDA_TRY(cudaLaunchKernel(kwalk, dim3((unsigned)std::min<uint64_t>(gw, (PW.total + kBlockWalk - 1) / kBlockWalk)),
-                                  dim3(kBlockWalk), aw, 0, xst));
+        CUDA_TRY(cudaLaunchKernel(kwalk, dim3((unsigned)std::min<uint64_t>(gw, (PW.total + bwalk - 1) / bwalk)),
+                                  dim3(bwalk), aw, 0, xst));
         void* ac[] = {&PC};
         CUDA_TRY(cudaLaunchKernel(kres, dim3((unsigned)gc), dim3(blk), ac, dyn, xst));
         CUDA_TRY(cudaGetLastError());
@@ -2126,13 +2413,13 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         CUDA_TRY(cudaEventRecord(s->wf_ev[1], xs[1]));
         CUDA_TRY(cudaStreamWaitEvent(st, s->wf_ev[1], 0));
       }
-      g_last_launches = launches;
+      g_last_launches += launches;
     }
     g_last_grid = (int)grid;
     g_last_block = blk;
     g_last_smem = (int)dyn;
   } else {
-    P.total = npix * ns;
+    P.total = npix_live * ns;
     int bps = 1;
     const void* kfn = vanilla_kernel_ptr(d.medium_shape, d.wall_mask != 0u, d.n_tris > 0);
     if (!kfn) return fail(DTS_E_INVALID_ARG, "no render kernel for this scene shape");
@@ -2152,7 +2439,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     void* args[] = {&P};
     CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(kBlock), args, vdyn, st));
     CUDA_TRY(cudaGetLastError());
-    g_last_launches = 1;
+    g_last_launches += 1;
     g_last_grid = (int)grid;
     g_last_block = kBlock;
     g_last_smem = (int)vdyn;

@@ -827,3 +827,110 @@ def test_two_stage_render_equals_one_stage(dts, monkeypatch, name, mk, spp):
             assert d1[k] == d2[k], (k, d1[k], d2[k])
     a, b = h1.double(), h2.double()
     assert float((a - b).norm() / a.norm()) < 1e-5
+
+
+# ------------------------------------------------------------------ camera-ray culling (live_rect)
+CULL = [
+    ("cfg2_full_image", lambda: I.config(2, n_bins=64, t1=10.0), 4, 1),
+    ("cfg2_pixel_mode", lambda: I.config(2, n_bins=64, t1=10.0, spp_mode="pixel"), 64, 1),
+    ("cfg2_offcentre_crop", lambda: I.config(2, n_bins=32, t1=10.0, crop=(40, 3, 64, 30)), 8, 1),
+    ("cfg4_walls_two_emitters", lambda: I.small(I.config(4, t1=9.0, n_bins=30), 48, 48), 64, 1),
+    ("cfg4_vanilla", lambda: I.small(I.config(4, t1=9.0, n_bins=30, strategy="vanilla"), 48, 48), 64, 1),
+    ("cfg6_mesh", lambda: I.small(I.config(6), 48, 48), 32, 1),
+    ("cfg2_split_two_stage", lambda: I.config(2, n_bins=64, t1=10.0, direction_mode="split"), 4, 1),
+    ("cfg2_out_of_view", lambda: I.config(2, n_bins=16, t1=10.0, crop=(0, 0, 6, 6)), 8, None),
+    ("cfg5_no_misses", lambda: I.small(I.config(5), 24, 20, n_bins=100, t1=20.0), 16, 0),
+]
+
+
+@pytest.mark.parametrize("name,mk,spp,extra", CULL, ids=[t[0] for t in CULL])
+def test_camera_culling_is_exact(dts, monkeypatch, name, mk, spp, extra):
+    """Pixels outside the medium's conservative image rectangle are not
+    launched (every ray through them misses, R18): the render must trace
+    exactly the paths of the unculled one -- every counter equal, camera
+    misses included (culled paths are counted as started misses) -- and the
+    same histogram up to fp32 summation order.  A culled launch adds one
+    counter kernel (``extra``; a crop that sees only vacuum, extra None,
+    launches only it)."""
+    c = I.as_f32(mk())
+    sc = _scene(dts, c)
+    monkeypatch.setenv("DTS_CULL", "0")
+    h1, _, c1 = dts.render_to_tensor(sc, spp, c["seed"])
+    torch.cuda.synchronize()
+    n1 = dts.last_launch()["n_launches"]
+    monkeypatch.setenv("DTS_CULL", "1")
+    h2, _, c2 = dts.render_to_tensor(sc, spp, c["seed"])
+    torch.cuda.synchronize()
+    n2 = dts.last_launch()["n_launches"]
+    d1, d2 = dts.counters_dict(c1), dts.counters_dict(c2)
+    print(f"{name}: {d1['paths']} paths, {d1['camera_miss']} camera misses, launches {n1} -> {n2}")
+    assert d1 == d2
+    assert n2 == (1 if extra is None else n1 + extra)
+    a, b = h1.double(), h2.double()
+    if float(a.norm()) > 0:
+        assert float((a - b).norm() / a.norm()) < 1e-5
+    else:
+        assert float(b.norm()) == 0.0
+    sc.close()
+
+
+def test_camera_culling_row_bands(dts, monkeypatch):
+    """Row-band launches (dts_render_rows) cull per band: a band wholly outside
+    the live rectangle launches only the counter kernel; the bands' sum equals
+    the unculled full render."""
+    c = I.as_f32(I.config(2, n_bins=32, t1=10.0))
+    sc = _scene(dts, c)
+    monkeypatch.setenv("DTS_CULL", "0")
+    full, _, cf = dts.render_to_tensor(sc, 8, 5)
+    monkeypatch.setenv("DTS_CULL", "1")
+    h = torch.zeros(sc.hist_shape(), device="cuda")
+    ctr = torch.zeros(dts.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    rowsz = c["width"] * c["n_bins"]
+    for k, (r0, r1) in enumerate([(0, 4), (4, 33), (33, 64)]):
+        sc.render_rows(8, 5, 0, 8, r0, r1, k, h.view(-1)[r0 * rowsz:r1 * rowsz], ctr)
+        torch.cuda.synchronize()
+        if k == 0:
+            assert dts.last_launch()["n_launches"] == 1   # the top rows see only vacuum
+    f, g = full.cpu().numpy(), h.cpu().numpy()
+    assert np.linalg.norm(f - g) <= 1e-5 * np.linalg.norm(f)
+    assert dts.counters_dict(ctr) == dts.counters_dict(cf)
+    sc.close()
+
+
+# ------------------------------------------------------------------ start stage of REUSE scenes (DESIGN.md 5)
+START_STAGE = [
+    ("cfg4_walls_two_emitters", lambda: I.small(I.config(4, t1=9.0, n_bins=30), 48, 48), 64, False),
+    ("cfg4_gate_full_size_crop", lambda: I.config(4, crop=(200, 200, 264, 232)), 64, False),
+    ("cfg2_sphere_unwarped", lambda: I.config(2, n_bins=64, t1=10.0), 8, False),
+    ("cfg2_pixel_mode", lambda: I.config(2, n_bins=64, t1=10.0, spp_mode="pixel"), 64, False),
+    ("cfg6_mesh", lambda: I.small(I.config(6), 48, 48), 32, False),
+    ("cfg2_sphere_with_sq", lambda: I.config(2, n_bins=32, t1=10.0), 8, True),
+]
+
+
+@pytest.mark.parametrize("name,mk,spp,sq", START_STAGE, ids=[t[0] for t in START_STAGE])
+def test_start_stage_equals_one_stage(dts, monkeypatch, name, mk, spp, sq):
+    """REUSE scenes: the start stage (path starts + camera vertices, hand-off
+    with the contribution so far) followed by the connect stage traces the same
+    paths as the one-stage kernel -- every counter equal -- and the same
+    histogram (and per-path squares) up to fp32 summation order.  Small chunks
+    (DTS_WF_CHUNK) exercise the chunk loop and its two-stream overlap."""
+    c = I.as_f32(mk())
+    sc = _scene(dts, c)
+    monkeypatch.setenv("DTS_START_STAGE", "0")
+    h1, s1, c1 = dts.render_to_tensor(sc, spp, c["seed"], with_sq=sq)
+    torch.cuda.synchronize()
+    n1 = dts.last_launch()["n_launches"]
+    monkeypatch.setenv("DTS_START_STAGE", "1")
+    monkeypatch.setenv("DTS_WF_CHUNK", "4096")
+    h2, s2, c2 = dts.render_to_tensor(sc, spp, c["seed"], with_sq=sq)
+    torch.cuda.synchronize()
+    n2 = dts.last_launch()["n_launches"]
+    d1, d2 = dts.counters_dict(c1), dts.counters_dict(c2)
+    print(f"{name}: {d1['vertices']} vertices ({d1['camera_vertices']} camera), launches {n1} -> {n2}")
+    assert n2 >= n1 + 3   # at least two chunks of start + connect kernels
+    assert d1 == d2
+    for a, b in ((h1, h2), (s1, s2)) if sq else ((h1, h2),):
+        a, b = a.double(), b.double()
+        assert float((a - b).norm() / a.norm()) < 1e-5
+    sc.close()
