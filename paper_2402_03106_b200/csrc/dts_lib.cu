@@ -134,7 +134,7 @@ __constant__ double kGLw8[8] = {0.10122853629037706, 0.22238103445337443, 0.3137
                                 0.36268378337836166, 0.3137066458778869,  0.22238103445337443, 0.10122853629037706};
 
 struct TableParams {
-  double sigma_s, sigma_a, sigma_t, D;
+  double sigma_s, sigma_a, sigma_t, D, norm;
   double smin, smax;
   int nr, ns;
 };
@@ -152,24 +152,27 @@ __device__ double e17_integrand(const TableParams& P, double C, double S, double
   if (tc > 0.0 && tc < tend) cuts[nc++] = tc;
   cuts[nc++] = tend;
   const double k = 1.0 / (4.0 * P.D);
-  const double norm = 1.0 / pow(4.0 * 3.14159265358979323846 * P.D, 1.5);
   double total = 0.0;
   for (int part = 0; part + 1 < nc; ++part) {
     const double a = cuts[part], h = (cuts[part + 1] - a) * 0.25;
+    double sum = 0.0;
     for (int panel = 0; panel < 4; ++panel) {
       const double pa = a + panel * h;
       for (int i = 0; i < 8; ++i) {
         const double t = pa + 0.5 * h * (1.0 + kGLx8[i]);
         const double r2 = t * t - 2.0 * t * C * cth + C * C;
         const double dt = S - t;
-        // sigma_s e^{-sigma_t t} Phi(r, dt): one exp of the summed exponents
-        if (dt > 0.0)
-          total += 0.5 * h * kGLw8[i] * P.sigma_s * norm * exp(-P.sigma_t * t - r2 * k / dt - P.sigma_a * dt) /
-                   (dt * sqrt(dt));
+        // e^{-sigma_t t} Phi(r, dt) / norm: one exp of the summed exponents, one
+        // division and one rsqrt (dt^{-3/2} = (1/dt) dt^{-1/2})
+        if (dt > 0.0) {
+          const double idt = 1.0 / dt;
+          sum += kGLw8[i] * exp(-P.sigma_t * t - r2 * k * idt - P.sigma_a * dt) * idt * rsqrt(dt);
+        }
       }
     }
+    total += 0.5 * h * sum;
   }
-  return total;
+  return P.sigma_s * P.norm * total;  // norm = (4 pi D)^{-3/2}
 }
 
 // grid = cells, block = 1024: four threads per cos bin, two of its eight
@@ -594,6 +597,16 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
   }
 }
 
+// splat of the lanes retiring in this iteration (dmask): per-cell launches
+// with >= 32 samples per cell (one_cell_warps) try the one-cell butterfly
+// first.  (A two-cell variant -- a butterfly per distinct cell for up to two
+// cells -- measured 5 % slower on config 4: profiles/ab_r02_start_knobs.log)
+__device__ __forceinline__ void splat_retired(const RenderParams& P, unsigned dmask, bool done, uint32_t cell, float v,
+                                              float v2, float* s_hist, float* s_sq, int lane) {
+  if (!(P.one_cell_warps && splat_one_cell(dmask, done, cell, v, v2, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells)))
+    splat(dmask, done, cell, v, v2, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells);
+}
+
 #ifndef DTS_MINB
 #define DTS_MINB 1
 #endif
@@ -631,7 +644,9 @@ constexpr uint32_t kHoBlock = 32;  // hand-off slots a warp reserves at a time
 // x) + (farthest medium point from any emitter) (may_connect_bound).  A
 // connection lands in the bin only if S >= R_m - E, so a positive margin means
 // it cannot (nor can the wall NEE: C <= that bound).  fp32 safety: 1e-4
-// relative + 1e-3 absolute.
+// relative + 1e-3 absolute.  (In a box the exact maximum of S is at a corner;
+// that bound moved 0.2 % of config 5's vertices into the walk stage and cost
+// more than it saved: profiles/ab_r02_margin_corners.log.)
 template <int SH>
 __device__ __forceinline__ float conn_margin(const DevScene& S, f3 x, double resM) {
   const float resm = d2f(resM - S.dt);
@@ -929,10 +944,7 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
     const unsigned dmask = __ballot_sync(FULL, done);
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
-      if (!(P.one_cell_warps &&
-            splat_one_cell(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane,
-                           P.cells)))
-        splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells);
+      splat_retired(P, dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, s_hist, s_sq, lane);
       if (done) active = false;
     }
   }
@@ -1101,7 +1113,7 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
 // which continues it from bounce 1.  Same path ids, random numbers, vertices
 // and per-path sums as the one-stage kernel.
 #ifndef DTS_BLOCK_START
-#define DTS_BLOCK_START 512
+#define DTS_BLOCK_START 1024
 #endif
 constexpr int kBlockStart = DTS_BLOCK_START;
 template <int SH, int FL>
@@ -1152,10 +1164,7 @@ __global__ void __launch_bounds__(kBlockStart) start_kernel(const RenderParams P
     const unsigned dmask = __ballot_sync(FULL, done);
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
-      if (!(P.one_cell_warps &&
-            splat_one_cell(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, nullptr, nullptr,
-                           lane, P.cells)))
-        splat(dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, P.hist, P.hist_sq, nullptr, nullptr, lane, P.cells);
+      splat_retired(P, dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, nullptr, nullptr, lane);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -2074,6 +2083,7 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
   P.sigma_a = d.sigma_a;
   P.sigma_t = st;
   P.D = 1.0 / (3.0 * ((double)d.sigma_a + (double)d.sigma_s * (1.0 - (double)d.g)));
+  P.norm = 1.0 / std::pow(4.0 * M_PI * P.D, 1.5);
   P.smin = smin;
   P.smax = smax;
   P.nr = nr;
@@ -2338,6 +2348,12 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       CUDA_TRY(cudaGetLastError());
       g_last_launches += 1;
     } else {
+      // connect-stage refills load a hand-off record instead of starting a path:
+      // refill at 4 idle lane-iterations (A/B: config 4 +2.2 %, config 2 +1.5 %,
+      // configs 3 and 5 +0.4 % against 8; profiles/ab_r02_start_knobs.log)
+      uint32_t refill_resume = 4u;
+      const char* rr = getenv("DTS_REFILL_K_RESUME");
+      if (rr && atoi(rr) >= 1 && atoi(rr) <= 4096) refill_resume = (uint32_t)atoi(rr);
       int bw = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bw, kwalk, bwalk, 0));
       if (bw < 1) bw = 1;
@@ -2347,12 +2363,15 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       // rank's share of config 5 is 2^27 paths) so that the second chunk's walk
       // stage fills the first one's tail
       uint64_t chunk = (uint64_t)1 << 27;
-      if (P.total >= ((uint64_t)1 << 21)) chunk = std::min<uint64_t>(chunk, (P.total + 1) / 2);
+      // (the start stage keeps one chunk up to 2^27 paths: one chunk is +5.9 % on
+      // config 2 against two overlapped ones, +0.5 % on config 4)
+      if (P.total >= ((uint64_t)1 << 21) && !start2) chunk = std::min<uint64_t>(chunk, (P.total + 1) / 2);
       const char* ch = getenv("DTS_WF_CHUNK");
       if (ch && atoll(ch) >= 1024) chunk = std::min<uint64_t>((uint64_t)atoll(ch), (uint64_t)1 << 31);
       if (chunk > P.total) chunk = P.total;
       // dts_render (slot 0) with more than one chunk: two halves, two streams
-      const bool overlap = slot == 0 && chunk < P.total;
+      const char* ov = getenv("DTS_WF_OVERLAP");
+      const bool overlap = slot == 0 && chunk < P.total && !(ov && ov[0] == '0');
       const int halves = overlap ? 2 : 1;
       const size_t cap = (size_t)chunk + (size_t)gw * (bwalk / 32) * kHoBlock;
       if (s->ho_cap[slot] < cap * halves) {
@@ -2399,6 +2418,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         RenderParams PC = PW;
         PC.w_base = 0;
         PC.work = wf + 1;
+        PC.refill_k = refill_resume;
         if (defer) PC.qover = s->d_qover + (size_t)h * ov1;
         CUDA_TRY(cudaMemsetAsync(wf, 0, 3 * sizeof(unsigned long long), xst));
         void* aw[] = {&PW};
