@@ -1273,7 +1273,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       f3 xn = fma3(ww, hi, ps.x);
       const int a = face >> 1;
       const float pl = (face & 1) ? S.bmax[a] : S.bmin[a];
-      if (a == 0) xn.x = pl; else if (a == 1) xn.y = pl; else xn.z = pl;  // snap onto the wall
+      xn.x = a == 0 ? pl : xn.x;  // snap onto the wall (selects, not branches)
+      xn.y = a == 1 ? pl : xn.y;
+      xn.z = a == 2 ? pl : xn.z;
       ps.x = xn;
       ps.resM -= f2d(counts * hi);
       ps.kind = KIND_WALL;

@@ -675,9 +675,9 @@ __device__ __forceinline__ void store_handoff(HandOff* ho, const PathCtx& pc) {
 
 __device__ __forceinline__ bool load_handoff(const RenderParams& P, uint64_t slot, PathCtx& pc) {
   const uint4* s = reinterpret_cast<const uint4*>(P.ho + slot);
-  const uint4 a = __ldcs(s + 1);
+  // all four 16-byte loads in flight at once (an empty slot's are harmless)
+  const uint4 a = __ldcs(s + 1), b = __ldcs(s), c = __ldcs(s + 2), d = __ldcs(s + 3);
   if (a.w == kHoEmpty) return false;
-  const uint4 b = __ldcs(s), c = __ldcs(s + 2), d = __ldcs(s + 3);
   PathState& ps = pc.ps;
   ps.x = mk(__uint_as_float(b.x), __uint_as_float(b.y), __uint_as_float(b.z));
   ps.beta = __uint_as_float(b.w);
