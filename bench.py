@@ -298,8 +298,9 @@ def run_gpu(args):
             "clocks": clocks,
             "per_rank": per_rank,
             "e2e": e2e,
-            # per step and rank: the table build + the render's launches (two-stage: 2 per chunk)
-            "gpu_launches": (1 + launch.get("n_launches", 1)) * args.steps * world,
+            # per step and rank: the table build (2 kernels) + the render's launches
+            # (two-stage: 2 per chunk; + 1 counter kernel when camera rays are culled)
+            "gpu_launches": (2 + launch.get("n_launches", 1)) * args.steps * world,
             "launch": launch,
             "counters": counts,
         }

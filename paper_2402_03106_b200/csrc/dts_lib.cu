@@ -96,6 +96,8 @@ struct dts_scene {
   DevScene S;
   uint16_t* d_table = nullptr;
   size_t table_n = 0;
+  double* d_table_f = nullptr;     // table build scratch: fp64 bin integrals (table_f_kernel)
+  size_t table_f_n = 0;
   unsigned long long* d_work = nullptr;  // global work counter
   float* d_hist_host = nullptr;          // dts_render_host scratch
   size_t d_hist_host_n = 0;              // its capacity in floats
@@ -175,19 +177,21 @@ __device__ double e17_integrand(const TableParams& P, double C, double S, double
   return P.sigma_s * P.norm * total;  // norm = (4 pi D)^{-3/2}
 }
 
-// grid = cells, block = 1024: four threads per cos bin, two of its eight
-// cos-direction Gauss-Legendre nodes each (fp64 latency needs the occupancy:
-// 256 cells x 256 threads left 14 warps per SM)
-constexpr int kTableThreads = 1024;
-__global__ void __launch_bounds__(kTableThreads) table_build_kernel(TableParams P, uint16_t* __restrict__ q,
-                                                                   size_t n_total) {
-  __shared__ double F[256];
-  const int cell = blockIdx.x;
+// Two kernels.  table_f_kernel: grid = 4 x cells, block = 256 (a quarter of a
+// cell's 64 cos bins per CTA): four threads per cos bin, two of its eight
+// cos-direction Gauss-Legendre nodes each, summed by two shuffles -> F (fp64,
+// global scratch).  Small CTAs spread the fp64 work evenly over the SMs (one
+// 1024-thread CTA per cell left some SMs with two cells and others with one;
+// DESIGN.md 5.3).  table_cdf_kernel: grid = cells, block = 256: the cell's
+// quantised CDF (one thread, in bin order, as the oracle) and its guide row.
+constexpr int kTableThreads = 256;
+__global__ void __launch_bounds__(kTableThreads) table_f_kernel(TableParams P, double* __restrict__ F) {
+  const int cell = blockIdx.x >> 2;
   const int ir = cell / P.ns, is = cell % P.ns;
   const double ratio = (ir + 0.5) / P.nr;
   const double S = P.smin * pow(P.smax / P.smin, (is + 0.5) / P.ns);
   const double C = ratio * S;
-  const int bin = threadIdx.x >> 2, part = threadIdx.x & 3;
+  const int bin = (blockIdx.x & 3) * 64 + (threadIdx.x >> 2), part = threadIdx.x & 3;
   const double dc = 2.0 / 256.0;
   const double c0 = -1.0 + bin * dc;
   double acc = 0.0;
@@ -195,10 +199,16 @@ __global__ void __launch_bounds__(kTableThreads) table_build_kernel(TableParams 
     acc += 0.5 * dc * kGLw8[n] * e17_integrand(P, C, S, c0 + 0.5 * dc * (1.0 + kGLx8[n]));
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-  if (part == 0) F[bin] = acc;
-  __syncthreads();
-  const int j = threadIdx.x;
+  if (part == 0) F[(size_t)cell * 256 + bin] = acc;
+}
+__global__ void __launch_bounds__(256) table_cdf_kernel(const double* __restrict__ Fg, uint16_t* __restrict__ q,
+                                                        size_t n_total) {
+  __shared__ double F[256];
   __shared__ uint16_t Q[256];
+  const int cell = blockIdx.x;
+  const int j = threadIdx.x;
+  F[j] = Fg[(size_t)cell * 256 + j];
+  __syncthreads();
   if (j == 0) {
     double total = 0.0;
     for (int i = 0; i < 256; ++i) total += F[i];
@@ -207,12 +217,11 @@ __global__ void __launch_bounds__(kTableThreads) table_build_kernel(TableParams 
       double qv = floor(65536.0 * cdf + 0.5);
       if (qv > 65535.0) qv = 65535.0;
       Q[i] = (uint16_t)qv;
-      q[(size_t)cell * 256 + i] = (uint16_t)qv;
       cdf += F[i] / total;
     }
   }
   __syncthreads();
-  if (j >= 256) return;
+  q[(size_t)cell * 256 + j] = Q[j];
   // guide row (acceleration structure of the same inverse transform):
   // guide[g] = largest i with Q[i] <= 256 g
   int lo = 0, hi = 255;
@@ -286,6 +295,7 @@ struct RenderParams {
   uint32_t flush1_at;             // stage-1 queue length that triggers a batch (SPLIT)
   float* qover;                   // DEFER: global overflow queue slots, kQueue x (kJobWords + kJob1Words) per warp
   uint32_t refill_k;              // idle lane-iterations that trigger a refill
+  uint32_t chunk;                 // work items a warp takes from the global counter at a time (32..kChunk)
   uint32_t one_cell_warps;        // 1: per-cell order with >= 32 samples per cell (splat fast path)
   uint32_t div32;                 // 1: work indices, sample indices + B fit 32 bits (fast divisions)
   uint32_t cells;                 // histogram cells of this launch (< 2^32; bounds checks of the check build)
@@ -314,7 +324,7 @@ constexpr int kBlockMesh = DTS_BLOCK_MESH;
 __host__ __device__ constexpr int render_block(bool defer, bool mesh = false) {
   return mesh ? kBlockMesh : (defer ? kBlock : kBlockImm);
 }
-constexpr uint32_t kChunk = 128;
+constexpr uint32_t kChunk = 128;  // work items per global-counter grab (P.chunk: 32..kChunk)
 #ifndef DTS_RIS_WARP
 #define DTS_RIS_WARP 0
 #endif
@@ -463,11 +473,12 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
 
 // ---------------------------------------------------------------- persistent work distribution
 // Hands the lanes of `need` (warp-uniform mask) consecutive work items from the
-// warp's private queue [wn, we), refilled with kChunk items from the global
-// counter `work` (one atomicAdd per chunk); returns this lane's item, ~0 if it
-// gets none (then `exhausted` is set: the global range is used up).
+// warp's private queue [wn, we), refilled with `chunk` (>= 32) items from the
+// global counter `work` (one atomicAdd per chunk); returns this lane's item, ~0
+// if it gets none (then `exhausted` is set: the global range is used up).
 __device__ __forceinline__ uint64_t take_work(unsigned need, int lane, unsigned lt_mask, uint64_t& wn, uint64_t& we,
-                                              bool& exhausted, unsigned long long* work, uint64_t ntotal) {
+                                              bool& exhausted, unsigned long long* work, uint64_t ntotal,
+                                              uint32_t chunk) {
   const uint32_t nidle = __popc(need);
   const uint32_t rank = __popc(need & lt_mask);
   const uint64_t avail = we - wn;
@@ -477,9 +488,9 @@ __device__ __forceinline__ uint64_t take_work(unsigned need, int lane, unsigned 
     wn += nidle;
   } else {
     unsigned long long nb = 0;
-    if (lane == 0) nb = atomicAdd(work, (unsigned long long)kChunk);
+    if (lane == 0) nb = atomicAdd(work, (unsigned long long)chunk);
     nb = __shfl_sync(0xffffffffu, nb, 0);
-    uint64_t ne = nb + kChunk < ntotal ? nb + kChunk : ntotal;
+    uint64_t ne = nb + chunk < ntotal ? nb + chunk : ntotal;
     if (nb >= ntotal) {
       exhausted = true;
       ne = nb;
@@ -853,7 +864,7 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
       // refill; measured slower, off by default)
       unsigned need = idle;
       for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
-        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal);
+        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal, P.chunk);
         const bool starts = my != ~0ull && my < ntotal;
         const unsigned sm = __ballot_sync(FULL, starts);
         if (!RESUME && lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
@@ -1014,7 +1025,7 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
       waste = 0;
       unsigned need = idle;  // (retry paths that retire at their start, as in render_darts_kernel)
       for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
-        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, P.total);
+        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, P.total, P.chunk);
         const bool starts = my != ~0ull && my < P.total;
         const unsigned sm = __ballot_sync(FULL, starts);
         if (lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
@@ -2028,6 +2039,7 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   if (!s) return DTS_OK;
   cudaDeviceSynchronize();
   cudaFree(s->d_table);
+  cudaFree(s->d_table_f);
   cudaFree(s->d_work);
   pool_put(s->device, s->d_hist_host, s->d_hist_host_n * sizeof(float));
   cudaFree(s->d_ctr_host);
@@ -2088,7 +2100,15 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
   P.smax = smax;
   P.nr = nr;
   P.ns = ns;
-  table_build_kernel<<<nr * ns, kTableThreads, 0, (cudaStream_t)stream>>>(P, s->d_table, n);
+  if (s->table_f_n < n) {
+    cudaFree(s->d_table_f);
+    s->d_table_f = nullptr;
+    s->table_f_n = 0;
+    if (cudaMalloc(&s->d_table_f, n * sizeof(double)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(table scratch) failed");
+    s->table_f_n = n;
+  }
+  table_f_kernel<<<nr * ns * 4, kTableThreads, 0, (cudaStream_t)stream>>>(P, s->d_table_f);
+  table_cdf_kernel<<<nr * ns, 256, 0, (cudaStream_t)stream>>>(s->d_table_f, s->d_table, n);
   s->S.table_n = (uint32_t)n;
   CUDA_TRY(cudaGetLastError());
   s->S.nr = nr;
@@ -2276,6 +2296,17 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     // 8: A/B in profiles/ab_r01_refill*.log (configs 6 / 4 +4 % / +2 %, 5 and 3 +0.2 % / +0.4 % vs 16)
     P.refill_k = rk ? (uint32_t)atoi(rk) : 8u;
     if (P.refill_k < 1 || P.refill_k > 4096) P.refill_k = 8u;
+    // warp grabs of kChunk items, but small launches (config 1: 2^18 paths) take
+    // 32 at a time so that every resident warp gets work: about 4 grabs per
+    // resident warp (2048 threads per SM), a multiple of 32 in [32, kChunk]
+    {
+      const uint64_t warps = (uint64_t)s->num_sms * 64u;
+      uint64_t c = P.total / (4u * warps);
+      c = c < 32u ? 32u : (c > kChunk ? kChunk : c & ~(uint64_t)31u);
+      const char* cv = getenv("DTS_GRAB");
+      if (cv && atoi(cv) >= 32 && atoi(cv) <= (int)kChunk) c = (uint64_t)atoi(cv) & ~31u;
+      P.chunk = (uint32_t)c;
+    }
     // a warp flushes at >= flush_at queued jobs and then pushes <= 32 more: the
     // shared slots plus the kQueue global overflow slots must hold flush_at - 1 + 32
     static_assert(kQueue >= 16, "queue too short for a warp's pushes");
