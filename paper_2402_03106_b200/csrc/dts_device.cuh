@@ -208,6 +208,11 @@ __device__ __forceinline__ float one_m_exp(float y) {
   return y < 0.0625f ? ser : big;
 }
 __device__ __forceinline__ float fexp(float x) { return exp2f(x * kLog2e); }
+// 1 - exp(-y) given T = fexp(-y) (the same value one_m_exp computes; one MUFU for both)
+__device__ __forceinline__ float one_m_exp_T(float y, float T) {
+  const float ser = y * fmaf(-y, fmaf(-y, fmaf(-y, fmaf(-y, 1.0f / 120.0f, 1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
+  return y < 0.0625f ? ser : 1.0f - T;
+}
 
 // ----------------------------------------------------------------- frames (R12)
 // Direction at polar angle theta about n: cos theta and sin theta are built
@@ -1139,8 +1144,9 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   }
   const float counts = (S.warped || ps.kind != KIND_CAMERA) ? 1.0f : 0.0f;
   const bool inf_hi = isinf(hi);
-  const float p_m = inf_hi ? 1.0f : one_m_exp(S.sigma_t * (hi - lo));  // E12, R28
-  const float T_m = inf_hi ? 0.0f : fexp(-S.sigma_t * (hi - lo));      // 1 - p_m
+  const float y_m = S.sigma_t * (hi - lo);
+  const float T_m = inf_hi ? 0.0f : fexp(-y_m);                        // 1 - p_m
+  const float p_m = inf_hi ? 1.0f : one_m_exp_T(y_m, T_m);             // E12, R28
   const float u0 = unif(r[0]);
   if (DBG) dbg->p_m = p_m;
   if (rq) rq->need = false;

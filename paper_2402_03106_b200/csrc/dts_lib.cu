@@ -303,6 +303,7 @@ struct RenderParams {
   uint64_t w_base;                // first work index of this launch (two-stage render: the chunk's)
   struct HandOff* ho;             // two-stage render: the chunk's hand-off records
   unsigned long long* ho_count;   // two-stage render: hand-off slots allocated (the connect stage's work count)
+  uint64_t ho_cap;                // two-stage render: hand-off slots of the chunk's buffer (bounds checks)
   FastDiv fd_ns, fd_npix, fd_cw, fd_b;  // division by n_s, npix, cw, n_bins (fastdiv.h)
 };
 
@@ -685,6 +686,7 @@ __device__ __forceinline__ void store_handoff(HandOff* ho, const PathCtx& pc) {
 }
 
 __device__ __forceinline__ bool load_handoff(const RenderParams& P, uint64_t slot, PathCtx& pc) {
+  DTS_CHECK(slot < P.ho_cap);
   const uint4* s = reinterpret_cast<const uint4*>(P.ho + slot);
   // all four 16-byte loads in flight at once (an empty slot's are harmless)
   const uint4 a = __ldcs(s + 1), b = __ldcs(s), c = __ldcs(s + 2), d = __ldcs(s + 3);
@@ -1089,6 +1091,7 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
         hn = nb32 + (nh - avail);
         he = nb32 + kHoBlock;
       }
+      DTS_CHECK(!hand || slot < P.ho_cap);
       if (hand) store_handoff(P.ho + slot, pc);
     }
     if (hand || done) active = false;
@@ -1170,6 +1173,7 @@ __global__ void __launch_bounds__(kBlockStart) start_kernel(const RenderParams P
       unsigned long long nb = 0;
       if (lane == 0) nb = atomicAdd(P.ho_count, (unsigned long long)__popc(hm));
       const uint32_t slot = (uint32_t)__shfl_sync(FULL, nb, 0) + __popc(hm & lt_mask);
+      DTS_CHECK(!hand || slot < P.ho_cap);
       if (hand) store_handoff(P.ho + slot, pc);
     }
     const unsigned dmask = __ballot_sync(FULL, done);
@@ -2446,6 +2450,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         PW.work = wf;
         PW.ho = s->d_ho[slot] + (size_t)h * cap;
         PW.ho_count = wf + 2;
+        PW.ho_cap = cap;
         RenderParams PC = PW;
         PC.w_base = 0;
         PC.work = wf + 1;

@@ -20,10 +20,17 @@ cases = [
     I.small(I.config(3), 8, 8, n_bins=32, t1=8.0),
     I.small(I.config(4), 16, 16),
     I.small(I.config(5), 8, 8, n_bins=50, t1=10.0),
+    I.config(5, crop=(500, 500, 532, 508), n_bins=200, t1=30.0, spp=8),
     I.small(I.config(4, strategy="eda_only"), 8, 8),
     I.small(I.config(3, strategy="da_only", conn_sampling="uniform"), 8, 8, n_bins=32, t1=8.0),
     I.small(I.config(4, strategy="vanilla"), 16, 16),
     I.config(4, crop=(256, 256, 260, 260), table_nr=32, table_ns=32),
+    # camera-ray culling + the start stage (sphere, unwarped camera; meshes), the
+    # two-stage render in a sphere, per-pixel mode with culled pixels
+    I.config(2, n_bins=32, t1=10.0, spp=4),
+    I.small(I.config(6), 24, 24),
+    I.config(2, n_bins=32, t1=10.0, spp=4, direction_mode="split"),
+    I.config(2, n_bins=32, t1=10.0, spp=64, spp_mode="pixel"),
 ]
 for c in cases:
     c = I.as_f32(c)
