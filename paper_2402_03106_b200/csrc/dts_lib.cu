@@ -304,6 +304,8 @@ struct RenderParams {
   struct HandOff* ho;             // two-stage render: the chunk's hand-off records
   unsigned long long* ho_count;   // two-stage render: hand-off slots allocated (the connect stage's work count)
   uint64_t ho_cap;                // two-stage render: hand-off slots of the chunk's buffer (bounds checks)
+  struct HandOff* ho_in;          // three-stage render (SPLIT): the start stage's records the walk stage continues
+  unsigned long long* ho_in_count;  // their count
   FastDiv fd_ns, fd_npix, fd_cw, fd_b;  // division by n_s, npix, cw, n_bins (fastdiv.h)
 };
 
@@ -685,9 +687,13 @@ __device__ __forceinline__ void store_handoff(HandOff* ho, const PathCtx& pc) {
                    __float_as_uint(pc.acc));
 }
 
+__device__ __forceinline__ bool load_handoff_from(const HandOff* rec, PathCtx& pc);
 __device__ __forceinline__ bool load_handoff(const RenderParams& P, uint64_t slot, PathCtx& pc) {
   DTS_CHECK(slot < P.ho_cap);
-  const uint4* s = reinterpret_cast<const uint4*>(P.ho + slot);
+  return load_handoff_from(P.ho + slot, pc);
+}
+__device__ __forceinline__ bool load_handoff_from(const HandOff* rec, PathCtx& pc) {
+  const uint4* s = reinterpret_cast<const uint4*>(rec);
   // all four 16-byte loads in flight at once (an empty slot's are harmless)
   const uint4 a = __ldcs(s + 1), b = __ldcs(s), c = __ldcs(s + 2), d = __ldcs(s + 3);
   if (a.w == kHoEmpty) return false;
@@ -1004,9 +1010,11 @@ constexpr int kBlockWalk = DTS_BLOCK_WALK;
 #define DTS_WALK_INNER 4
 #endif
 constexpr int kWalkInner = DTS_WALK_INNER;
-template <int SH, int FL>
+template <int SH, int FL, bool RESUME = false>
 __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams P) {
   static_assert((FL & FL_SPLIT) && !(FL & FL_MESH), "walk stage: SPLIT scenes without meshes");
+  // RESUME (three-stage render): the work items are the start stage's records
+  const uint64_t ntotal = RESUME ? (uint64_t)*(volatile unsigned long long*)P.ho_in_count : P.total;
   __shared__ uint32_t s_ctr[DTS_NUM_COUNTERS];
   if (threadIdx.x < DTS_NUM_COUNTERS) s_ctr[threadIdx.x] = 0u;
   __syncthreads();
@@ -1027,12 +1035,18 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
       waste = 0;
       unsigned need = idle;  // (retry paths that retire at their start, as in render_darts_kernel)
       for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
-        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, P.total, P.chunk);
-        const bool starts = my != ~0ull && my < P.total;
+        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal, P.chunk);
+        const bool starts = my != ~0ull && my < ntotal;
         const unsigned sm = __ballot_sync(FULL, starts);
-        if (lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
+        if (!RESUME && lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
         if (starts) {
-          active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
+          if (RESUME) {
+            DTS_CHECK(my < P.ho_cap);
+            const HandOff* src = P.ho_in + my;
+            active = load_handoff_from(src, pc);
+          } else {
+            active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
+          }
           margin = conn_margin<SH>(S, pc.ps.x, pc.ps.resM);
           c_camw += (active && margin > 0.0f) ? 1u : 0u;  // its camera vertex runs in the walk stage
         }
@@ -1130,9 +1144,12 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
 #define DTS_BLOCK_START 1024
 #endif
 constexpr int kBlockStart = DTS_BLOCK_START;
-template <int SH, int FL>
+// CAM = false (three-stage render of SPLIT scenes): the path starts only; every
+// started path is handed to the walk stage (walk_kernel<RESUME>), which runs its
+// camera vertex like any other.
+template <int SH, int FL, bool CAM = true>
 __global__ void __launch_bounds__(kBlockStart) start_kernel(const RenderParams P) {
-  static_assert(!(FL & FL_SPLIT), "start stage: REUSE scenes (SPLIT scenes run the walk stage)");
+  static_assert(!CAM || !(FL & FL_SPLIT), "start stage with camera vertices: REUSE scenes");
   __shared__ uint32_t s_ctr[DTS_NUM_COUNTERS];
   if (threadIdx.x < DTS_NUM_COUNTERS) s_ctr[threadIdx.x] = 0u;
   __syncthreads();
@@ -1149,7 +1166,7 @@ __global__ void __launch_bounds__(kBlockStart) start_kernel(const RenderParams P
     if (my < P.total) active = start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
     if (lane == 0) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)(P.total - base < 32u ? P.total - base : 32u));
     bool done = false;
-    if (active) {
+    if (CAM && active) {
       const u4 a = philox_rk(pc.id_lo, pc.id_hi, 0u, 0u, S.rk);
       const u4 b = philox_rk(pc.id_lo, pc.id_hi, 0u, 1u, S.rk);
       const uint32_t r[8] = {a.a, a.b, a.c, a.d, b.a, b.b, b.c, b.d};
@@ -1176,7 +1193,7 @@ __global__ void __launch_bounds__(kBlockStart) start_kernel(const RenderParams P
       DTS_CHECK(!hand || slot < P.ho_cap);
       if (hand) store_handoff(P.ho + slot, pc);
     }
-    const unsigned dmask = __ballot_sync(FULL, done);
+    const unsigned dmask = CAM ? __ballot_sync(FULL, done) : 0u;
     if (dmask) {
       const float v = isfinite(pc.acc) ? pc.acc : 0.0f;
       splat_retired(P, dmask, done, pc.cell, v * pc.inv_n, v * v * pc.inv_n, nullptr, nullptr, lane);
@@ -1187,7 +1204,7 @@ __global__ void __launch_bounds__(kBlockStart) start_kernel(const RenderParams P
     c_conn += __shfl_xor_sync(FULL, c_conn, o);
     c_samp += __shfl_xor_sync(FULL, c_samp, o);
   }
-  if (lane == 0 && P.counters) {
+  if (CAM && lane == 0 && P.counters) {
     atomicAdd(P.counters + DTS_CTR_VERTICES, (unsigned long long)c_vert);
     atomicAdd(P.counters + DTS_CTR_CAMERA_VERTICES, (unsigned long long)c_vert);  // every vertex here is one
     atomicAdd(P.counters + DTS_CTR_CONN_NONEMPTY, (unsigned long long)c_conn);
@@ -1574,6 +1591,34 @@ struct PickStartMesh {
   static const void* inf() { return nullptr; }
   static const void* sph() {
     if constexpr ((FL & (FL_SPLIT | FL_WALLS)) == 0) return (const void*)start_kernel<DTS_MEDIUM_SPHERE, FL | FL_MESH>;
+    return nullptr;
+  }
+};
+// three-stage render of SPLIT scenes: start stage (path starts only) + walk stage
+// continuing the start records
+template <int FL>
+struct PickStartSplit {
+  static const void* box() {
+    if constexpr ((FL & FL_SPLIT) != 0) return (const void*)start_kernel<DTS_MEDIUM_BOX, FL, false>;
+    return nullptr;
+  }
+  static const void* inf() { return nullptr; }
+  static const void* sph() {
+    if constexpr ((FL & FL_SPLIT) != 0 && (FL & FL_WALLS) == 0)
+      return (const void*)start_kernel<DTS_MEDIUM_SPHERE, FL, false>;
+    return nullptr;
+  }
+};
+template <int FL>
+struct PickWalkResume {
+  static const void* box() {
+    if constexpr ((FL & FL_SPLIT) != 0) return (const void*)walk_kernel<DTS_MEDIUM_BOX, FL, true>;
+    return nullptr;
+  }
+  static const void* inf() { return nullptr; }
+  static const void* sph() {
+    if constexpr ((FL & FL_SPLIT) != 0 && (FL & FL_WALLS) == 0)
+      return (const void*)walk_kernel<DTS_MEDIUM_SPHERE, FL, true>;
     return nullptr;
   }
 };
@@ -2362,8 +2407,17 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     const void* kwalk = nullptr;
     const void* kres = nullptr;
     int bwalk = kBlockWalk;
+    // SPLIT scenes: a start stage (path starts only) ahead of the walk stage
+    // (three-stage render) in per-pixel mode, where a start draws two Philox
+    // blocks (R21 offset, path start): A/B config 5 +2.2 %, config 3 (per-cell)
+    // -0.8 % (profiles/ab_r02_three_stage.log); DTS_START_STAGE=0 / 1 forces
+    // it off / on
+    const void* kstart3 = nullptr;
+    const bool want3 = ss ? ss[0] == '1' : d.spp_mode == DTS_SPP_PER_PIXEL;
+    if (wave && want3) kstart3 = pick_fl<PickStartSplit>(d.medium_shape, scene_flags(d));
     if (wave) {
-      kwalk = pick_fl<PickWalk>(d.medium_shape, scene_flags(d));
+      kwalk = kstart3 ? pick_fl<PickWalkResume>(d.medium_shape, scene_flags(d))
+                      : pick_fl<PickWalk>(d.medium_shape, scene_flags(d));
       kres = defer ? (smem ? pick_fl<PickResume<true, true>::F>(d.medium_shape, scene_flags(d))
                            : pick_fl<PickResume<false, true>::F>(d.medium_shape, scene_flags(d)))
                    : (smem ? pick_fl<PickResume<true>::F>(d.medium_shape, scene_flags(d))
@@ -2409,7 +2463,10 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       const bool overlap = slot == 0 && chunk < P.total && !(ov && ov[0] == '0');
       const int halves = overlap ? 2 : 1;
       const size_t cap = (size_t)chunk + (size_t)gw * (bwalk / 32) * kHoBlock;
-      if (s->ho_cap[slot] < cap * halves) {
+      // buffers per half: the connect stage's records, and (three-stage) the
+      // start stage's records after all halves' connect-stage buffers
+      const int nbuf = halves * (kstart3 ? 2 : 1);
+      if (s->ho_cap[slot] < cap * nbuf) {
         if (s->d_ho[slot]) {  // (a smaller one: its last use must be over before it is pooled)
           CUDA_TRY(cudaStreamSynchronize(st));
           pool_put(s->device, s->d_ho[slot], s->ho_cap[slot] * sizeof(HandOff));
@@ -2418,12 +2475,12 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         s->ho_cap[slot] = 0;
         void* p = nullptr;
         size_t got = 0;
-        if (pool_get(s->device, cap * halves * sizeof(HandOff), &p, &got) != cudaSuccess)
+        if (pool_get(s->device, cap * nbuf * sizeof(HandOff), &p, &got) != cudaSuccess)
           return fail(DTS_E_OOM, "cudaMalloc(hand-off buffer) failed");
         s->d_ho[slot] = static_cast<HandOff*>(p);
         s->ho_cap[slot] = got / sizeof(HandOff);
       }
-      if (!s->d_wf && cudaMalloc(&s->d_wf, 3 * (2 + kHostBands) * sizeof(unsigned long long)) != cudaSuccess)
+      if (!s->d_wf && cudaMalloc(&s->d_wf, 5 * (2 + kHostBands) * sizeof(unsigned long long)) != cudaSuccess)
         return fail(DTS_E_OOM, "cudaMalloc(two-stage counters) failed");
       cudaStream_t xs[2] = {st, st};
       if (overlap) {
@@ -2436,6 +2493,12 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         CUDA_TRY(cudaStreamWaitEvent(xs[1], s->wf_ev[0], 0));
       }
       const uint64_t gc = std::min<uint64_t>(grid, (cap + 31) / 32 / (blk / 32) + 1);
+      uint64_t gs3 = 0;
+      if (kstart3) {
+        int b3 = 1;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, kstart3, kBlockStart, 0));
+        gs3 = (uint64_t)s->num_sms * (b3 < 1 ? 1 : b3);
+      }
       CUDA_TRY(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
       int launches = 0;
       int i = 0;
@@ -2443,7 +2506,8 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         const int h = overlap ? (i & 1) : 0;
         cudaStream_t xst = xs[h];
         // counters: slot 0 uses pairs 0 and 1 (halves), slot k >= 1 uses pair k + 1
-        unsigned long long* wf = s->d_wf + 3 * (slot == 0 ? h : slot + 1);
+        // (5 per pair: walk work, connect work, connect slots, start slots, spare)
+        unsigned long long* wf = s->d_wf + 5 * (slot == 0 ? h : slot + 1);
         RenderParams PW = P;
         PW.w_base = w0;
         PW.total = std::min<uint64_t>(chunk, P.total - w0);
@@ -2456,7 +2520,19 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         PC.work = wf + 1;
         PC.refill_k = refill_resume;
         if (defer) PC.qover = s->d_qover + (size_t)h * ov1;
-        CUDA_TRY(cudaMemsetAsync(wf, 0, 3 * sizeof(unsigned long long), xst));
+        CUDA_TRY(cudaMemsetAsync(wf, 0, 4 * sizeof(unsigned long long), xst));
+        if (kstart3) {  // start stage -> the start records; the walk stage continues them
+          RenderParams PS = PW;
+          PS.ho = s->d_ho[slot] + (size_t)(halves + h) * cap;
+          PS.ho_count = wf + 3;
+          void* as[] = {&PS};
+          CUDA_TRY(cudaLaunchKernel(kstart3, dim3((unsigned)std::min<uint64_t>(gs3, (PS.total + kBlockStart - 1) / kBlockStart)),
+                                    dim3(kBlockStart), as, 0, xst));
+          PW.ho_in = PS.ho;
+          PW.ho_in_count = PS.ho_count;
+          PW.refill_k = refill_resume;
+          ++launches;
+        }
         void* aw[] = {&PW};
         CUDA_TRY(cudaLaunchKernel(kwalk, dim3((unsigned)std::min<uint64_t>(gw, (PW.total + bwalk - 1) / bwalk)),
                                   dim3(bwalk), aw, 0, xst));

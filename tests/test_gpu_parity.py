@@ -801,18 +801,22 @@ TWO_STAGE = [
 ]
 
 
+@pytest.mark.parametrize("start", ["1", "0"], ids=["three_stage", "two_stage"])
 @pytest.mark.parametrize("name,mk,spp", TWO_STAGE, ids=[t[0] for t in TWO_STAGE])
-def test_two_stage_render_equals_one_stage(dts, monkeypatch, name, mk, spp):
+def test_two_stage_render_equals_one_stage(dts, monkeypatch, name, mk, spp, start):
     """The walk stage only skips connections that provably cannot land in the
-    bin: the two-stage render (walk kernel + hand-off + connect kernel) traces
-    the same paths as the one-stage kernel -- every counter equal, vertices
-    included -- and the same histogram up to fp32 summation order.  Small
-    chunks (DTS_WF_CHUNK) exercise the chunk loop and its two-stream overlap."""
+    bin: the two-stage render (walk kernel + hand-off + connect kernel) and the
+    three-stage one (a start stage ahead of it, DTS_START_STAGE=1, the default)
+    trace the same paths as the one-stage kernel -- every counter equal,
+    vertices included -- and the same histogram up to fp32 summation order.
+    Small chunks (DTS_WF_CHUNK) exercise the chunk loop and its two-stream
+    overlap."""
     c = I.as_f32(mk())
     sc = _scene(dts, c)
     monkeypatch.setenv("DTS_WAVEFRONT", "0")
     h1, _, c1 = dts.render_to_tensor(sc, spp, c["seed"])
     monkeypatch.setenv("DTS_WAVEFRONT", "1")
+    monkeypatch.setenv("DTS_START_STAGE", start)
     monkeypatch.setenv("DTS_WF_CHUNK", "8192")
     h2, _, c2 = dts.render_to_tensor(sc, spp, c["seed"])
     torch.cuda.synchronize()
