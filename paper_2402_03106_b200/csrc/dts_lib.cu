@@ -2437,10 +2437,12 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       CUDA_TRY(cudaGetLastError());
       g_last_launches += 1;
     } else {
-      // connect-stage refills load a hand-off record instead of starting a path:
-      // refill at 4 idle lane-iterations (A/B: config 4 +2.2 %, config 2 +1.5 %,
-      // configs 3 and 5 +0.4 % against 8; profiles/ab_r02_start_knobs.log)
-      uint32_t refill_resume = 4u;
+      // connect-stage (and three-stage walk-stage) refills load a hand-off record
+      // instead of starting a path: refill on any idle lane (A/B against 8:
+      // config 4 +2.2 %, config 2 +1.5 % (at 4); config 5 +1.0 % at 1 against 4,
+      // configs 2, 3, 4 within 0.2 %: profiles/ab_r02_start_knobs.log,
+      // profiles/ab_r02_refill_resume.log)
+      uint32_t refill_resume = 1u;
       const char* rr = getenv("DTS_REFILL_K_RESUME");
       if (rr && atoi(rr) >= 1 && atoi(rr) <= 4096) refill_resume = (uint32_t)atoi(rr);
       int bw = 1;
