@@ -216,7 +216,12 @@ dts_status dts_scene_destroy(dts_scene_t scene);
 
 /* Builds the EDA direction table of E17 on the device by the
  * deterministic quadrature of R9 in fp64, quantised to 16-bit per-cell CDFs
- * (R10).  desc may be NULL (defaults).  Asynchronous on stream. */
+ * (R10).  desc may be NULL (defaults).  Asynchronous on stream.  (With
+ * DTS_TABLE_OVERLAP=1 in the environment the build is ordered after the work
+ * already enqueued on stream but runs on a scene-internal stream, so that
+ * later work that reads no table -- a render's start / walk stage -- overlaps
+ * it; every library call that reads the table (dts_render*, dts_sample_debug,
+ * dts_table_export) then waits for it.) */
 dts_status dts_table_build(dts_scene_t scene, const dts_table_desc* desc, void* stream);
 /* Copies the quantised table (n_ratio*n_s*256 uint16, cell-major, cell =
  * ir*n_s + is) to host memory.  Synchronous.  n must equal the table size. */

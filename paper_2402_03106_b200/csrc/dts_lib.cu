@@ -98,6 +98,11 @@ struct dts_scene {
   size_t table_n = 0;
   double* d_table_f = nullptr;     // table build scratch: fp64 bin integrals (table_f_kernel)
   size_t table_f_n = 0;
+  // the table build runs on its own stream, forked from the caller's; table
+  // readers (render, debug) wait for tab_ready (table_wait)
+  cudaStream_t tab_stream = nullptr;
+  cudaEvent_t tab_fork = nullptr, tab_ready = nullptr;
+  bool tab_async = false;
   unsigned long long* d_work = nullptr;  // global work counter
   float* d_hist_host = nullptr;          // dts_render_host scratch
   size_t d_hist_host_n = 0;              // its capacity in floats
@@ -128,6 +133,11 @@ struct dts_scene {
   int device = 0;
   int live[4] = {0, 0, 0, 0};  // pixels [x0, x1) x [y0, y1) outside which every camera ray misses (live_rect)
 };
+
+// a stream about to run a kernel that reads the EDA table waits for its build
+static cudaError_t table_wait(dts_scene* s, cudaStream_t st) {
+  return s->tab_async ? cudaStreamWaitEvent(st, s->tab_ready, 0) : cudaSuccess;
+}
 
 // ============================================================== EDA table build (fp64, R9/R10)
 __constant__ double kGLx8[8] = {-0.9602898564975362, -0.7966664774136267, -0.525532409916329, -0.18343464249564978,
@@ -2089,6 +2099,9 @@ dts_status dts_scene_destroy(dts_scene_t s) {
   cudaDeviceSynchronize();
   cudaFree(s->d_table);
   cudaFree(s->d_table_f);
+  if (s->tab_stream) cudaStreamDestroy(s->tab_stream);
+  if (s->tab_fork) cudaEventDestroy(s->tab_fork);
+  if (s->tab_ready) cudaEventDestroy(s->tab_ready);
   cudaFree(s->d_work);
   pool_put(s->device, s->d_hist_host, s->d_hist_host_n * sizeof(float));
   cudaFree(s->d_ctr_host);
@@ -2151,13 +2164,35 @@ dts_status dts_table_build(dts_scene_t s, const dts_table_desc* td, void* stream
   P.ns = ns;
   if (s->table_f_n < n) {
     cudaFree(s->d_table_f);
+  if (s->tab_stream) cudaStreamDestroy(s->tab_stream);
+  if (s->tab_fork) cudaEventDestroy(s->tab_fork);
+  if (s->tab_ready) cudaEventDestroy(s->tab_ready);
     s->d_table_f = nullptr;
     s->table_f_n = 0;
     if (cudaMalloc(&s->d_table_f, n * sizeof(double)) != cudaSuccess) return fail(DTS_E_OOM, "cudaMalloc(table scratch) failed");
     s->table_f_n = n;
   }
-  table_f_kernel<<<nr * ns * 4, kTableThreads, 0, (cudaStream_t)stream>>>(P, s->d_table_f);
-  table_cdf_kernel<<<nr * ns, 256, 0, (cudaStream_t)stream>>>(s->d_table_f, s->d_table, n);
+  // DTS_TABLE_OVERLAP=1: asynchronous with the caller's later work, so that a
+  // render's start / walk stage, which reads no table, overlaps it (A/B: step
+  // time -2 % on configs 1, 2, 6; profiles/ab_r02_table_overlap.log).  Off by
+  // default: the render's CUDA-event time -- the roofline's kernel time -- would
+  // then include waiting for the table.
+  cudaStream_t tst = (cudaStream_t)stream;
+  const char* tov = getenv("DTS_TABLE_OVERLAP");
+  s->tab_async = tov && tov[0] == '1';
+  if (s->tab_async) {
+    if (!s->tab_stream) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&s->tab_stream, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&s->tab_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&s->tab_ready, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(s->tab_fork, (cudaStream_t)stream));  // after the caller's prior work
+    CUDA_TRY(cudaStreamWaitEvent(s->tab_stream, s->tab_fork, 0));
+    tst = s->tab_stream;
+  }
+  table_f_kernel<<<nr * ns * 4, kTableThreads, 0, tst>>>(P, s->d_table_f);
+  table_cdf_kernel<<<nr * ns, 256, 0, tst>>>(s->d_table_f, s->d_table, n);
+  if (s->tab_async) CUDA_TRY(cudaEventRecord(s->tab_ready, tst));
   s->S.table_n = (uint32_t)n;
   CUDA_TRY(cudaGetLastError());
   s->S.nr = nr;
@@ -2432,6 +2467,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     }
     if (!kwalk || !kres) {
       CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
+      CUDA_TRY(table_wait(s, st));
       void* args[] = {&P};
       CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(blk), args, dyn, st));
       CUDA_TRY(cudaGetLastError());
@@ -2539,6 +2575,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         CUDA_TRY(cudaLaunchKernel(kwalk, dim3((unsigned)std::min<uint64_t>(gw, (PW.total + bwalk - 1) / bwalk)),
                                   dim3(bwalk), aw, 0, xst));
         void* ac[] = {&PC};
+        if (i < halves) CUDA_TRY(table_wait(s, xst));  // (once per stream)
         CUDA_TRY(cudaLaunchKernel(kres, dim3((unsigned)gc), dim3(blk), ac, dyn, xst));
         CUDA_TRY(cudaGetLastError());
         launches += 2;
@@ -2687,6 +2724,7 @@ dts_status dts_sample_debug(dts_scene_t s, int32_t n, const dts_debug_in* d_in, 
   DevScene S = s->S;
   set_round_keys(S, 0);
   void* args[] = {&S, &tab, &n, &d_in, &d_out};
+  if (s->d_table) CUDA_TRY(table_wait(s, (cudaStream_t)stream));
   CUDA_TRY(cudaLaunchKernel(kfn, dim3((n + 127) / 128), dim3(128), args, 0, (cudaStream_t)stream));
   CUDA_TRY(cudaGetLastError());
   return DTS_OK;

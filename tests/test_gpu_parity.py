@@ -938,3 +938,31 @@ def test_start_stage_equals_one_stage(dts, monkeypatch, name, mk, spp, sq):
         a, b = a.double(), b.double()
         assert float((a - b).norm() / a.norm()) < 1e-5
     sc.close()
+
+
+def test_table_overlap_equals_in_stream_build(dts, monkeypatch):
+    """DTS_TABLE_OVERLAP=1 builds the table on a scene-internal stream that the
+    table readers wait for: the renders (start stage, three-stage SPLIT) and a
+    debug batch see the finished table -- the same counters and histograms as
+    with the build on the caller's stream, across repeated rebuilds."""
+    for mk in (lambda: I.small(I.config(4, t1=9.0, n_bins=30), 32, 32),
+               lambda: I.small(I.config(5), 24, 20, n_bins=100, t1=20.0)):
+        c = I.as_f32(mk())
+        sc = dts.Scene(c)
+        monkeypatch.setenv("DTS_TABLE_OVERLAP", "0")
+        sc.table_build()
+        h1, _, c1 = dts.render_to_tensor(sc, 16, c["seed"])
+        torch.cuda.synchronize()
+        monkeypatch.setenv("DTS_TABLE_OVERLAP", "1")
+        for _ in range(3):
+            sc.table_build()
+            h2, _, c2 = dts.render_to_tensor(sc, 16, c["seed"])
+        torch.cuda.synchronize()
+        assert dts.counters_dict(c1) == dts.counters_dict(c2)
+        a, b = h1.double(), h2.double()
+        assert float((a - b).norm() / a.norm()) < 1e-5
+        sc.table_build()
+        out = dts.debug(sc, I.debug_records(c, 256, seed=5))
+        torch.cuda.synchronize()
+        assert np.isfinite(np.asarray(out["p_mix"])).all()
+        sc.close()
