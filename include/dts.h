@@ -266,9 +266,17 @@ size_t dts_hist_cells(dts_scene_t scene);
  * 2^27 paths, and at least two for launches of >= 2^21 paths; DTS_WF_CHUNK
  * overrides; dts_render holds two chunks' worth -- 17 GB for config 5 -- and
  * overlaps consecutive chunks on an internal stream ordered after `stream`;
- * each row band holds one chunk's worth and runs its chunks in order).  The paths, counters and histogram are those of the one-stage
- * kernel (DTS_WAVEFRONT=0 selects it); failing to allocate the buffer is
- * DTS_E_OOM. */
+ * each row band holds one chunk's worth and runs its chunks in order).  In
+ * per-pixel mode a start kernel decodes the paths ahead of the walk kernel
+ * (three stages, a second buffer of the same size).  REUSE
+ * scenes in BOX / SPHERE media with the table in shared memory render in two
+ * stages too: a start kernel runs every path's start and camera vertex, a
+ * connect kernel continues the survivors (one chunk up to 2^27 paths).  Pixels
+ * whose every camera ray misses the medium are not launched (camera-ray
+ * culling); they are counted as started paths that missed.
+ * The paths, counters and histogram are those of the one-stage kernel
+ * (DTS_WAVEFRONT=0, DTS_START_STAGE=0, DTS_CULL=0 select it); failing to
+ * allocate a buffer is DTS_E_OOM. */
 dts_status dts_render(dts_scene_t scene, uint64_t spp, uint64_t seed, uint64_t sample_begin,
                       uint64_t sample_end, float* d_hist, float* d_hist_sq, uint64_t* d_counters,
                       void* stream);
