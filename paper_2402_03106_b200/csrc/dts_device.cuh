@@ -822,7 +822,10 @@ __device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_
 // *walk_margin carries the margin in and its lower bound after the step out
 // (margin - (1 + counts) d: see walk_kernel); while it stays positive the early
 // exit test is skipped (R_M - E - C >= R_m - E - S_max > 0).
-template <bool DBG, bool SMEM, int SH, int FL, bool DEFER = false, bool WALK = false>
+// NOCAM: the caller never passes a camera vertex (the connect stage of a REUSE
+// scene's start-stage render: the start stage ran every camera vertex), so the
+// camera branches (and R17) are compiled out.
+template <bool DBG, bool SMEM, int SH, int FL, bool DEFER = false, bool WALK = false, bool NOCAM = false>
 __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* __restrict__ tab, PathState& ps,
                                              const uint32_t (&r)[8], float& contrib, dts_debug_out* dbg,
                                              bool& conn_nonempty, bool& wall_nee, int& end_reason,
@@ -843,6 +846,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   f3 wc, ww;
   float wconn = 1.0f;
   const float resM = d2f(ps.resM);
+  const bool cam = !NOCAM && ps.kind == KIND_CAMERA;  // (ps.kind changes only in step 1 below)
 
   // ---- SPLIT render kernel: queue this vertex's whole connection stage (stage 1) ----
   // A medium vertex whose connection can reach its bin at all (may_connect_bound)
@@ -874,7 +878,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
   }
 
   // ---- step 2: direction ----
-  if (ps.kind == KIND_CAMERA) {
+  if (cam) {
     wc = ww = ps.w;
     if (DBG) {
       dbg->tech = 2;
@@ -997,7 +1001,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     if (tri >= 0) { hi = tm; hit = HIT_SURF; face = tri; }
   }
   // render kernel: non-empty connections of medium/wall vertices are queued (df)
-  const bool defer = DEFER && !DBG && ps.kind != KIND_CAMERA;
+  const bool defer = DEFER && !DBG && !cam;
 
   bool want_job = false;
   float job_dlo = 0.0f, job_width = 0.0f;
@@ -1030,7 +1034,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     float t = 0.0f, pt = 0.0f, Ssamp = 0.0f;
     float pSt = 0.0f;  // S - t (= r2 on the ellipse)
     bool ok = false;
-    if (!(S.warped == 0 && ps.kind == KIND_CAMERA)) {
+    if (!(S.warped == 0 && cam)) {
       const SRange rg = conn_range(S, ps.x, wc, xe, C, q, clo, chi, ps.resM);
       if (DBG) { dbg->S_lo = C + rg.dlo; dbg->S_hi = C + rg.dhi; }
       if (rg.width > 0.0f && defer) {
@@ -1101,7 +1105,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
       contrib += c;
       if (nsamp && c != 0.0f) ++*nsamp;
       if (DBG) {
-        dbg->S = (S.warped == 0 && ps.kind == KIND_CAMERA) ? t + r2 : Ssamp;
+        dbg->S = (S.warped == 0 && cam) ? t + r2 : Ssamp;
         dbg->t = t;
         dbg->x_ell[0] = xell.x; dbg->x_ell[1] = xell.y; dbg->x_ell[2] = xell.z;
         dbg->p_t = pt;
@@ -1142,7 +1146,7 @@ __device__ __forceinline__ bool darts_vertex(const DevScene& S, const uint16_t* 
     end_reason = DTS_CTR_ESCAPES;
     return false;
   }
-  const float counts = (S.warped || ps.kind != KIND_CAMERA) ? 1.0f : 0.0f;
+  const float counts = (S.warped || !cam) ? 1.0f : 0.0f;
   const bool inf_hi = isinf(hi);
   const float y_m = S.sigma_t * (hi - lo);
   const float T_m = inf_hi ? 0.0f : fexp(-y_m);                        // 1 - p_m

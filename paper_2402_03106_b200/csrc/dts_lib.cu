@@ -193,7 +193,7 @@ __device__ double e17_integrand(const TableParams& P, double C, double S, double
 // global scratch).  Small CTAs spread the fp64 work evenly over the SMs (one
 // 1024-thread CTA per cell left some SMs with two cells and others with one;
 // DESIGN.md 5.3).  table_cdf_kernel: grid = cells, block = 256: the cell's
-// quantised CDF (one thread, in bin order, as the oracle) and its guide row.
+// quantised CDF (serial sums in bin order, as the oracle) and its guide row.
 constexpr int kTableThreads = 256;
 __global__ void __launch_bounds__(kTableThreads) table_f_kernel(TableParams P, double* __restrict__ F) {
   const int cell = blockIdx.x >> 2;
@@ -213,22 +213,38 @@ __global__ void __launch_bounds__(kTableThreads) table_f_kernel(TableParams P, d
 }
 __global__ void __launch_bounds__(256) table_cdf_kernel(const double* __restrict__ Fg, uint16_t* __restrict__ q,
                                                         size_t n_total) {
-  __shared__ double F[256];
+  __shared__ double F[256], Cd[256];
+  __shared__ double s_total;
   __shared__ uint16_t Q[256];
   const int cell = blockIdx.x;
   const int j = threadIdx.x;
   F[j] = Fg[(size_t)cell * 256 + j];
   __syncthreads();
+  // the oracle's operations in its order (total, then cdf_i = sum_{k<i} F_k / total
+  // accumulated in bin order); only the divisions, which are independent, and the
+  // quantisation run on all 256 threads (the serial chains are fp64 adds only)
   if (j == 0) {
     double total = 0.0;
     for (int i = 0; i < 256; ++i) total += F[i];
+    s_total = total;
+  }
+  __syncthreads();
+  const double pj = F[j] / s_total;
+  __syncthreads();
+  F[j] = pj;
+  __syncthreads();
+  if (j == 0) {
     double cdf = 0.0;
     for (int i = 0; i < 256; ++i) {
-      double qv = floor(65536.0 * cdf + 0.5);
-      if (qv > 65535.0) qv = 65535.0;
-      Q[i] = (uint16_t)qv;
-      cdf += F[i] / total;
+      Cd[i] = cdf;
+      cdf += F[i];
     }
+  }
+  __syncthreads();
+  {
+    double qv = floor(65536.0 * Cd[j] + 0.5);
+    if (qv > 65535.0) qv = 65535.0;
+    Q[j] = (uint16_t)qv;
   }
   __syncthreads();
   q[(size_t)cell * 256 + j] = Q[j];
@@ -334,8 +350,15 @@ constexpr int kBlockImm = DTS_BLOCK_IMM;
 #define DTS_BLOCK_MESH 768
 #endif
 constexpr int kBlockMesh = DTS_BLOCK_MESH;
-__host__ __device__ constexpr int render_block(bool defer, bool mesh = false) {
-  return mesh ? kBlockMesh : (defer ? kBlock : kBlockImm);
+// connect stage of a REUSE scene's start-stage render (no camera vertices):
+// 32 warps at <= 64 registers (A/B against 896: config 2 +0.7 %, config 4 +0.8 %,
+// profiles/ab_r02v_nocam_block.log)
+#ifndef DTS_BLOCK_RESUME_REUSE
+#define DTS_BLOCK_RESUME_REUSE 1024
+#endif
+constexpr int kBlockResReuse = DTS_BLOCK_RESUME_REUSE;
+__host__ __device__ constexpr int render_block(bool defer, bool mesh = false, bool resume_reuse = false) {
+  return mesh ? kBlockMesh : (defer ? kBlock : (resume_reuse ? kBlockResReuse : kBlockImm));
 }
 constexpr uint32_t kChunk = 128;  // work items per global-counter grab (P.chunk: 32..kChunk)
 #ifndef DTS_RIS_WARP
@@ -489,9 +512,19 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
 // warp's private queue [wn, we), refilled with `chunk` (>= 32) items from the
 // global counter `work` (one atomicAdd per chunk); returns this lane's item, ~0
 // if it gets none (then `exhausted` is set: the global range is used up).
+#ifndef DTS_HO_PREFETCH
+#define DTS_HO_PREFETCH 1
+#endif
+// L2 prefetch of a byte range by the TMA unit (no registers, no completion to wait for)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// (pf: the hand-off records when the work items are hand-off slots (64 bytes
+// each): a grab prefetches its records into L2, so the later refills from the
+// chunk load them from L2 instead of HBM)
 __device__ __forceinline__ uint64_t take_work(unsigned need, int lane, unsigned lt_mask, uint64_t& wn, uint64_t& we,
                                               bool& exhausted, unsigned long long* work, uint64_t ntotal,
-                                              uint32_t chunk) {
+                                              uint32_t chunk, const char* pf = nullptr) {
   const uint32_t nidle = __popc(need);
   const uint32_t rank = __popc(need & lt_mask);
   const uint64_t avail = we - wn;
@@ -517,6 +550,7 @@ __device__ __forceinline__ uint64_t take_work(unsigned need, int lane, unsigned 
     const uint64_t nq = nb + (nidle - avail);
     wn = nq < ne ? nq : ne;
     we = ne;
+    if (DTS_HO_PREFETCH && pf && lane == 0 && ne > nb) prefetch_l2_bulk(pf + nb * 64u, (uint32_t)((ne - nb) * 64u));
   }
   return ((need >> lane) & 1u) ? my : ~0ull;
 }
@@ -725,8 +759,12 @@ __device__ __forceinline__ bool load_handoff_from(const HandOff* rec, PathCtx& p
 }
 
 template <bool SMEM, int SH, int FL, bool DEFER, bool RESUME = false>
-__global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_MINB) render_darts_kernel(const RenderParams P) {
+__global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0, RESUME && (FL & FL_SPLIT) == 0), DTS_MINB)
+    render_darts_kernel(const RenderParams P) {
   constexpr bool WALLS = (FL & FL_WALLS) != 0;
+  // the connect stage of a REUSE scene resumes paths after the start stage's
+  // camera vertex: no camera vertices (SPLIT scenes hand paths over at any vertex)
+  constexpr bool kNoCam = RESUME && (FL & FL_SPLIT) == 0;
   // RESUME (connect stage): the work items are the walk stage's hand-off slots
   const uint64_t ntotal = RESUME ? (uint64_t)*(volatile unsigned long long*)P.ho_count : P.total;
   extern __shared__ __align__(16) uint16_t s_dyn[];
@@ -882,11 +920,13 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
       // refill; measured slower, off by default)
       unsigned need = idle;
       for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
-        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal, P.chunk);
+        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal, P.chunk,
+                                      RESUME ? reinterpret_cast<const char*>(P.ho) : nullptr);
         const bool starts = my != ~0ull && my < ntotal;
         const unsigned sm = __ballot_sync(FULL, starts);
         if (!RESUME && lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
         if (starts) active = RESUME ? load_handoff(P, my, pc) : start_path<SH, FL>(P, P.w_base + my, pc, s_ctr);
+        DTS_CHECK(!(kNoCam && active && pc.ps.kind == KIND_CAMERA));
         need = __ballot_sync(FULL, ((need >> lane) & 1u) && !active);
       }
     }
@@ -929,7 +969,7 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
       if (run) {
         // vertex mix of the roofline basis (bench/opcounts.json): camera vertices
         // (once per walk, shared-memory counter), wall / surface vertices
-        if (pc.ps.kind == KIND_CAMERA) atomicAdd(s_ctr + DTS_CTR_CAMERA_VERTICES, 1u);
+        if (!kNoCam && pc.ps.kind == KIND_CAMERA) atomicAdd(s_ctr + DTS_CTR_CAMERA_VERTICES, 1u);
         if (WALLS || (FL & FL_MESH)) c_wall += (pc.ps.kind == KIND_WALL || pc.ps.kind == KIND_SURF) ? 1u : 0u;
         const u4 a = philox_rk(pc.id_lo, pc.id_hi, pc.k, 0u, S.rk);
         const u4 b = philox_rk(pc.id_lo, pc.id_hi, pc.k, 1u, S.rk);
@@ -938,7 +978,7 @@ __global__ void __launch_bounds__(render_block(DEFER, (FL & FL_MESH) != 0), DTS_
         df.act = act_r;
         df.cell = pc.cell;
         df.inv_n = pc.inv_n;
-        alive = darts_vertex<false, SMEM, SH, FL, DEFER>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
+        alive = darts_vertex<false, SMEM, SH, FL, DEFER, false, kNoCam>(S, tab, pc.ps, r, contrib, nullptr, cn, wnee, reason,
                                                          DEFER ? &df : nullptr, &pushed, kRisWarp ? &rq : nullptr,
                                                          &c_samp, &pushed1);
       }
@@ -1045,7 +1085,8 @@ __global__ void __launch_bounds__(kBlockWalk, 1) walk_kernel(const RenderParams 
       waste = 0;
       unsigned need = idle;  // (retry paths that retire at their start, as in render_darts_kernel)
       for (int t = 0; t < kStartTries && need && !exhausted; ++t) {
-        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal, P.chunk);
+        const uint64_t my = take_work(need, lane, lt_mask, wn, we, exhausted, P.work, ntotal, P.chunk,
+                                      RESUME ? reinterpret_cast<const char*>(P.ho_in) : nullptr);
         const bool starts = my != ~0ull && my < ntotal;
         const unsigned sm = __ballot_sync(FULL, starts);
         if (!RESUME && lane == 0 && sm) atomicAdd(s_ctr + DTS_CTR_PATHS, (uint32_t)__popc(sm));
@@ -2530,7 +2571,9 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         CUDA_TRY(cudaEventRecord(s->wf_ev[0], st));  // fork: the aux stream starts after the caller's prior work
         CUDA_TRY(cudaStreamWaitEvent(xs[1], s->wf_ev[0], 0));
       }
-      const uint64_t gc = std::min<uint64_t>(grid, (cap + 31) / 32 / (blk / 32) + 1);
+      // (the connect stage of a REUSE scene has its own block size: render_block)
+      const int bres = render_block(defer, d.n_tris > 0, !wave);
+      const uint64_t gc = std::min<uint64_t>(grid, (cap + 31) / 32 / (bres / 32) + 1);
       uint64_t gs3 = 0;
       if (kstart3) {
         int b3 = 1;
@@ -2576,7 +2619,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
                                   dim3(bwalk), aw, 0, xst));
         void* ac[] = {&PC};
         if (i < halves) CUDA_TRY(table_wait(s, xst));  // (once per stream)
-        CUDA_TRY(cudaLaunchKernel(kres, dim3((unsigned)gc), dim3(blk), ac, dyn, xst));
+        CUDA_TRY(cudaLaunchKernel(kres, dim3((unsigned)gc), dim3(bres), ac, dyn, xst));
         CUDA_TRY(cudaGetLastError());
         launches += 2;
       }
@@ -2587,7 +2630,7 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
       g_last_launches += launches;
     }
     g_last_grid = (int)grid;
-    g_last_block = blk;
+    g_last_block = (kwalk && kres) ? render_block(defer, d.n_tris > 0, !wave) : blk;  // (the connect stage's)
     g_last_smem = (int)dyn;
   } else {
     P.total = npix_live * ns;
