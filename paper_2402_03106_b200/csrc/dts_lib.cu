@@ -512,8 +512,11 @@ __device__ __forceinline__ bool start_path(const RenderParams& P, uint64_t widx,
 // warp's private queue [wn, we), refilled with `chunk` (>= 32) items from the
 // global counter `work` (one atomicAdd per chunk); returns this lane's item, ~0
 // if it gets none (then `exhausted` is set: the global range is used up).
+// (hand-off prefetch on grabs: measured -0.35 % on config 5, within +-0.3 % on
+// configs 2, 3, 4 -- the refill loads were not what stalls the connect stage;
+// off by default: profiles/ab_r02x_ho_prefetch.log)
 #ifndef DTS_HO_PREFETCH
-#define DTS_HO_PREFETCH 1
+#define DTS_HO_PREFETCH 0
 #endif
 // L2 prefetch of a byte range by the TMA unit (no registers, no completion to wait for)
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
