@@ -323,6 +323,7 @@ struct RenderParams {
   uint32_t refill_k;              // idle lane-iterations that trigger a refill
   uint32_t chunk;                 // work items a warp takes from the global counter at a time (32..kChunk)
   uint32_t one_cell_warps;        // 1: per-cell order with >= 32 samples per cell (splat fast path)
+  uint32_t splat_plain;           // 2: one RED per retiring lane (default); 0 / 1: in-warp aggregation (-DDTS_SPLAT_AGG=1 builds)
   uint32_t div32;                 // 1: work indices, sample indices + B fit 32 bits (fast divisions)
   uint32_t cells;                 // histogram cells of this launch (< 2^32; bounds checks of the check build)
   uint32_t van_rows;              // vanilla: 1 = pixel-major batches splat into per-warp shared-memory rows
@@ -596,11 +597,12 @@ __device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t 
 
 // ---------------------------------------------------------------- histogram splat (step 4)
 // Per-bin dedicated paths: a retiring path adds its whole
-// contribution to its own cell.  Lanes that retire in the same iteration on the
-// same cell (consecutive sample ids of one cell) are combined first
-// (__match_any_sync + shuffles, one RED per distinct cell and warp); the RED
-// goes to a shared-memory copy of the histogram when the CTA privatises it
-// (small histograms, flushed once at kernel end), else to HBM/L2.
+// contribution to its own cell by a RED (splat_retired below): to a shared-
+// memory copy of the histogram when the CTA privatises it (small histograms,
+// flushed once at kernel end), else to HBM/L2.  The in-warp aggregation that
+// follows is the DTS_SPLAT_AGG=1 build option (and the deferred-connection
+// kernels' flush): lanes that retire in the same iteration on the same cell are
+// combined first (__match_any_sync + shuffles, one RED per distinct cell and warp).
 // Every retiring lane of the warp on one cell (per-cell issue order with >= 32
 // samples per cell: a warp's paths are mostly consecutive samples of one cell):
 // a 5-step butterfly and one RED.  Called by all 32 lanes of a converged warp;
@@ -658,14 +660,37 @@ __device__ __forceinline__ void splat(unsigned dmask, bool done, uint32_t cell, 
   }
 }
 
-// splat of the lanes retiring in this iteration (dmask): per-cell launches
-// with >= 32 samples per cell (one_cell_warps) try the one-cell butterfly
-// first.  (A two-cell variant -- a butterfly per distinct cell for up to two
-// cells -- measured 5 % slower on config 4: profiles/ab_r02_start_knobs.log)
+// splat of the lanes retiring in this iteration (dmask): one RED per retiring
+// lane with a non-zero contribution, to the CTA's private histogram or to L2.
+// Plain REDs beat the in-warp aggregation (one-cell butterfly, then
+// __match_any_sync + shuffles, one RED per distinct cell) on every config:
+// config 4 +4.9 %, config 2 +4.1 %, config 6 +1.3 %, config 3 +0.9 %, config 5
+// +0.2 %, config 1 even (profiles/ab_r02z_splat.log) -- the aggregation cost
+// ~1.9 warp-instructions per vertex at SIMT 11 in config 4's connect stage,
+// while the L2 absorbs same-address REDs of paths that retire at different
+// times.  -DDTS_SPLAT_AGG=1 builds keep the aggregation, selected per launch
+// by DTS_SPLAT_PLAIN=0 (aggregate) / 1 (butterfly, else plain) / 2 (plain).
+// (A two-cell butterfly variant measured 5 % slower than the aggregation on
+// config 4: profiles/ab_r02_start_knobs.log)
+#ifndef DTS_SPLAT_AGG
+#define DTS_SPLAT_AGG 0
+#endif
 __device__ __forceinline__ void splat_retired(const RenderParams& P, unsigned dmask, bool done, uint32_t cell, float v,
                                               float v2, float* s_hist, float* s_sq, int lane) {
-  if (!(P.one_cell_warps && splat_one_cell(dmask, done, cell, v, v2, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells)))
-    splat(dmask, done, cell, v, v2, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells);
+  if (DTS_SPLAT_AGG && P.splat_plain < 2u) {
+    if (P.one_cell_warps && splat_one_cell(dmask, done, cell, v, v2, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells))
+      return;
+    if (P.splat_plain == 0u) {
+      splat(dmask, done, cell, v, v2, P.hist, P.hist_sq, s_hist, s_sq, lane, P.cells);
+      return;
+    }
+  }
+  if (done && v != 0.0f) {
+    DTS_CHECK(cell < P.cells);
+    atomicAdd((s_hist ? s_hist : P.hist) + cell, v);
+    float* sq = s_hist ? s_sq : P.hist_sq;
+    if (sq) atomicAdd(sq + cell, v2);
+  }
 }
 
 #ifndef DTS_MINB
@@ -2375,6 +2400,10 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
   P.fd_cw = fastdiv_make(std::max<uint32_t>(P.cw, 1u));
   P.fd_b = fastdiv_make((uint32_t)d.n_bins);
   P.one_cell_warps = (d.spp_mode == DTS_SPP_PER_CELL && ns >= 32u) ? 1u : 0u;
+  {
+    const char* sp = getenv("DTS_SPLAT_PLAIN");
+    P.splat_plain = (DTS_SPLAT_AGG && sp && sp[0] >= '0' && sp[0] <= '2') ? (uint32_t)(sp[0] - '0') : 2u;
+  }
   P.spp_div_b = (uint32_t)(spp / (uint64_t)d.n_bins);
   P.spp_mod_b = (uint32_t)(spp % (uint64_t)d.n_bins);
   cudaStream_t st = (cudaStream_t)stream;
