@@ -687,9 +687,13 @@ __device__ __forceinline__ void splat_retired(const RenderParams& P, unsigned dm
   }
   if (done && v != 0.0f) {
     DTS_CHECK(cell < P.cells);
-    atomicAdd((s_hist ? s_hist : P.hist) + cell, v);
-    float* sq = s_hist ? s_sq : P.hist_sq;
-    if (sq) atomicAdd(sq + cell, v2);
+    if (s_hist) {  // (one branch per address space: a selected pointer compiles to generic atomics)
+      atomicAdd(s_hist + cell, v);
+      if (s_sq) atomicAdd(s_sq + cell, v2);
+    } else {
+      atomicAdd(P.hist + cell, v);
+      if (P.hist_sq) atomicAdd(P.hist_sq + cell, v2);
+    }
   }
 }
 
