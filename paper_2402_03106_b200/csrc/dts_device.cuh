@@ -734,6 +734,9 @@ __device__ __forceinline__ bool may_connect_bound(const DevScene& S, f3 x, float
 // 16-bit CDF; HG about w), phi = pi (2 u6 - 1) (R12).  GUIDE: the CDF rows are
 // followed by 8-bit guide rows (REUSE kernels stage both); without it the bin
 // is found by an 8-step branchless binary search -- the same bin.
+#ifndef DTS_EDA_PRED
+#define DTS_EDA_PRED 0
+#endif
 struct MixDir {
   f3 om;
   float gamma, p_eda, p_hg, p_mix;
@@ -772,6 +775,9 @@ __device__ __forceinline__ MixDir mix_direction(const DevScene& S, const uint16_
     j = (int)gload<SMEM>(gc, gi);
     int jh = gi == 255u ? 255 : (int)gload<SMEM>(gc, gi + 1);
     DTS_CHECK(gi < 256u && j >= 0 && j < 256 && jh >= 0 && jh < 256);
+#if DTS_EDA_PRED
+    jh = m.eda ? jh : j;  // an HG lane's bin is unused (its p_eda bin is looked up below): it skips the bisection
+#endif
     while (j < jh) {
       const int mid = (j + jh + 1) >> 1;
       DTS_CHECK(mid > 0 && mid < 256);

@@ -43,5 +43,5 @@ if len(sys.argv) > 3:
         t = sum(v for (ff, l), v in thr.items() if ff == f and a <= l <= b)
         print(f"{name:24s} {e / verts:6.2f} warp/vtx  simt {t / max(e, 1):5.1f}")
 print()
-for k, e in agg.most_common(int(40)):
+for k, e in agg.most_common(int(__import__("os").environ.get("NCU_LINES_TOP", "40"))):
     print(f"{k[0]:16s} {k[1]:5d} {e / verts:6.3f} simt {thr[k] / e:5.1f}  {src[k]}")
