@@ -2457,12 +2457,15 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
     // 8: A/B in profiles/ab_r01_refill*.log (configs 6 / 4 +4 % / +2 %, 5 and 3 +0.2 % / +0.4 % vs 16)
     P.refill_k = rk ? (uint32_t)atoi(rk) : 8u;
     if (P.refill_k < 1 || P.refill_k > 4096) P.refill_k = 8u;
-    // warp grabs of kChunk items, but small launches (config 1: 2^18 paths) take
-    // 32 at a time so that every resident warp gets work: about 4 grabs per
-    // resident warp (2048 threads per SM), a multiple of 32 in [32, kChunk]
+    // warp grabs of kChunk items, but small launches take fewer at a time so that
+    // every resident warp gets work (config 1: 2^18 paths) and the tail of a
+    // millisecond render stays short: at least 32 grabs per resident warp (2048
+    // threads per SM), a multiple of 32 in [32, kChunk].  Configs 2 and 6 (2^24 /
+    // 2^23 paths) take 32: +1.2 % / +2.4 % against 128; config 4 (2^26) keeps 128
+    // (32: -0.5 %); profiles/ab_r02zf_knobs.log
     {
       const uint64_t warps = (uint64_t)s->num_sms * 64u;
-      uint64_t c = P.total / (4u * warps);
+      uint64_t c = P.total / (32u * warps);
       c = c < 32u ? 32u : (c > kChunk ? kChunk : c & ~(uint64_t)31u);
       const char* cv = getenv("DTS_GRAB");
       if (cv && atoi(cv) >= 32 && atoi(cv) <= (int)kChunk) c = (uint64_t)atoi(cv) & ~31u;
