@@ -285,6 +285,10 @@ def run_gpu(args):
             "roofline": {
                 "bound": "alu", "achieved": achieved, "peak": peak_tips, "unit": "Tinst/s",
                 "frac": achieved / peak_tips, "frac_measured_peak": achieved / MEASURED_ISSUE_TIPS,
+                # the frozen basis counts two Philox blocks at every vertex; a walk-only SPLIT
+                # vertex draws one since the R24 re-layout: frac on that count
+                "frac_walk_one_philox": achieved / peak_tips * (
+                    1.0 - 51.5 * mix.get("medium_split_walk_only", 0) / max(alg * counts["vertices"], 1.0)),
                 "traffic": traffic,
                 "basis": f"{alg:.1f} algorithmic thread-instructions per vertex: bench/opcounts.json frozen counts "
                          f"x the measured vertex mix {{{', '.join(f'{k}: {v / max(counts['vertices'], 1):.4f}' for k, v in mix.items())}}}"
