@@ -255,8 +255,13 @@ size_t dts_hist_cells(dts_scene_t scene);
  * with per-warp connection queues (default off: the immediate kernels are as
  * fast or faster on every config); DTS_FLUSH_AT (1..32, default 28) is the queue length
  * that triggers a batch; DTS_REFILL_K (default 8) is the idle
- * lane-iterations that trigger a lane refill.  None changes any result
- * beyond fp32 summation order.  DTS_DEFER applies to dts_render only: row-band
+ * lane-iterations that trigger a lane refill; DTS_GRAB (32..128, a multiple of
+ * 32; default 1/32 of the launch per resident warp within that range) is the
+ * number of work items a warp takes from the global counter at a time.  None
+ * changes any result beyond fp32 summation order.  Each path's contribution
+ * reaches its histogram cell by one fp32 RED; builds with
+ * -DDTS_SPLAT_AGG=1 can combine a warp's same-cell contributions first
+ * (DTS_SPLAT_PLAIN=0).  DTS_DEFER applies to dts_render only: row-band
  * launches (dts_render_rows, dts_render_host's bands), which may run
  * concurrently on one scene, always take the immediate kernels.
  * SPLIT scenes (R29) without meshes in BOX or SPHERE media render in two stages

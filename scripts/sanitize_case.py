@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Small renders of every kernel variant for compute-sanitizer runs:
 DARTS (deferred queue, smem table via TMA bulk copy, privatised histogram for
-config 1, warp-aggregated splats), the ablations, RESPONSE mode, vanilla, the
+config 1, plain-RED splats), the ablations, RESPONSE mode, vanilla, the
 global-memory table path, and dts_sample_debug."""
 import os
 import sys
