@@ -266,6 +266,38 @@ def test_render_same_key(dts, oracle, name, mk, spp):
     assert out[0] <= max(2, 0.01 * out[1])
 
 
+# ------------------------------------------------------------------ sweep points
+# The sigma_s and gate-width sweeps of scripts/sweeps.py run
+# the config-3 slab with one time gate at scattering coefficients and gate
+# widths the other parity cases do not visit: same-key parity at the ends of
+# both sweeps (DARTS, and the vanilla baseline the sweeps compare it with).
+SWEEP = [
+    ("sigma_s_2", dict(sigma_s=2.0, t0=6.0, t1=6.1), "darts", 64),
+    ("sigma_s_12", dict(sigma_s=12.0, t0=6.0, t1=6.1), "darts", 64),
+    ("sigma_s_12_vanilla", dict(sigma_s=12.0, t0=6.0, t1=6.1), "vanilla", 512),
+    ("gate_0.025", dict(t0=6.0, t1=6.025), "darts", 64),
+    ("gate_0.8", dict(t0=6.0, t1=6.8), "darts", 64),
+    ("gate_0.8_vanilla", dict(t0=6.0, t1=6.8), "vanilla", 512),
+]
+
+
+@pytest.mark.parametrize("name,kw,strategy,spp", SWEEP, ids=[s[0] for s in SWEEP])
+def test_sweep_points_same_key(dts, oracle, name, kw, strategy, spp):
+    c = I.as_f32(I.crop_center(I.config(3, n_bins=1, spp=spp, strategy=strategy, **kw), 6, 6))
+    g, o, ctr = _same_key(dts, oracle, c, spp, c["seed"])
+    ho = o["hist"]
+    st = o["stats"]
+    assert np.linalg.norm(ho) > 0.0
+    rel = np.linalg.norm(g - ho) / np.linalg.norm(ho)
+    out = _cell_outliers(g, ho)
+    print(f"sweep {name}: same-key relative L2 {rel:.3e}, vertices gpu {ctr['vertices']} oracle {st['vertices']}, "
+          f"cells off by > 1 % {out[0]}/{out[1]}")
+    assert ctr["paths"] == st["paths"]
+    assert abs(ctr["vertices"] - st["vertices"]) <= 0.02 * st["vertices"]
+    assert rel <= SAME_KEY_L2
+    assert out[0] <= max(2, 0.01 * out[1])
+
+
 # ------------------------------------------------------------------ full BASELINE sizes, bench launch config
 FULL = [
     ("cfg3_full_crop", 3, (126, 126, 130, 130)),
