@@ -2635,6 +2635,10 @@ static dts_status render_impl(dts_scene_t s, uint64_t spp, uint64_t seed, uint64
         PW.ho = s->d_ho[slot] + (size_t)h * cap;
         PW.ho_count = wf + 2;
         PW.ho_cap = cap;
+        // a two-stage walk kernel that starts its own paths (no start stage; config 3)
+        // refills at 4 idle lane-iterations: +0.5 % against 8, 1 and 2 even with 8
+        // (profiles/ab_r02zn_refill_walk.log); DTS_REFILL_K overrides
+        if (wave && !kstart3 && !rk) PW.refill_k = 4u;
         RenderParams PC = PW;
         PC.w_base = 0;
         PC.work = wf + 1;
